@@ -1,0 +1,342 @@
+// elementwise.cu — HBM-bound launch units of a partition: RMSNorm fwd/bwd, RoPE fwd/bwd,
+// SwiGLU fwd/bwd, fp32 column sums.
+//
+// These stand in for the reference's memory-bound KernelSpecs ("norm", "rope", "fused_norm";
+// reference pkg/src/schedfront/workloads.py:44-46,60,87), which compose.py:48-76
+// (`group_memory_bound`) treats as single logical launch units.  Roofline: HBM bytes
+// (read + write) / measured copy bandwidth; all loads/stores are 16-byte vectors, one warp per
+// row for the row-reductions so a row is read once from HBM and the second pass hits L1.
+#include "common.cuh"
+
+namespace kpo {
+
+// ===================================================================== RMSNorm forward
+// One warp per row.  Rows of up to 32*8*NV elements are cached in registers (NV uint4 per lane).
+template <int NV>
+__global__ void __launch_bounds__(256) rmsnorm_fwd_cached(const __nv_bfloat16* __restrict__ x,
+                                                          const __nv_bfloat16* __restrict__ w,
+                                                          __nv_bfloat16* __restrict__ y,
+                                                          float* __restrict__ rstd, int64_t rows,
+                                                          int cols, float eps) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + row * cols);
+  uint4 v[NV];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    v[i] = ld_nc_v4(xr + lane + 32 * i);
+    float f[8];
+    unpack8(v[i], f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) ss += f[j] * f[j];
+  }
+  ss = warp_sum(ss);
+  const float r = rsqrtf(ss / (float)cols + eps);
+  if (lane == 0 && rstd) rstd[row] = r;
+  const uint4* wr = reinterpret_cast<const uint4*>(w);
+  uint4* yr = reinterpret_cast<uint4*>(y + row * cols);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    float f[8], g[8];
+    unpack8(v[i], f);
+    unpack8(wr[lane + 32 * i], g);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[j] = f[j] * r * g[j];
+    yr[lane + 32 * i] = pack8(f);
+  }
+}
+
+// Generic fallback: two passes over the row (second pass served by L1/L2).
+__global__ void __launch_bounds__(256) rmsnorm_fwd_generic(const __nv_bfloat16* __restrict__ x,
+                                                           const __nv_bfloat16* __restrict__ w,
+                                                           __nv_bfloat16* __restrict__ y,
+                                                           float* __restrict__ rstd, int64_t rows,
+                                                           int cols, float eps) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + row * cols);
+  const int nv = cols / 8;
+  float ss = 0.f;
+  for (int i = lane; i < nv; i += 32) {
+    float f[8];
+    unpack8(xr[i], f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) ss += f[j] * f[j];
+  }
+  ss = warp_sum(ss);
+  const float r = rsqrtf(ss / (float)cols + eps);
+  if (lane == 0 && rstd) rstd[row] = r;
+  const uint4* wr = reinterpret_cast<const uint4*>(w);
+  uint4* yr = reinterpret_cast<uint4*>(y + row * cols);
+  for (int i = lane; i < nv; i += 32) {
+    float f[8], g[8];
+    unpack8(xr[i], f);
+    unpack8(wr[i], g);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[j] = f[j] * r * g[j];
+    yr[i] = pack8(f);
+  }
+}
+
+// ===================================================================== RMSNorm backward
+// dx_i = r*w_i*dy_i - x_i * r^3/n * sum_j(w_j*dy_j*x_j)  (+ dres_i)
+// dw_j partial per CTA: sum over the CTA's rows of dy_j*x_j*r, written as fp32 [blocks, cols].
+constexpr int kNormBwdRowsPerBlock = 64;
+constexpr int kNormBwdWarps = 8;
+
+__global__ void __launch_bounds__(kNormBwdWarps * 32)
+    rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+                       const __nv_bfloat16* __restrict__ w, const float* __restrict__ rstd,
+                       const __nv_bfloat16* __restrict__ dres, __nv_bfloat16* __restrict__ dx,
+                       float* __restrict__ dw_partial, int64_t rows, int cols) {
+  extern __shared__ float dw_smem[];  // [cols] accumulated across warps
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nv = cols / 8;
+  for (int i = threadIdx.x; i < cols; i += blockDim.x) dw_smem[i] = 0.f;
+  __syncthreads();
+  const uint4* wr = reinterpret_cast<const uint4*>(w);
+  const int64_t row0 = (int64_t)blockIdx.x * kNormBwdRowsPerBlock;
+  for (int rr = warp; rr < kNormBwdRowsPerBlock; rr += kNormBwdWarps) {
+    const int64_t row = row0 + rr;
+    if (row >= rows) break;
+    const uint4* xr = reinterpret_cast<const uint4*>(x + row * cols);
+    const uint4* dyr = reinterpret_cast<const uint4*>(dy + row * cols);
+    const float r = rstd[row];
+    float dot = 0.f;
+    for (int i = lane; i < nv; i += 32) {
+      float a[8], b[8], g[8];
+      unpack8(xr[i], a);
+      unpack8(dyr[i], b);
+      unpack8(wr[i], g);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) dot += g[j] * b[j] * a[j];
+    }
+    dot = warp_sum(dot);
+    const float c = dot * r * r * r / (float)cols;
+    uint4* dxr = reinterpret_cast<uint4*>(dx + row * cols);
+    const uint4* dresr = dres ? reinterpret_cast<const uint4*>(dres + row * cols) : nullptr;
+    for (int i = lane; i < nv; i += 32) {
+      float a[8], b[8], g[8], o[8];
+      unpack8(xr[i], a);
+      unpack8(dyr[i], b);
+      unpack8(wr[i], g);
+      float res[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      if (dresr) unpack8(dresr[i], res);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        o[j] = r * g[j] * b[j] - a[j] * c + res[j];
+        atomicAdd(&dw_smem[i * 8 + j], b[j] * a[j] * r);
+      }
+      dxr[i] = pack8(o);
+    }
+  }
+  __syncthreads();
+  float* out = dw_partial + (int64_t)blockIdx.x * cols;
+  for (int i = threadIdx.x; i < cols; i += blockDim.x) out[i] = dw_smem[i];
+}
+
+// out[c] = sum_r in[r, c]; one thread per column, coalesced across the warp.
+__global__ void colsum_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
+                              int64_t rows, int64_t cols) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  float s = 0.f;
+  for (int64_t r = 0; r < rows; ++r) s += in[r * cols + c];
+  out[c] = f2bf(s);
+}
+
+// ===================================================================== RoPE
+// One CTA per token; the token's cos/sin table (head_dim/2 entries) is built once in smem and
+// reused by every head.  Each thread rotates 8 consecutive pairs of one head.
+__global__ void rope_kernel(const __nv_bfloat16* __restrict__ in, int64_t in_stride,
+                            __nv_bfloat16* __restrict__ out, int64_t out_stride, int heads,
+                            int head_dim, float log2_theta, int64_t pos0, int inverse) {
+  extern __shared__ float cs[];  // [half] cos, [half] sin
+  const int half = head_dim / 2;
+  const int64_t t = blockIdx.x;
+  const float pos = (float)(pos0 + t);
+  for (int i = threadIdx.x; i < half; i += blockDim.x) {
+    const float inv_freq = exp2f(-(2.0f * (float)i / (float)head_dim) * log2_theta);
+    float s, c;
+    sincosf(pos * inv_freq, &s, &c);
+    cs[i] = c;
+    cs[half + i] = inverse ? -s : s;
+  }
+  __syncthreads();
+  const int chunks = half / 8;  // 8-pair chunks per head
+  const __nv_bfloat16* src = in + t * in_stride;
+  __nv_bfloat16* dst = out + t * out_stride;
+  for (int job = threadIdx.x; job < heads * chunks; job += blockDim.x) {
+    const int h = job / chunks, ch = job % chunks;
+    const int i0 = ch * 8;
+    const __nv_bfloat16* hp = src + (int64_t)h * head_dim;
+    float a[8], b[8], oa[8], ob[8];
+    unpack8(*reinterpret_cast<const uint4*>(hp + i0), a);
+    unpack8(*reinterpret_cast<const uint4*>(hp + half + i0), b);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float c = cs[i0 + j], s = cs[half + i0 + j];
+      oa[j] = a[j] * c - b[j] * s;
+      ob[j] = b[j] * c + a[j] * s;
+    }
+    __nv_bfloat16* op = dst + (int64_t)h * head_dim;
+    *reinterpret_cast<uint4*>(op + i0) = pack8(oa);
+    *reinterpret_cast<uint4*>(op + half + i0) = pack8(ob);
+  }
+}
+
+// ===================================================================== SwiGLU
+__device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + __expf(-x)); }
+
+__global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ act,
+                                  int64_t rows, int64_t ffn) {
+  const int64_t nvr = ffn / 8;
+  const int64_t total = rows * nvr;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx / nvr, c = idx % nvr;
+    const __nv_bfloat16* row = gu + r * 2 * ffn;
+    float g[8], u[8], o[8];
+    unpack8(ld_nc_v4(row + c * 8), g);
+    unpack8(ld_nc_v4(row + ffn + c * 8), u);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = g[j] * sigmoidf_(g[j]) * u[j];
+    *reinterpret_cast<uint4*>(act + r * ffn + c * 8) = pack8(o);
+  }
+}
+
+__global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ dact, const __nv_bfloat16* __restrict__ gu,
+                                  __nv_bfloat16* __restrict__ dgu, int64_t rows, int64_t ffn) {
+  const int64_t nvr = ffn / 8;
+  const int64_t total = rows * nvr;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = idx / nvr, c = idx % nvr;
+    const __nv_bfloat16* row = gu + r * 2 * ffn;
+    float g[8], u[8], d[8], dg[8], du[8];
+    unpack8(ld_nc_v4(row + c * 8), g);
+    unpack8(ld_nc_v4(row + ffn + c * 8), u);
+    unpack8(ld_nc_v4(dact + r * ffn + c * 8), d);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float s = sigmoidf_(g[j]);
+      const float silu = g[j] * s;
+      du[j] = d[j] * silu;
+      dg[j] = d[j] * u[j] * s * (1.f + g[j] * (1.f - s));
+    }
+    __nv_bfloat16* orow = dgu + r * 2 * ffn;
+    *reinterpret_cast<uint4*>(orow + c * 8) = pack8(dg);
+    *reinterpret_cast<uint4*>(orow + ffn + c * 8) = pack8(du);
+  }
+}
+
+static int elem_grid(int64_t work, int threads) {
+  const int64_t want = (work + threads - 1) / threads;
+  const int64_t cap = (int64_t)num_sms() * 16;
+  return (int)(want < cap ? (want > 0 ? want : 1) : cap);
+}
+
+}  // namespace kpo
+
+using namespace kpo;
+
+static inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+extern "C" int kpo_rmsnorm_fwd(const void* x, const void* w, void* y, float* rstd, int64_t rows,
+                               int64_t cols, float eps, void* stream) {
+  KPO_CHECK_ARG(x && w && y, "rmsnorm_fwd: null pointer");
+  KPO_CHECK_ARG(rows >= 0 && cols > 0 && cols % 8 == 0, "rmsnorm_fwd: cols must be a positive multiple of 8");
+  KPO_CHECK_ARG(aligned16(x) && aligned16(w) && aligned16(y), "rmsnorm_fwd: pointers must be 16B aligned");
+  if (rows == 0) return KPO_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int warps = 8;
+  const dim3 grid((unsigned)((rows + warps - 1) / warps)), block(warps * 32);
+  auto X = (const __nv_bfloat16*)x;
+  auto W = (const __nv_bfloat16*)w;
+  auto Y = (__nv_bfloat16*)y;
+  if (cols % 256 == 0 && cols / 256 <= 16) {
+    switch (cols / 256) {
+#define KPO_NORM_CASE(n) \
+  case n: rmsnorm_fwd_cached<n><<<grid, block, 0, s>>>(X, W, Y, rstd, rows, (int)cols, eps); break;
+      KPO_NORM_CASE(1) KPO_NORM_CASE(2) KPO_NORM_CASE(3) KPO_NORM_CASE(4) KPO_NORM_CASE(5)
+      KPO_NORM_CASE(6) KPO_NORM_CASE(8) KPO_NORM_CASE(10) KPO_NORM_CASE(12) KPO_NORM_CASE(16)
+#undef KPO_NORM_CASE
+      default: rmsnorm_fwd_generic<<<grid, block, 0, s>>>(X, W, Y, rstd, rows, (int)cols, eps);
+    }
+  } else {
+    rmsnorm_fwd_generic<<<grid, block, 0, s>>>(X, W, Y, rstd, rows, (int)cols, eps);
+  }
+  KPO_LAUNCH_CHECK();
+  return KPO_OK;
+}
+
+extern "C" int kpo_rmsnorm_bwd_partial_rows(int64_t rows, int64_t cols, int64_t* n_partials) {
+  KPO_CHECK_ARG(n_partials, "null n_partials");
+  (void)cols;
+  *n_partials = (rows + kNormBwdRowsPerBlock - 1) / kNormBwdRowsPerBlock;
+  return KPO_OK;
+}
+
+extern "C" int kpo_rmsnorm_bwd(const void* dy, const void* x, const void* w, const float* rstd,
+                               const void* dres, void* dx, float* dw_partial, int64_t rows, int64_t cols,
+                               void* stream) {
+  KPO_CHECK_ARG(dy && x && w && rstd && dx && dw_partial, "rmsnorm_bwd: null pointer");
+  KPO_CHECK_ARG(cols > 0 && cols % 8 == 0 && cols * 4 <= 200 * 1024, "rmsnorm_bwd: bad cols");
+  if (rows == 0) return KPO_OK;
+  const unsigned blocks = (unsigned)((rows + kNormBwdRowsPerBlock - 1) / kNormBwdRowsPerBlock);
+  const size_t smem = (size_t)cols * sizeof(float);
+  if (smem > 48 * 1024)
+    KPO_CUDA(cudaFuncSetAttribute(rmsnorm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  rmsnorm_bwd_kernel<<<blocks, kNormBwdWarps * 32, smem, (cudaStream_t)stream>>>(
+      (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const __nv_bfloat16*)w, rstd,
+      (const __nv_bfloat16*)dres, (__nv_bfloat16*)dx, dw_partial, rows, (int)cols);
+  KPO_LAUNCH_CHECK();
+  return KPO_OK;
+}
+
+extern "C" int kpo_colsum_f32_to_bf16(const float* in, void* out, int64_t rows, int64_t cols, void* stream) {
+  KPO_CHECK_ARG(in && out && rows >= 0 && cols > 0, "colsum: bad args");
+  colsum_kernel<<<(unsigned)((cols + 255) / 256), 256, 0, (cudaStream_t)stream>>>(in, (__nv_bfloat16*)out,
+                                                                                rows, cols);
+  KPO_LAUNCH_CHECK();
+  return KPO_OK;
+}
+
+extern "C" int kpo_rope(const void* in, int64_t in_row_stride, void* out, int64_t out_row_stride,
+                        int64_t tokens, int heads, int head_dim, float theta, int64_t pos0, int inverse,
+                        void* stream) {
+  KPO_CHECK_ARG(in && out, "rope: null pointer");
+  KPO_CHECK_ARG(head_dim % 16 == 0 && head_dim <= 512, "rope: head_dim must be a multiple of 16");
+  KPO_CHECK_ARG(in_row_stride % 8 == 0 && out_row_stride % 8 == 0 && aligned16(in) && aligned16(out),
+                "rope: strides/pointers must be 16B aligned");
+  KPO_CHECK_ARG(theta > 1.f, "rope: theta must be > 1");
+  if (tokens == 0) return KPO_OK;
+  const int threads = 256;
+  rope_kernel<<<(unsigned)tokens, threads, head_dim * sizeof(float), (cudaStream_t)stream>>>(
+      (const __nv_bfloat16*)in, in_row_stride, (__nv_bfloat16*)out, out_row_stride, heads, head_dim,
+      log2f(theta), pos0, inverse);
+  KPO_LAUNCH_CHECK();
+  return KPO_OK;
+}
+
+extern "C" int kpo_swiglu_fwd(const void* gu, void* act, int64_t rows, int64_t ffn, void* stream) {
+  KPO_CHECK_ARG(gu && act && ffn % 8 == 0 && aligned16(gu) && aligned16(act), "swiglu_fwd: bad args");
+  if (rows == 0) return KPO_OK;
+  swiglu_fwd_kernel<<<elem_grid(rows * ffn / 8, 256), 256, 0, (cudaStream_t)stream>>>(
+      (const __nv_bfloat16*)gu, (__nv_bfloat16*)act, rows, ffn);
+  KPO_LAUNCH_CHECK();
+  return KPO_OK;
+}
+
+extern "C" int kpo_swiglu_bwd(const void* dact, const void* gu, void* dgu, int64_t rows, int64_t ffn,
+                              void* stream) {
+  KPO_CHECK_ARG(dact && gu && dgu && ffn % 8 == 0, "swiglu_bwd: bad args");
+  if (rows == 0) return KPO_OK;
+  swiglu_bwd_kernel<<<elem_grid(rows * ffn / 8, 256), 256, 0, (cudaStream_t)stream>>>(
+      (const __nv_bfloat16*)dact, (const __nv_bfloat16*)gu, (__nv_bfloat16*)dgu, rows, ffn);
+  KPO_LAUNCH_CHECK();
+  return KPO_OK;
+}

@@ -1,0 +1,430 @@
+// gemm_sm100.cu — warp-specialized tcgen05 GEMM for sm_100a (bf16 in, fp32 accumulate in TMEM).
+//
+// Replaces the reference's abstract compute-bound kernels ("linear_qkv", "linear_proj",
+// "linear_up", "linear_down", "linear"; reference workloads.py:45,48,61-62,73) whose cost the
+// simulator models as flops / (SMs * peak_flops_per_sm_mhz * f)  (simgpu.py:77-79,166).
+//
+// Design (B200-first):
+//   * one CTA per SM (smem > half the SM), 6 warps: warp0 = tile scheduler + TMA producer,
+//     warp1 = TMEM allocator + single-thread tcgen05.mma issuer, warps 2-5 = epilogue
+//     (tcgen05.ld TMEM -> registers -> bf16 -> global, optional fused residual add);
+//   * operands staged by TMA (cp.async.bulk.tensor, 128B swizzle) into a STAGES-deep
+//     smem ring guarded by mbarriers; accumulators double-buffered in TMEM so the epilogue of
+//     tile i overlaps the main loop of tile i+1;
+//   * K-major or MN-major A/B (forward = TN, dgrad = NN, wgrad = TT) selected by template,
+//     expressed only in the TMA boxes and the UMMA smem/instruction descriptors;
+//   * dynamic persistent tile scheduler: grid = min(tiles, max_ctas) CTAs fetch tiles from a
+//     global atomic counter.  CTAs that cannot become resident while the SM-budgeted collective
+//     owns its SMs launch when those SMs free up and steal the remaining tiles — this is the
+//     hardware analogue of the simulator handing all SMs back once communication ends
+//     (simgpu.py:221).  The last CTA to finish resets the counter (graph-replay safe).
+#include "common.cuh"
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+namespace kpo {
+namespace gemm {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kThreads = 192;
+constexpr int GROUP_M = 16;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+// UMMA shared-memory descriptor, SWIZZLE_128B, sm_100 version bit.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (Blackwell)
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// 32 lanes x 32 columns of fp32 from TMEM.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+template <int BN>
+struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (BN == 256) ? 4 : 6;
+  static constexpr int TMEM_COLS = 2 * BN;  // double-buffered accumulator (power of two)
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;  // + barriers + alignment slack
+};
+
+__device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
+  const int per_group = GROUP_M * num_n;
+  const int g = t / per_group;
+  const int first_m = g * GROUP_M;
+  const int gsize = min(num_m - first_m, GROUP_M);
+  const int r = t % per_group;
+  mb = first_m + r % gsize;
+  nb = r / gsize;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                __nv_bfloat16* __restrict__ D, const __nv_bfloat16* __restrict__ C, int M, int N, int K,
+                int64_t ldd, int* __restrict__ sched) {
+  using CF = Cfg<BN>;
+  constexpr int STAGES = CF::STAGES;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + CF::BAR_OFF);
+  // barrier layout
+  uint64_t* full = bars;                  // [STAGES]
+  uint64_t* empty = bars + STAGES;        // [STAGES]
+  uint64_t* tfull = bars + 2 * STAGES;    // [2]
+  uint64_t* tempty = tfull + 2;           // [2]
+  uint64_t* sfull = tempty + 2;           // [2]
+  uint64_t* sempty = sfull + 2;           // [2]
+  int* stile = reinterpret_cast<int*>(sempty + 2);        // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stile + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
+  const int num_tiles = num_m * num_n;
+  const int num_kb = (K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&tfull[i]), 1);
+      mbar_init(smem_u32(&tempty[i]), 4);
+      mbar_init(smem_u32(&sfull[i]), 1);
+      mbar_init(smem_u32(&sempty[i]), 5);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(CF::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===================== tile scheduler + TMA producer
+      int it = 0, stage = 0;
+      uint32_t phase = 0;
+      while (true) {
+        const int tile = atomicAdd(&sched[0], 1);
+        const int slot = it & 1;
+        mbar_wait(smem_u32(&sempty[slot]), ((it >> 1) & 1) ^ 1);
+        stile[slot] = tile;
+        mbar_arrive(smem_u32(&sfull[slot]));
+        ++it;
+        if (tile >= num_tiles) break;
+        int mb, nb;
+        tile_coords(tile, num_m, num_n, mb, nb);
+        const int m0 = mb * BM, n0 = nb * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+          const uint32_t fb = smem_u32(&full[stage]);
+          mbar_arrive_expect_tx(fb, CF::STAGE_BYTES);
+          const uint32_t sa = smem_u32(smem + stage * CF::STAGE_BYTES);
+          const uint32_t sb = sa + CF::A_BYTES;
+          const int k0 = kb * BK;
+          if (!A_MN) {
+            tma_load_2d(sa, &tmA, fb, k0, m0);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BM / 64; ++c) tma_load_2d(sa + c * (BK * 128), &tmA, fb, m0 + c * 64, k0);
+          }
+          if (!B_MN) {
+            tma_load_2d(sb, &tmB, fb, k0, n0);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BN / 64; ++c) tma_load_2d(sb + c * (BK * 128), &tmB, fb, n0 + c * 64, k0);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+      // the last CTA out resets the scheduler word for the next launch (graph-replay safe)
+      __threadfence();
+      const int done = atomicAdd(&sched[1], 1);
+      if (done == (int)gridDim.x - 1) {
+        sched[0] = 0;
+        sched[1] = 0;
+        __threadfence();
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ===================== MMA issuer (single thread)
+      constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)A_MN << 15) |
+                                 ((uint32_t)B_MN << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+      // K-major SW128: SBO = 8 rows * 128B; MN-major SW128: LBO = MN-chunk stride, SBO = 8 K-rows.
+      constexpr uint32_t A_LBO = A_MN ? BK * 128 : 16, A_SBO = 1024;
+      constexpr uint32_t B_LBO = B_MN ? BK * 128 : 16, B_SBO = 1024;
+      constexpr uint32_t A_KSTEP = A_MN ? 16 * 128 : 32;  // bytes per UMMA_K=16 step
+      constexpr uint32_t B_KSTEP = B_MN ? 16 * 128 : 32;
+      int it = 0, stage = 0, acc_it = 0;
+      uint32_t phase = 0;
+      while (true) {
+        const int slot = it & 1;
+        mbar_wait(smem_u32(&sfull[slot]), (it >> 1) & 1);
+        const int tile = stile[slot];
+        mbar_arrive(smem_u32(&sempty[slot]));
+        ++it;
+        if (tile >= num_tiles) break;
+        const int acc = acc_it & 1;
+        mbar_wait(smem_u32(&tempty[acc]), ((acc_it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(smem_u32(&full[stage]), phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * CF::STAGE_BYTES);
+          const uint32_t sb = sa + CF::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t da = smem_desc(sa + k * A_KSTEP, A_LBO, A_SBO);
+            const uint64_t db = smem_desc(sb + k * B_KSTEP, B_LBO, B_SBO);
+            tc_mma(d_tmem, da, db, IDESC, (kb | k) != 0);
+          }
+          tc_commit(smem_u32(&empty[stage]));
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit(smem_u32(&tfull[acc]));
+        ++acc_it;
+      }
+    }
+  } else {
+    // ===================== epilogue warps 2..5: TMEM lanes 32*(warp%4) .. +31
+    const int q = warp & 3;
+    int it = 0, acc_it = 0;
+    while (true) {
+      const int slot = it & 1;
+      mbar_wait(smem_u32(&sfull[slot]), (it >> 1) & 1);
+      const int tile = stile[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&sempty[slot]));
+      ++it;
+      if (tile >= num_tiles) break;
+      int mb, nb;
+      tile_coords(tile, num_m, num_n, mb, nb);
+      const int acc = acc_it & 1;
+      mbar_wait(smem_u32(&tfull[acc]), (acc_it >> 1) & 1);
+      tc_fence_after();
+      const int row = mb * BM + q * 32 + lane;
+      const bool row_ok = row < M;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
+        const int col0 = nb * BN + c * 32;
+        if (row_ok) {
+          __nv_bfloat16* drow = D + (int64_t)row * ldd;
+          const __nv_bfloat16* crow = C ? C + (int64_t)row * ldd : nullptr;
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int col = col0 + v * 8;
+            if (col < N) {
+              float f[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) f[j] = __uint_as_float(r[v * 8 + j]);
+              if (crow) {
+                float cf[8];
+                unpack8(*reinterpret_cast<const uint4*>(crow + col), cf);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) f[j] += cf[j];
+              }
+              *reinterpret_cast<uint4*>(drow + col) = pack8(f);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&tempty[acc]));
+      ++acc_it;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(CF::TMEM_COLS));
+  }
+}
+
+// ------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor map: inner (contiguous) extent, outer extent, outer stride (elements), box.
+static int make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t stride_elems,
+                    uint32_t box_inner, uint32_t box_outer) {
+  auto enc = get_encode();
+  if (!enc) {
+    set_error("gemm: cuTensorMapEncodeTiled unavailable");
+    return KPO_ERR_UNSUPPORTED;
+  }
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {stride_elems * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("gemm: cuTensorMapEncodeTiled failed (%d) inner=%llu outer=%llu stride=%llu", (int)r,
+              (unsigned long long)inner, (unsigned long long)outer, (unsigned long long)stride_elems);
+    return KPO_ERR_INVALID;
+  }
+  return KPO_OK;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+static int launch(const CUtensorMap& ta, const CUtensorMap& tb, void* D, const void* C, int64_t M, int64_t N,
+                  int64_t K, int64_t ldd, int grid, int* sched, cudaStream_t s) {
+  auto kern = gemm_kernel<BN, A_MN, B_MN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    KPO_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
+    attr_set = true;
+  }
+  kern<<<grid, kThreads, Cfg<BN>::SMEM, s>>>(ta, tb, (__nv_bfloat16*)D, (const __nv_bfloat16*)C, (int)M, (int)N,
+                                              (int)K, ldd, sched);
+  KPO_LAUNCH_CHECK();
+  return KPO_OK;
+}
+
+}  // namespace gemm
+}  // namespace kpo
+
+using namespace kpo;
+
+extern "C" int kpo_gemm(const void* A, const void* B, void* D, const void* C, int64_t M, int64_t N, int64_t K,
+                        int a_mn_major, int b_mn_major, int64_t lda, int64_t ldb, int64_t ldd, int max_ctas,
+                        int* sched, void* stream) {
+  using namespace kpo::gemm;
+  KPO_CHECK_ARG(A && B && D && sched, "gemm: null pointer");
+  KPO_CHECK_ARG(M > 0 && N > 0 && K > 0, "gemm: M, N, K must be positive");
+  KPO_CHECK_ARG(M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31), "gemm: dims too large");
+  KPO_CHECK_ARG(N % 8 == 0 && K % 8 == 0 && ldd % 8 == 0 && lda % 8 == 0 && ldb % 8 == 0,
+                "gemm: N, K and leading dimensions must be multiples of 8");
+  KPO_CHECK_ARG(((uintptr_t)A & 15) == 0 && ((uintptr_t)B & 15) == 0 && ((uintptr_t)D & 15) == 0 &&
+                    ((uintptr_t)C & 15) == 0,
+                "gemm: pointers must be 16B aligned");
+  KPO_CHECK_ARG(ldd >= N, "gemm: ldd < N");
+  KPO_CHECK_ARG(a_mn_major ? lda >= M : lda >= K, "gemm: lda too small");
+  KPO_CHECK_ARG(b_mn_major ? ldb >= N : ldb >= K, "gemm: ldb too small");
+  const int sms = num_sms();
+  // tile width: best SM-wave efficiency, ties -> 256
+  auto eff = [&](int bn) {
+    const int64_t tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
+    const int64_t waves = (tiles + sms - 1) / sms;
+    return (double)tiles / (double)(waves * sms) * (double)(bn == 256 ? 1.0 : 0.93);
+  };
+  const int bn = eff(256) >= eff(128) ? 256 : 128;
+  const int64_t tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
+  int cap = max_ctas > 0 ? max_ctas : sms;
+  if (cap > sms) cap = sms;
+  const int grid = (int)(tiles < cap ? tiles : cap);
+
+  CUtensorMap ta, tb;
+  int st;
+  if (!a_mn_major) st = make_map(&ta, A, K, M, lda, BK, BM);
+  else st = make_map(&ta, A, M, K, lda, 64, BK);
+  if (st) return st;
+  if (!b_mn_major) st = make_map(&tb, B, K, N, ldb, BK, bn);
+  else st = make_map(&tb, B, N, K, ldb, 64, BK);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+#define KPO_GEMM_DISPATCH(BNv)                                                                      \
+  if (!a_mn_major && !b_mn_major) return launch<BNv, false, false>(ta, tb, D, C, M, N, K, ldd, grid, sched, s); \
+  if (!a_mn_major && b_mn_major) return launch<BNv, false, true>(ta, tb, D, C, M, N, K, ldd, grid, sched, s);   \
+  if (a_mn_major && !b_mn_major) return launch<BNv, true, false>(ta, tb, D, C, M, N, K, ldd, grid, sched, s);   \
+  return launch<BNv, true, true>(ta, tb, D, C, M, N, K, ldd, grid, sched, s);
+  if (bn == 256) {
+    KPO_GEMM_DISPATCH(256)
+  } else {
+    KPO_GEMM_DISPATCH(128)
+  }
+#undef KPO_GEMM_DISPATCH
+}

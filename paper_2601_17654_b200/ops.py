@@ -1,0 +1,163 @@
+"""Thin torch-tensor front end over libkpo.so.
+
+PyTorch only owns memory and streams here; every op below is one or more hand-written sm_100a
+kernels reached through the C ABI (include/kpo.h).  There is no eager/PyTorch fallback: a CPU
+tensor or a missing library raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+
+BF16 = torch.bfloat16
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream: torch.cuda.Stream | None = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _need_cuda(*ts: torch.Tensor | None) -> None:
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("kpo ops take CUDA tensors only (no CPU fallback)")
+
+
+# ------------------------------------------------------------------ RMSNorm
+def rmsnorm_fwd(x: torch.Tensor, w: torch.Tensor, y: torch.Tensor, rstd: torch.Tensor, eps: float = 1e-5,
+                stream=None) -> None:
+    _need_cuda(x, w, y, rstd)
+    rows, cols = x.shape
+    _lib.call("kpo_rmsnorm_fwd", _ptr(x), _ptr(w), _ptr(y), _ptr(rstd), rows, cols, ctypes.c_float(eps),
+              _stream(stream))
+
+
+def rmsnorm_partials(rows: int, cols: int) -> int:
+    n = ctypes.c_int64(0)
+    _lib.call("kpo_rmsnorm_bwd_partial_rows", rows, cols, ctypes.byref(n))
+    return n.value
+
+
+def rmsnorm_bwd(dy, x, w, rstd, dx, dw_partial, dres=None, stream=None) -> None:
+    _need_cuda(dy, x, w, rstd, dx, dw_partial, dres)
+    rows, cols = x.shape
+    _lib.call("kpo_rmsnorm_bwd", _ptr(dy), _ptr(x), _ptr(w), _ptr(rstd), _ptr(dres), _ptr(dx), _ptr(dw_partial),
+              rows, cols, _stream(stream))
+
+
+def colsum(partial: torch.Tensor, out: torch.Tensor, stream=None) -> None:
+    _need_cuda(partial, out)
+    rows, cols = partial.shape
+    _lib.call("kpo_colsum_f32_to_bf16", _ptr(partial), _ptr(out), rows, cols, _stream(stream))
+
+
+# ------------------------------------------------------------------ RoPE / SwiGLU
+def rope(inp: torch.Tensor, out: torch.Tensor, heads: int, head_dim: int, theta: float, pos0: int = 0,
+         inverse: bool = False, stream=None) -> None:
+    """inp/out: 2-D views [tokens, >= heads*head_dim] (row strides may differ)."""
+    _need_cuda(inp, out)
+    tokens = inp.shape[0]
+    _lib.call("kpo_rope", _ptr(inp), inp.stride(0), _ptr(out), out.stride(0), tokens, heads, head_dim,
+              ctypes.c_float(theta), pos0, int(inverse), _stream(stream))
+
+
+def swiglu_fwd(gu: torch.Tensor, act: torch.Tensor, stream=None) -> None:
+    _need_cuda(gu, act)
+    rows, ffn = act.shape
+    _lib.call("kpo_swiglu_fwd", _ptr(gu), _ptr(act), rows, ffn, _stream(stream))
+
+
+def swiglu_bwd(dact: torch.Tensor, gu: torch.Tensor, dgu: torch.Tensor, stream=None) -> None:
+    _need_cuda(dact, gu, dgu)
+    rows, ffn = dact.shape
+    _lib.call("kpo_swiglu_bwd", _ptr(dact), _ptr(gu), _ptr(dgu), rows, ffn, _stream(stream))
+
+
+# ------------------------------------------------------------------ GEMM
+class GemmScheduler:
+    """Device-resident tile-scheduler words (int32[2] per concurrently running GEMM)."""
+
+    def __init__(self, device, slots: int = 64):
+        self.buf = torch.zeros(slots * 2, dtype=torch.int32, device=device)
+        self.slots = slots
+        self._next = 0
+
+    def slot(self) -> int:
+        i = self._next % self.slots
+        self._next += 1
+        return self.buf.data_ptr() + 8 * i
+
+
+_default_sched: dict[int, GemmScheduler] = {}
+
+
+def default_sched(device) -> int:
+    idx = torch.device(device).index or 0
+    if idx not in _default_sched:
+        _default_sched[idx] = GemmScheduler(torch.device("cuda", idx), slots=1)
+    return _default_sched[idx].buf.data_ptr()
+
+
+def gemm_raw(A: torch.Tensor, B: torch.Tensor, D: torch.Tensor, M: int, N: int, K: int, a_mn: bool, b_mn: bool,
+             C: torch.Tensor | None = None, max_ctas: int = 0, sched: int | None = None, stream=None) -> None:
+    _need_cuda(A, B, D, C)
+    lda, ldb, ldd = A.stride(0), B.stride(0), D.stride(0)
+    if sched is None:
+        sched = default_sched(A.device)
+    _lib.call("kpo_gemm", _ptr(A), _ptr(B), _ptr(D), _ptr(C), M, N, K, int(a_mn), int(b_mn), lda, ldb, ldd,
+              max_ctas, sched, _stream(stream))
+
+
+def linear(x: torch.Tensor, w: torch.Tensor, out: torch.Tensor, residual: torch.Tensor | None = None,
+           **kw) -> None:
+    """out[M,N] = x[M,K] @ w[N,K]^T (+ residual) — forward (TN)."""
+    M, K = x.shape
+    N = w.shape[0]
+    gemm_raw(x, w, out, M, N, K, False, False, C=residual, **kw)
+
+
+def linear_dgrad(dy: torch.Tensor, w: torch.Tensor, dx: torch.Tensor, accumulate: torch.Tensor | None = None,
+                 **kw) -> None:
+    """dx[M,K] = dy[M,N] @ w[N,K]  (B is MN-major: w rows are the reduction dim)."""
+    M, N = dy.shape
+    K = w.shape[1]
+    gemm_raw(dy, w, dx, M, K, N, False, True, C=accumulate, **kw)
+
+
+def linear_wgrad(dy: torch.Tensor, x: torch.Tensor, dw: torch.Tensor, accumulate: torch.Tensor | None = None,
+                 **kw) -> None:
+    """dw[N,K] = dy[M,N]^T @ x[M,K]  (both operands MN-major: reduction over tokens)."""
+    M, N = dy.shape
+    K = x.shape[1]
+    gemm_raw(dy, x, dw, N, K, M, True, True, C=accumulate, **kw)
+
+
+# ------------------------------------------------------------------ attention
+def attn_fwd(q, k, v, o, lse, T: int, hq: int, hkv: int, d: int, scale: float, causal: bool = True,
+             stream=None) -> None:
+    """q/k/v/o: 2-D token-major views ([T, >=heads*d], any row stride); lse: fp32 [hq, T]."""
+    _need_cuda(q, k, v, o, lse)
+    _lib.call("kpo_attn_fwd", _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), T, hq, hkv, d, q.stride(0),
+              k.stride(0), v.stride(0), o.stride(0), ctypes.c_float(scale), int(causal), _stream(stream))
+
+
+def attn_bwd_workspace(T: int, hq: int, hkv: int, d: int, device) -> torch.Tensor:
+    n = _lib.lib().kpo_attn_bwd_workspace_bytes(T, hq, hkv, d)
+    return torch.empty(n, dtype=torch.uint8, device=device)
+
+
+def attn_bwd(q, k, v, o, dout, lse, dq, dk, dv, T, hq, hkv, d, scale, workspace, causal=True, stream=None):
+    _need_cuda(q, k, v, o, dout, lse, dq, dk, dv, workspace)
+    if dout.stride(0) != o.stride(0):
+        raise ValueError("attn_bwd: dout must share o's token stride")
+    _lib.call("kpo_attn_bwd", _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(dout), _ptr(lse), _ptr(dq), _ptr(dk),
+              _ptr(dv), T, hq, hkv, d, q.stride(0), k.stride(0), v.stride(0), o.stride(0), dq.stride(0),
+              dk.stride(0), dv.stride(0), ctypes.c_float(scale), int(causal), _ptr(workspace), _stream(stream))

@@ -1,0 +1,160 @@
+"""Numerics of the hand-written sm_100a kernels against plain PyTorch fp32 references."""
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_err(a, b):
+    a = a.float()
+    b = b.float()
+    return ((a - b).norm() / b.norm().clamp_min(1e-12)).item()
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 256, 64), (128, 128, 128), (4096, 3072, 3072), (1000, 776, 520),
+                                   (4096, 768, 4096), (384, 16384, 256)])
+@pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, False), (True, True)])
+def test_gemm_all_majors(cuda, M, N, K, a_mn, b_mn):
+    from paper_2601_17654_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N * 3 + K)
+    A = torch.randn((K, M) if a_mn else (M, K), device=cuda, generator=g).bfloat16()
+    B = torch.randn((K, N) if b_mn else (N, K), device=cuda, generator=g).bfloat16()
+    D = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+    ops.gemm_raw(A, B, D, M, N, K, a_mn, b_mn)
+    torch.cuda.synchronize()
+    Af = A.float().t() if a_mn else A.float()
+    Bf = B.float() if b_mn else B.float().t()
+    ref = Af @ Bf
+    assert rel_err(D, ref) < 8e-3
+
+
+def test_gemm_residual_and_cap(cuda):
+    from paper_2601_17654_b200 import ops
+    M, N, K = 512, 1024, 512
+    x = torch.randn(M, K, device=cuda).bfloat16()
+    w = torch.randn(N, K, device=cuda).bfloat16()
+    r = torch.randn(M, N, device=cuda).bfloat16()
+    out = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+    for cap in (0, 1, 7, 148):
+        ops.linear(x, w, out, residual=r, max_ctas=cap)
+        torch.cuda.synchronize()
+        ref = x.float() @ w.float().t() + r.float()
+        assert rel_err(out, ref) < 8e-3
+
+
+def test_gemm_replay_resets_scheduler(cuda):
+    from paper_2601_17654_b200 import ops
+    M, N, K = 1024, 1024, 256
+    x = torch.randn(M, K, device=cuda).bfloat16()
+    w = torch.randn(N, K, device=cuda).bfloat16()
+    out = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+    ref = (x.float() @ w.float().t())
+    for _ in range(20):
+        out.zero_()
+        ops.linear(x, w, out)
+    torch.cuda.synchronize()
+    assert rel_err(out, ref) < 8e-3
+    assert int(ops._default_sched[0].buf.abs().sum()) == 0
+
+
+@pytest.mark.parametrize("rows,cols", [(4096, 3072), (100, 1024), (33, 8192), (7, 520)])
+def test_rmsnorm(cuda, rows, cols):
+    from paper_2601_17654_b200 import ops
+    x = torch.randn(rows, cols, device=cuda).bfloat16()
+    w = (1 + 0.1 * torch.randn(cols, device=cuda)).bfloat16()
+    y = torch.empty_like(x)
+    rstd = torch.empty(rows, device=cuda)
+    ops.rmsnorm_fwd(x, w, y, rstd, eps=1e-5)
+    xf = x.float().requires_grad_()
+    wf = w.float().requires_grad_()
+    ref = xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + 1e-5) * wf
+    assert rel_err(y, ref) < 5e-3
+    dy = torch.randn_like(x)
+    dres = torch.randn_like(x)
+    dx = torch.empty_like(x)
+    parts = torch.empty(ops.rmsnorm_partials(rows, cols), cols, device=cuda)
+    ops.rmsnorm_bwd(dy, x, w, rstd, dx, parts, dres=dres)
+    dw = torch.empty(cols, device=cuda, dtype=torch.bfloat16)
+    ops.colsum(parts, dw)
+    ref.backward(dy.float())
+    assert rel_err(dx, xf.grad + dres.float()) < 1e-2
+    assert rel_err(dw, wf.grad) < 1e-2
+
+
+def _rope_ref(x, heads, d, theta, inverse=False):
+    T = x.shape[0]
+    half = d // 2
+    inv = theta ** (-(torch.arange(half, dtype=torch.float64, device=x.device) * 2 / d))
+    ang = torch.arange(T, dtype=torch.float64, device=x.device)[:, None] * inv[None]
+    c, s = ang.cos().float(), ang.sin().float()
+    if inverse:
+        s = -s
+    xv = x.float().view(T, heads, d)
+    a, b = xv[..., :half], xv[..., half:]
+    out = torch.cat([a * c[:, None] - b * s[:, None], b * c[:, None] + a * s[:, None]], -1)
+    return out.view(T, heads * d)
+
+
+def test_rope_strided(cuda):
+    from paper_2601_17654_b200 import ops
+    T, hq, hkv, d = 300, 6, 2, 128
+    qkv = torch.randn(T, (hq + 2 * hkv) * d, device=cuda).bfloat16()
+    out = torch.empty(T, (hq + hkv) * d, device=cuda, dtype=torch.bfloat16)
+    ops.rope(qkv, out, hq + hkv, d, 500000.0)
+    ref = _rope_ref(qkv[:, : (hq + hkv) * d], hq + hkv, d, 500000.0)
+    assert rel_err(out, ref) < 5e-3
+    back = torch.empty_like(out)
+    ops.rope(out, back, hq + hkv, d, 500000.0, inverse=True)
+    assert rel_err(back, qkv[:, : (hq + hkv) * d]) < 1e-2
+
+
+def test_swiglu(cuda):
+    from paper_2601_17654_b200 import ops
+    rows, ffn = 513, 1024
+    gu = torch.randn(rows, 2 * ffn, device=cuda).bfloat16()
+    act = torch.empty(rows, ffn, device=cuda, dtype=torch.bfloat16)
+    ops.swiglu_fwd(gu, act)
+    guf = gu.float().requires_grad_()
+    ref = torch.nn.functional.silu(guf[:, :ffn]) * guf[:, ffn:]
+    assert rel_err(act, ref) < 5e-3
+    dact = torch.randn_like(act)
+    dgu = torch.empty_like(gu)
+    ops.swiglu_bwd(dact, gu, dgu)
+    ref.backward(dact.float())
+    assert rel_err(dgu, guf.grad) < 1e-2
+
+
+def _attn_ref(q, k, v, hq, hkv, d, causal=True):
+    T = q.shape[0]
+    qf = q.float().view(T, hq, d).transpose(0, 1)
+    kf = k.float().view(T, hkv, d).transpose(0, 1).repeat_interleave(hq // hkv, 0)
+    vf = v.float().view(T, hkv, d).transpose(0, 1).repeat_interleave(hq // hkv, 0)
+    return torch.nn.functional.scaled_dot_product_attention(qf, kf, vf, is_causal=causal)
+
+
+@pytest.mark.parametrize("T,hq,hkv,d", [(256, 4, 1, 128), (1000, 6, 2, 128), (512, 8, 8, 64), (4096, 3, 1, 128)])
+def test_attention_fwd_bwd(cuda, T, hq, hkv, d):
+    from paper_2601_17654_b200 import ops
+    torch.manual_seed(T + hq)
+    qkv = torch.randn(T, (hq + 2 * hkv) * d, device=cuda).bfloat16()
+    q = qkv[:, : hq * d]
+    k = qkv[:, hq * d:(hq + hkv) * d]
+    v = qkv[:, (hq + hkv) * d:]
+    o = torch.empty(T, hq * d, device=cuda, dtype=torch.bfloat16)
+    lse = torch.empty(hq, T, device=cuda)
+    scale = 1.0 / math.sqrt(d)
+    ops.attn_fwd(q, k, v, o, lse, T, hq, hkv, d, scale)
+    qf, kf, vf = (t.float().requires_grad_() for t in (q, k, v))
+    ref = _attn_ref(qf, kf, vf, hq, hkv, d)  # [hq, T, d]
+    assert rel_err(o.view(T, hq, d).transpose(0, 1), ref) < 1e-2
+    dout = torch.randn(T, hq * d, device=cuda).bfloat16()
+    dqkv = torch.empty_like(qkv)
+    dq, dk, dv = dqkv[:, : hq * d], dqkv[:, hq * d:(hq + hkv) * d], dqkv[:, (hq + hkv) * d:]
+    ws = ops.attn_bwd_workspace(T, hq, hkv, d, cuda)
+    ops.attn_bwd(q, k, v, o, dout, lse, dq, dk, dv, T, hq, hkv, d, scale, ws)
+    ref.backward(dout.float().view(T, hq, d).transpose(0, 1))
+    assert rel_err(dq, qf.grad) < 2e-2
+    assert rel_err(dk, kf.grad) < 2e-2
+    assert rel_err(dv, vf.grad) < 2e-2

@@ -263,11 +263,20 @@ extern "C" int kpo_comm_create(int rank, int world, int device, size_t sym_bytes
   }
   int optin = 0;
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-  c->smem_bytes = optin;
+  // full-SM reservation: static + dynamic shared memory == the per-block opt-in maximum, which
+  // together with the 1 KB per-CTA system reservation is the whole SM's shared memory.
   const void* kernels[] = {(const void*)all_gather_kernel, (const void*)reduce_scatter_kernel,
                            (const void*)all_reduce_kernel};
+  size_t max_static = 0;
   for (const void* k : kernels) {
-    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    cudaFuncAttributes fa;
+    e = cudaFuncGetAttributes(&fa, k);
+    if (e != cudaSuccess) return fail(e, "cudaFuncGetAttributes");
+    if (fa.sharedSizeBytes > max_static) max_static = fa.sharedSizeBytes;
+  }
+  c->smem_bytes = optin - (int)max_static;
+  for (const void* k : kernels) {
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_bytes);
     if (e != cudaSuccess) return fail(e, "cudaFuncSetAttribute(smem)");
   }
   e = cudaDeviceSynchronize();

@@ -1,0 +1,425 @@
+"""Partitioned transformer layer: real tensors, launch units and partition programs.
+
+A *partition* (reference domain.py:201-229) is one communication unit overlapped with the
+ordered computation kernels of the other nanobatch.  Here every abstract KernelSpec of the
+reference's workloads (workloads.py:38-93: norm, linear_qkv, rope, attention_core, linear_proj,
+linear_up, linear_down, allreduce) is a concrete *launch unit* that issues hand-written sm_100a
+kernels on preallocated device buffers, and the comm kernel is an SM-budgeted P2P collective.
+
+Per layer iteration (forward + backward, 2 nanobatches) there are 8 partitions:
+
+  TP (Megatron-style, all-reduce; config 3):
+    fwd   attn(b) = [norm1, qkv, rope, attention, o_proj(+residual on rank 0)]  || AR(prev block out)
+          mlp(b)  = [norm2, gate_up, swiglu, down(+residual on rank 0)]        || AR(...)
+    bwd   mlp(b)  = [norm1_bwd(upper layer), down_dgrad, down_wgrad, swiglu_bwd, gu_dgrad, gu_wgrad]
+          attn(b) = [norm2_bwd(+dres), o_dgrad, o_wgrad, attention_bwd, rope_bwd, qkv_dgrad, qkv_wgrad]
+    comm of partition i = all-reduce of the partial sum produced by partition i-1 (the other
+    nanobatch), exactly the nanobatching overlap of the paper.
+  FSDP (ZeRO-3, all-gather / reduce-scatter; configs 2 and 4):
+    same compute units on full (gathered) weights; fwd comm = all-gather of the next layer's
+    weight tensor (qkv, o, gate_up, down — one per partition); bwd comm = reduce-scatter of the
+    previous layer's gradient of one tensor fused with the re-gather of the next layer's weight
+    (reference compose.py:32-45 fuses consecutive comm kernels into one unit).
+
+Weights are random-init N(0, 0.02) from one seed on every rank, then sharded; activations are
+N(0, 1) (synthetic data).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Callable
+
+import torch
+
+from . import ops
+from .comm import Communicator
+from .domain import KernelSpec, PartitionSpec
+from .model import Workload
+
+BF16 = torch.bfloat16
+
+
+@dataclass
+class LaunchUnit:
+    name: str
+    spec: KernelSpec
+    fn: Callable[[torch.cuda.Stream], None]
+    kind: str = "memory"  # "gemm" | "attention" | "memory"
+
+
+@dataclass
+class CommUnit:
+    name: str
+    spec: KernelSpec
+    fn: Callable[[torch.cuda.Stream, int], None]
+    algo_bytes: float = 0.0   # bytes each rank moves over the link (busbw numerator)
+
+
+@dataclass
+class PartitionProgram:
+    name: str
+    units: list[LaunchUnit]
+    comm: CommUnit
+    comm_group_size: int
+
+    def spec(self) -> PartitionSpec:
+        return PartitionSpec(tuple(u.spec for u in self.units), self.comm.spec, self.comm_group_size, self.name)
+
+
+def _gemm_spec(name, M, N, K):
+    return KernelSpec(name, flops=2.0 * M * N * K, bytes=2.0 * (M * K + N * K + M * N))
+
+
+def _mem_spec(name, nbytes, flops=0.0):
+    return KernelSpec(name, flops=float(flops), bytes=float(nbytes))
+
+
+class PartitionedLayer:
+    """One rank's partitioned layer (weights, activations, gradients) for a Workload."""
+
+    def __init__(self, wl: Workload, comm: Communicator, device=None, seed: int = 0, data_seed: int | None = None,
+                 fill_virtual_peers: bool = True):
+        self.wl = wl
+        self.comm = comm
+        self.device = torch.device(device or comm.device)
+        self.rank, self.world = comm.rank, comm.world
+        if comm.world != wl.world:
+            raise ValueError("communicator world size does not match the workload")
+        self.sched = ops.GemmScheduler(self.device, slots=64)
+        self._init_weights(seed)
+        self._init_activations(1000 + self.rank if data_seed is None else data_seed)
+        self.programs: dict[str, PartitionProgram] = {}
+        self.order: list[str] = []
+        self._build_units()
+        self._build_programs()
+
+    # ------------------------------------------------------------------ init
+    def _full_weights(self, seed: int) -> dict[str, torch.Tensor]:
+        m = self.wl.model
+        g = torch.Generator(device=self.device).manual_seed(seed)
+        qkv_full = (m.n_heads + 2 * m.n_kv_heads) * m.head_dim
+
+        def randn(*shape, std=0.02):
+            return (torch.randn(*shape, generator=g, device=self.device) * std).to(BF16)
+
+        return {
+            "wqkv": randn(qkv_full, m.hidden),
+            "wo": randn(m.hidden, m.n_heads * m.head_dim),
+            "wgu": randn(2 * m.ffn, m.hidden),
+            "wd": randn(m.hidden, m.ffn),
+            "g1": (1.0 + 0.1 * torch.randn(m.hidden, generator=g, device=self.device)).to(BF16),
+            "g2": (1.0 + 0.1 * torch.randn(m.hidden, generator=g, device=self.device)).to(BF16),
+        }
+
+    def tp_shard(self, full: dict[str, torch.Tensor], r: int) -> dict[str, torch.Tensor]:
+        """Rank r's TP shard of the full weights (Megatron column/row parallel layout)."""
+        wl, m = self.wl, self.wl.model
+        d, hq, hkv, f = wl.d, wl.hq, wl.hkv, wl.ffn
+        kv0 = (r * m.n_kv_heads) // wl.world if m.n_kv_heads >= wl.world else (r * m.n_kv_heads) // wl.world
+        q_rows = full["wqkv"][r * hq * d:(r + 1) * hq * d]
+        k_base = m.n_heads * d
+        v_base = (m.n_heads + m.n_kv_heads) * d
+        k_rows = full["wqkv"][k_base + kv0 * d:k_base + (kv0 + hkv) * d]
+        v_rows = full["wqkv"][v_base + kv0 * d:v_base + (kv0 + hkv) * d]
+        return {
+            "wqkv": torch.cat([q_rows, k_rows, v_rows]).contiguous(),
+            "wo": full["wo"][:, r * hq * d:(r + 1) * hq * d].contiguous(),
+            "wgu": torch.cat([full["wgu"][r * f:(r + 1) * f], full["wgu"][m.ffn + r * f:m.ffn + (r + 1) * f]]).contiguous(),
+            "wd": full["wd"][:, r * f:(r + 1) * f].contiguous(),
+            "g1": full["g1"].clone(),
+            "g2": full["g2"].clone(),
+        }
+
+    def _init_weights(self, seed: int) -> None:
+        wl = self.wl
+        full = self._full_weights(seed)
+        self.full_weights = full if wl.world == 1 or wl.parallel == "fsdp" else None
+        self.tensors = ("wqkv", "wo", "wgu", "wd")
+        if wl.parallel == "tp":
+            self.w = self.tp_shard(full, self.rank)
+        else:
+            self.w = {k: v for k, v in full.items()}
+        self._full_for_oracle = full  # small configs only (kept for parity tests)
+        T, h = wl.tokens, wl.h
+        dev = self.device
+        c = self.comm
+        if wl.parallel == "fsdp":
+            # flat shards of every weight tensor live in the symmetric buffer
+            self.shard = {}
+            self.w_next = {}
+            self.dw_sym = [{}, {}]  # two layer-parity gradient buffers (RS inputs)
+            self.dw_shard = {}
+            for name in self.tensors:
+                n = full[name].numel()
+                if n % (8 * wl.world):
+                    raise ValueError(f"{name} numel {n} not divisible by 8*world")
+                per = n // wl.world
+                reg = c.alloc(per * 2)
+                reg.local().copy_(full[name].view(-1)[self.rank * per:(self.rank + 1) * per])
+                if c.loopback:
+                    for p in range(wl.world):
+                        if p != self.rank:
+                            reg.peer(p).copy_(full[name].view(-1)[p * per:(p + 1) * per])
+                self.shard[name] = reg
+                self.w_next[name] = torch.empty_like(full[name])
+                for par in range(2):
+                    self.dw_sym[par][name] = c.alloc(n * 2)
+                self.dw_shard[name] = torch.empty(per, dtype=BF16, device=dev)
+            self.dw = {k: self.dw_sym[0][k].local().view(self.w[k].shape) for k in self.tensors}
+        else:
+            self.dw = {k: torch.empty_like(self.w[k]) for k in self.tensors}
+            self.partial = [{}, {}]
+            for b in range(wl.nanobatches):
+                for name in ("hp", "yp", "dxn2p", "dxn1p"):
+                    self.partial[b % 2][(name, b)] = c.alloc(T * h * 2)
+            self.stage = c.alloc(T * h * 2)
+        self.dg1 = torch.empty(h, dtype=BF16, device=dev)
+        self.dg2 = torch.empty(h, dtype=BF16, device=dev)
+
+    def _init_activations(self, data_seed: int) -> None:
+        wl = self.wl
+        T, h, d = wl.tokens, wl.h, wl.d
+        dev = self.device
+        g = torch.Generator(device=dev).manual_seed(data_seed)
+        E = lambda *s, dt=BF16: torch.zeros(*s, dtype=dt, device=dev)
+        self.nb = []
+        nparts = ops.rmsnorm_partials(T, h)
+        for b in range(wl.nanobatches):
+            a = {
+                "x": torch.randn(T, h, generator=g, device=dev).to(BF16),
+                "dy": torch.randn(T, h, generator=g, device=dev).to(BF16),
+                "xn1": E(T, h), "rstd1": E(T, dt=torch.float32), "qkv": E(T, wl.qkv_dim),
+                "qkr": E(T, (wl.hq + wl.hkv) * d), "ao": E(T, wl.hq * d), "lse": E(wl.hq, T, dt=torch.float32),
+                "h": E(T, h), "xn2": E(T, h), "rstd2": E(T, dt=torch.float32), "gu": E(T, 2 * wl.ffn),
+                "act": E(T, wl.ffn), "y": E(T, h),
+                "dact": E(T, wl.ffn), "dgu": E(T, 2 * wl.ffn), "dxn2": E(T, h), "dh": E(T, h),
+                "dao": E(T, wl.hq * d), "dqkr": E(T, (wl.hq + wl.hkv) * d), "dqkv": E(T, wl.qkv_dim),
+                "dxn1": E(T, h), "dx": E(T, h),
+                "dwp1": E(nparts, h, dt=torch.float32), "dwp2": E(nparts, h, dt=torch.float32),
+            }
+            if wl.parallel == "fsdp":
+                a["dxn2p"] = a["dxn2"]
+                a["dxn1p"] = a["dxn1"]
+            self.nb.append(a)
+        self.attn_ws = ops.attn_bwd_workspace(T, wl.hq, wl.hkv, d, dev)
+
+    # ------------------------------------------------------------------ launch units
+    def _gemm(self, slot):
+        def run(fn, *args, **kw):
+            fn(*args, sched=slot, **kw)
+        return run
+
+    def _build_units(self) -> None:
+        wl = self.wl
+        T, h, d, hq, hkv, f = wl.tokens, wl.h, wl.d, wl.hq, wl.hkv, wl.ffn
+        qd = (hq + hkv) * d
+        scale = 1.0 / math.sqrt(d)
+        eps, theta = wl.model.norm_eps, wl.model.rope_theta
+        tp = wl.parallel == "tp"
+        rank0 = self.rank == 0
+        W = self.w
+        self.units: dict[tuple[str, int], LaunchUnit] = {}
+        attn_flops = 2.0 * T * T * hq * d  # causal: 4*T^2*hq*d / 2
+
+        for b in range(wl.nanobatches):
+            a = self.nb[b]
+            ga = self.sched.slot
+            # partial-sum outputs of row-parallel GEMMs (TP) live in the symmetric buffer
+            if tp:
+                hp = self.partial[b % 2][("hp", b)].local().view(T, h)
+                yp = self.partial[b % 2][("yp", b)].local().view(T, h)
+                dxn2p = self.partial[b % 2][("dxn2p", b)].local().view(T, h)
+                dxn1p = self.partial[b % 2][("dxn1p", b)].local().view(T, h)
+            else:
+                hp, yp, dxn2p, dxn1p = a["h"], a["y"], a["dxn2"], a["dxn1"]
+            a["hp"], a["yp"], a["dxn2p_t"], a["dxn1p_t"] = hp, yp, dxn2p, dxn1p
+            res_attn = a["x"] if (not tp or rank0) else None
+            res_mlp = a["h"] if (not tp or rank0) else None
+            s = {k: ga() for k in ("qkv", "o", "gu", "d", "dd", "dwd", "dgu", "dwgu", "do", "dwo", "dqkv", "dwqkv")}
+            acc = b > 0  # weight gradients accumulate over nanobatches
+
+            def U(name, spec, fn, kind="memory"):
+                self.units[(name, b)] = LaunchUnit(name, spec, fn, kind)
+
+            # ---------------- forward
+            U("norm1", _mem_spec("norm1", 4 * T * h + 2 * h + 4 * T, 3 * T * h),
+              lambda st, a=a: ops.rmsnorm_fwd(a["x"], W["g1"], a["xn1"], a["rstd1"], eps, stream=st))
+            U("linear_qkv", _gemm_spec("linear_qkv", T, wl.qkv_dim, h),
+              lambda st, a=a, s=s: ops.linear(a["xn1"], W["wqkv"], a["qkv"], sched=s["qkv"], stream=st), "gemm")
+            U("rope", _mem_spec("rope", 4 * T * qd, 6 * T * qd),
+              lambda st, a=a: ops.rope(a["qkv"], a["qkr"], hq + hkv, d, theta, stream=st))
+            U("attention_core", KernelSpec("attention_core", flops=attn_flops, bytes=2.0 * T * (2 * hq + 2 * hkv) * d),
+              lambda st, a=a: ops.attn_fwd(a["qkr"][:, :hq * d], a["qkr"][:, hq * d:], a["qkv"][:, qd:], a["ao"],
+                                           a["lse"], T, hq, hkv, d, scale, stream=st), "attention")
+            U("linear_proj", _gemm_spec("linear_proj", T, h, hq * d),
+              lambda st, a=a, s=s, hp=hp, r=res_attn: ops.linear(a["ao"], W["wo"], hp, residual=r, sched=s["o"],
+                                                                 stream=st), "gemm")
+            U("norm2", _mem_spec("norm2", 4 * T * h + 2 * h + 4 * T, 3 * T * h),
+              lambda st, a=a: ops.rmsnorm_fwd(a["h"], W["g2"], a["xn2"], a["rstd2"], eps, stream=st))
+            U("linear_up", _gemm_spec("linear_up", T, 2 * f, h),
+              lambda st, a=a, s=s: ops.linear(a["xn2"], W["wgu"], a["gu"], sched=s["gu"], stream=st), "gemm")
+            U("swiglu", _mem_spec("swiglu", 2 * T * 3 * f, 4 * T * f),
+              lambda st, a=a: ops.swiglu_fwd(a["gu"], a["act"], stream=st))
+            U("linear_down", _gemm_spec("linear_down", T, h, f),
+              lambda st, a=a, s=s, yp=yp, r=res_mlp: ops.linear(a["act"], W["wd"], yp, residual=r, sched=s["d"],
+                                                                stream=st), "gemm")
+            # ---------------- backward (dW accumulate over nanobatches through the epilogue C input)
+            dw = self.dw
+            U("norm1_bwd", _mem_spec("norm1_bwd", 2 * 5 * T * h, 8 * T * h),
+              lambda st, a=a: ops.rmsnorm_bwd(a["dxn1"], a["x"], W["g1"], a["rstd1"], a["dx"], a["dwp1"],
+                                              dres=a["dh"], stream=st))
+            U("down_dgrad", _gemm_spec("down_dgrad", T, f, h),
+              lambda st, a=a, s=s: ops.linear_dgrad(a["dy"], W["wd"], a["dact"], sched=s["dd"], stream=st), "gemm")
+            U("down_wgrad", _gemm_spec("down_wgrad", h, f, T),
+              lambda st, a=a, s=s, acc=acc: ops.linear_wgrad(a["dy"], a["act"], dw["wd"],
+                                                             accumulate=dw["wd"] if acc else None, sched=s["dwd"],
+                                                             stream=st), "gemm")
+            U("swiglu_bwd", _mem_spec("swiglu_bwd", 2 * T * 5 * f, 10 * T * f),
+              lambda st, a=a: ops.swiglu_bwd(a["dact"], a["gu"], a["dgu"], stream=st))
+            U("gu_dgrad", _gemm_spec("gu_dgrad", T, h, 2 * f),
+              lambda st, a=a, s=s, o=dxn2p: ops.linear_dgrad(a["dgu"], W["wgu"], o, sched=s["dgu"], stream=st), "gemm")
+            U("gu_wgrad", _gemm_spec("gu_wgrad", 2 * f, h, T),
+              lambda st, a=a, s=s, acc=acc: ops.linear_wgrad(a["dgu"], a["xn2"], dw["wgu"],
+                                                             accumulate=dw["wgu"] if acc else None, sched=s["dwgu"],
+                                                             stream=st), "gemm")
+            U("norm2_bwd", _mem_spec("norm2_bwd", 2 * 5 * T * h, 8 * T * h),
+              lambda st, a=a: ops.rmsnorm_bwd(a["dxn2"], a["h"], W["g2"], a["rstd2"], a["dh"], a["dwp2"],
+                                              dres=a["dy"], stream=st))
+            U("o_dgrad", _gemm_spec("o_dgrad", T, hq * d, h),
+              lambda st, a=a, s=s: ops.linear_dgrad(a["dh"], W["wo"], a["dao"], sched=s["do"], stream=st), "gemm")
+            U("o_wgrad", _gemm_spec("o_wgrad", h, hq * d, T),
+              lambda st, a=a, s=s, acc=acc: ops.linear_wgrad(a["dh"], a["ao"], dw["wo"],
+                                                             accumulate=dw["wo"] if acc else None, sched=s["dwo"],
+                                                             stream=st), "gemm")
+            U("attention_bwd", KernelSpec("attention_bwd", flops=2.5 * attn_flops,
+                                          bytes=2.0 * T * (4 * hq + 4 * hkv) * d + 8.0 * T * hq * d),
+              lambda st, a=a: ops.attn_bwd(a["qkr"][:, :hq * d], a["qkr"][:, hq * d:], a["qkv"][:, qd:], a["ao"],
+                                           a["dao"], a["lse"], a["dqkr"][:, :hq * d], a["dqkr"][:, hq * d:],
+                                           a["dqkv"][:, qd:], T, hq, hkv, d, scale, self.attn_ws, stream=st),
+              "attention")
+            U("rope_bwd", _mem_spec("rope_bwd", 4 * T * qd, 6 * T * qd),
+              lambda st, a=a: ops.rope(a["dqkr"], a["dqkv"], hq + hkv, d, theta, inverse=True, stream=st))
+            U("qkv_dgrad", _gemm_spec("qkv_dgrad", T, h, wl.qkv_dim),
+              lambda st, a=a, s=s, o=dxn1p: ops.linear_dgrad(a["dqkv"], W["wqkv"], o, sched=s["dqkv"], stream=st),
+              "gemm")
+            U("qkv_wgrad", _gemm_spec("qkv_wgrad", wl.qkv_dim, h, T),
+              lambda st, a=a, s=s, acc=acc: ops.linear_wgrad(a["dqkv"], a["xn1"], dw["wqkv"],
+                                                             accumulate=dw["wqkv"] if acc else None, sched=s["dwqkv"],
+                                                             stream=st), "gemm")
+
+    # ------------------------------------------------------------------ comm units
+    def _ar_unit(self, src_key: tuple[str, int], out: torch.Tensor) -> CommUnit:
+        name, b = src_key
+        reg = self.partial[b % 2][src_key]
+        T, h, W = self.wl.tokens, self.wl.h, self.world
+        nbytes = T * h * 2
+        link = 2.0 * (W - 1) / W * nbytes  # bytes each rank sends (= receives) over the link
+
+        def fn(st, ncta, reg=reg, out=out):
+            self.comm.all_reduce(reg, self.stage, out, ncta, stream=st)
+
+        return CommUnit(f"allreduce_{name}{b}", KernelSpec(f"allreduce_{name}{b}", comm_bytes=max(link, 1.0)), fn,
+                        algo_bytes=link)
+
+    def _fsdp_unit(self, tensors: list[tuple[str, str]]) -> CommUnit:
+        """Fused comm unit: ('rs', name) reduce-scatters the previous layer's gradient of `name`,
+        ('ag', name) all-gathers the next layer's weight `name`."""
+        W = self.world
+        link = 0.0
+        ops_ = []
+        for kind, name in tensors:
+            n = self.w[name].numel()
+            link += (W - 1) / W * n * 2
+            ops_.append((kind, name))
+
+        def fn(st, ncta):
+            for kind, name in ops_:
+                if kind == "ag":
+                    self.comm.all_gather(self.shard[name], self.w_next[name], ncta, stream=st)
+                else:
+                    self.comm.reduce_scatter(self.dw_sym[1][name], self.dw_shard[name], ncta, stream=st)
+
+        label = "+".join(f"{k}_{n}" for k, n in tensors)
+        return CommUnit(label, KernelSpec(label, comm_bytes=max(link, 1.0)), fn, algo_bytes=link)
+
+    def _build_programs(self) -> None:
+        wl = self.wl
+        g = wl.world
+        fwd_attn = ["norm1", "linear_qkv", "rope", "attention_core", "linear_proj"]
+        fwd_mlp = ["norm2", "linear_up", "swiglu", "linear_down"]
+        bwd_mlp = ["norm1_bwd", "down_dgrad", "down_wgrad", "swiglu_bwd", "gu_dgrad", "gu_wgrad"]
+        bwd_attn = ["norm2_bwd", "o_dgrad", "o_wgrad", "attention_bwd", "rope_bwd", "qkv_dgrad", "qkv_wgrad"]
+        nb = wl.nanobatches
+        assert nb == 2, "partition programs are built for 2 nanobatches"
+        blocks = [("fwd_attn", fwd_attn), ("fwd_mlp", fwd_mlp), ("bwd_mlp", bwd_mlp), ("bwd_attn", bwd_attn)]
+        if wl.parallel == "tp":
+            # comm of each partition = all-reduce of the previous partition's partial output
+            produced = {"fwd_attn": "hp", "fwd_mlp": "yp", "bwd_mlp": "dxn2p", "bwd_attn": "dxn1p"}
+            consumer_out = {"hp": "h", "yp": "y", "dxn2p": "dxn2", "dxn1p": "dxn1"}
+            seq = [(blk, b) for blk, _ in blocks[:2] for b in range(nb)] + [(blk, b) for blk, _ in blocks[2:]
+                                                                             for b in range(nb)]
+            for i, (blk, b) in enumerate(seq):
+                pblk, pb = seq[i - 1]  # i == 0 wraps to the last partition (steady state)
+                src = (produced[pblk], pb)
+                comm = self._ar_unit(src, self.nb[pb][consumer_out[produced[pblk]]])
+                units = [self.units[(k, b)] for k in dict(blocks)[blk]]
+                name = f"{blk}{b}"
+                self.programs[name] = PartitionProgram(name, units, comm, g)
+                self.order.append(name)
+        else:
+            comms = {
+                ("fwd_attn", 0): [("ag", "wqkv")], ("fwd_attn", 1): [("ag", "wo")],
+                ("fwd_mlp", 0): [("ag", "wgu")], ("fwd_mlp", 1): [("ag", "wd")],
+                ("bwd_mlp", 0): [("rs", "wd"), ("ag", "wd")], ("bwd_mlp", 1): [("rs", "wgu"), ("ag", "wgu")],
+                ("bwd_attn", 0): [("rs", "wo"), ("ag", "wo")], ("bwd_attn", 1): [("rs", "wqkv"), ("ag", "wqkv")],
+            }
+            for blk, names in blocks:
+                for b in range(nb):
+                    units = [self.units[(k, b)] for k in names]
+                    name = f"{blk}{b}"
+                    self.programs[name] = PartitionProgram(name, units, self._fsdp_unit(comms[(blk, b)]), g)
+                    self.order.append(name)
+
+    # ------------------------------------------------------------------ helpers
+    def finalize_norm_grads(self, stream=None) -> None:
+        """dg1/dg2 = column sums of the per-CTA partials of both nanobatches."""
+        p1 = torch.cat([a["dwp1"] for a in self.nb])
+        p2 = torch.cat([a["dwp2"] for a in self.nb])
+        ops.colsum(p1, self.dg1, stream=stream)
+        ops.colsum(p2, self.dg2, stream=stream)
+
+    def partition_specs(self) -> list[PartitionSpec]:
+        return [self.programs[n].spec() for n in self.order]
+
+    def run_unrolled(self, stream=None, ncta: int = 16) -> None:
+        """Dependency-correct single-layer forward+backward (for parity tests): every launch unit
+        once per nanobatch, each collective right after the unit that produces its input."""
+        st = stream or torch.cuda.current_stream()
+        tp = self.wl.parallel == "tp"
+        for b in range(self.wl.nanobatches):
+            a = self.nb[b]
+            for k in ["norm1", "linear_qkv", "rope", "attention_core", "linear_proj"]:
+                self.units[(k, b)].fn(st)
+            if tp:
+                self.comm.all_reduce(self.partial[b % 2][("hp", b)], self.stage, a["h"], ncta, stream=st)
+            for k in ["norm2", "linear_up", "swiglu", "linear_down"]:
+                self.units[(k, b)].fn(st)
+            if tp:
+                self.comm.all_reduce(self.partial[b % 2][("yp", b)], self.stage, a["y"], ncta, stream=st)
+        for b in range(self.wl.nanobatches):
+            a = self.nb[b]
+            for k in ["down_dgrad", "down_wgrad", "swiglu_bwd", "gu_dgrad", "gu_wgrad"]:
+                self.units[(k, b)].fn(st)
+            if tp:
+                self.comm.all_reduce(self.partial[b % 2][("dxn2p", b)], self.stage, a["dxn2"], ncta, stream=st)
+            for k in ["norm2_bwd", "o_dgrad", "o_wgrad", "attention_bwd", "rope_bwd", "qkv_dgrad", "qkv_wgrad"]:
+                self.units[(k, b)].fn(st)
+            if tp:
+                self.comm.all_reduce(self.partial[b % 2][("dxn1p", b)], self.stage, a["dxn1"], ncta, stream=st)
+            self.units[("norm1_bwd", b)].fn(st)
+        self.finalize_norm_grads(st)
+
+    def weight_grad(self, name: str) -> torch.Tensor:
+        return self.dw[name]

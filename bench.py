@@ -1,0 +1,381 @@
+#!/usr/bin/env python
+"""bench.py — partitioned-overlap layer iteration on B200 (driver contract, one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1]): one Llama-3.2-3B transformer layer under FSDP, forward +
+backward, 2 nanobatches x 4096 tokens per rank, executed as the 8 partitions of the Kareus
+partitioned-overlap model (each: hand-written sm_100a compute kernels on the compute stream, an
+SM-budgeted P2P collective on the comm stream).  A *step* = one such layer iteration under the
+baseline nanobatching schedule (f_max, default comm CTAs, overlap(0, n)).
+
+  N = 1: the 8-rank FSDP group runs in loopback (virtual peers' shards in local HBM; the kernels,
+         CTA budget and barriers are the real ones, the link is HBM).
+  N > 1: one process per GPU (torchrun), CUDA-IPC peer mapping, FSDP over N ranks; time = max over
+         ranks, energy = sum over ranks, value = whole-job iteration time.
+
+`--impl reference` times the reference-side CPU path (the oracle's fp32 execution of the same
+layer iteration, oracle/layer_ref.py) on the host cores; see DESIGN.md §Measurement.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "iteration time (s) & energy (J/iter) Pareto frontier, 1-8 B200; comm bus GB/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="kpo", choices=["kpo", "reference"])
+    ap.add_argument("--config", type=int, default=1, help="BASELINE.json configs index (1..3)")
+    ap.add_argument("--tokens", type=int, default=4096)
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-tokens", type=int, default=1024)
+    ap.add_argument("--sweep-window", type=float, default=0.8)
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def iteration_flops(wl) -> float:
+    """Algorithmic FLOPs of one layer iteration (fwd + bwd, all nanobatches) for one rank."""
+    T, h, d, hq, hkv, f = wl.tokens, wl.h, wl.d, wl.hq, wl.hkv, wl.ffn
+    gemm_fwd = 2.0 * T * h * (wl.qkv_dim + hq * d + 2 * f + f)
+    attn_fwd = 2.0 * T * T * hq * d
+    per_nb = 3 * gemm_fwd + attn_fwd * 3.5
+    return per_nb * wl.nanobatches
+
+
+# ---------------------------------------------------------------------------- CPU baseline
+def cpu_sample(wl, tokens: int, threads: int) -> dict:
+    """Oracle fp32 forward+backward of ONE nanobatch at `tokens` tokens, scaled by FLOPs to the
+    full iteration (nanobatches x wl.tokens)."""
+    import torch
+
+    from oracle import layer_ref
+    from paper_2601_17654_b200.model import Workload
+
+    torch.set_num_threads(threads)
+    m = wl.model
+    g = torch.Generator().manual_seed(0)
+    W = {
+        "wqkv": torch.randn((m.n_heads + 2 * m.n_kv_heads) * m.head_dim, m.hidden, generator=g) * 0.02,
+        "wo": torch.randn(m.hidden, m.n_heads * m.head_dim, generator=g) * 0.02,
+        "wgu": torch.randn(2 * m.ffn, m.hidden, generator=g) * 0.02,
+        "wd": torch.randn(m.hidden, m.ffn, generator=g) * 0.02,
+        "g1": torch.ones(m.hidden), "g2": torch.ones(m.hidden),
+    }
+    x = torch.randn(tokens, m.hidden, generator=g)
+    dy = torch.randn(tokens, m.hidden, generator=g)
+    t0 = time.perf_counter()
+    layer_ref.layer_fwd_bwd([x], [dy], W, m)
+    dt = time.perf_counter() - t0
+    sample = Workload(m, "fsdp", 1, tokens, nanobatches=1)
+    full = Workload(m, "fsdp", 1, wl.tokens, nanobatches=wl.nanobatches)
+    scale = iteration_flops(full) / iteration_flops(sample)
+    return {"sample_s": dt, "scale": scale, "value": dt * scale}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    import torch
+
+    from paper_2601_17654_b200.model import baseline_workload
+
+    wl = baseline_workload(args.config, world=8, tokens=args.tokens)
+    threads = os.cpu_count() or 1
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_sample(wl, args.cpu_tokens, threads)
+        if i >= args.warmup:
+            vals.append(r["value"])
+    v = statistics.mean(vals)
+    sample = (f"oracle fp32 fwd+bwd of 1 nanobatch x {args.cpu_tokens} tokens per step, scaled by FLOPs to "
+              f"{wl.nanobatches} x {wl.tokens} tokens")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "s/iter", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{wl.model.name} layer iteration (fwd+bwd, {wl.nanobatches} nanobatches x "
+                               f"{wl.tokens} tokens), CPU fp32", "model": wl.model.name},
+        "cpu_baseline": {"value": v, "unit": "s/iter", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": v, "unit": "s/iter", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------- GPU arm
+def run_kpo(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_17654_b200.comm import Communicator
+    from paper_2601_17654_b200.device import b200_model, load_measured_peaks
+    from paper_2601_17654_b200.domain import LaunchTiming, ScheduleConfig
+    from paper_2601_17654_b200.device import ProfilingProtocol
+    from paper_2601_17654_b200.engine import Engine
+    from paper_2601_17654_b200.layer import PartitionedLayer
+    from paper_2601_17654_b200.model import baseline_workload
+    from paper_2601_17654_b200.runner import LayerRunner, sequential_schedule
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    group_world = world if world > 1 else 8
+    wl = baseline_workload(args.config, world=group_world, tokens=args.tokens)
+    peaks = load_measured_peaks()
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    tf_burst = peaks.get("bf16_tflops", 1590.0)
+    tf_sust = peaks.get("bf16_tflops_sustained", 1400.0)
+    peak_src = "measured" if peaks else "fallback"
+    gpu = b200_model(hbm_gbs=hbm, bf16_tflops=tf_burst)
+
+    # symmetric buffer: FSDP shards + two gradient buffers; TP: 4 partials x 2 nb + stage
+    numels = wl.weight_numels()
+    if wl.parallel == "fsdp":
+        sym = sum(int(n * 2 / group_world) + 2 * n * 2 for n in numels.values()) + (64 << 20)
+    else:
+        sym = 9 * wl.tokens * wl.h * 2 + (64 << 20)
+    comm = (Communicator.loopback_group(group_world, sym, device=dev) if world == 1
+            else Communicator.from_process_group(sym, device=dev))
+    layer = PartitionedLayer(wl, comm)
+    eng = Engine.for_layer(layer, gpu)
+    run = LayerRunner(layer, eng)
+    run.warm()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t)
+
+    def sum_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t)
+
+    for _ in range(max(3, args.warmup)):
+        run.step()
+    torch.cuda.synchronize(dev)
+    # ------------------------------------------------ timed region (device time, max over ranks)
+    barrier()
+    torch.cuda.synchronize(dev)
+    st = eng.exec.compute
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record(st)
+    for _ in range(args.steps):
+        run.step()
+    e1.record(st)
+    torch.cuda.synchronize(dev)
+    t1 = time.perf_counter()
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    clocks = eng.sampler.clocks_summary(t0, t1)
+
+    # ------------------------------------------------ end to end through the host-buffer entry point
+    pin = lambda t: torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    xs = [pin(a["x"]).copy_(a["x"].cpu()) for a in layer.nb]
+    dys = [pin(a["dy"]).copy_(a["dy"].cpu()) for a in layer.nb]
+    dxs = [pin(a["dx"]) for a in layer.nb]
+    run.step_host(xs, dys, dxs)
+    n_e2e = max(3, args.steps // 3)
+    barrier()
+    h0 = time.perf_counter()
+    for _ in range(n_e2e):
+        run.step_host(xs, dys, dxs)
+    h1 = time.perf_counter()
+    e2e_s = max_over_ranks((h1 - h0) / n_e2e)
+    h2d = sum(t.numel() * t.element_size() for t in xs + dys)
+    d2h = sum(t.numel() * t.element_size() for t in dxs)
+
+    # ------------------------------------------------ dominant kernel: per-unit times inside the step
+    ut = run.unit_times(iters=3)
+    per_unit = {}
+    for name in layer.order:
+        for u in layer.programs[name].units:
+            per_unit.setdefault(u.name, (u, []))
+    totals = {k: sum(v) / 3.0 for k, v in ut.items()}
+    step_ms_instr = sum(totals.values())
+    dom = max(totals, key=lambda k: totals[k])  # dominant launch unit by share of the step
+    kernels = []
+    for k in sorted(totals, key=lambda k: -totals[k]):
+        u = per_unit[k][0]
+        avg = statistics.mean(ut[k])
+        if u.kind in ("gemm", "attention"):
+            ach = u.spec.flops / (avg / 1e3) / 1e12
+            kernels.append({"unit": k, "bound": "tensor", "achieved": round(ach, 1), "unit_of": "TFLOP/s",
+                            "frac": round(ach / tf_sust, 4), "avg_launch_ms": round(avg, 4),
+                            "share": round(totals[k] / step_ms_instr, 4)})
+        else:
+            ach = u.spec.bytes / (avg / 1e3) / 1e9
+            kernels.append({"unit": k, "bound": "hbm", "achieved": round(ach, 1), "unit_of": "GB/s",
+                            "frac": round(ach / hbm, 4), "avg_launch_ms": round(avg, 4),
+                            "share": round(totals[k] / step_ms_instr, 4)})
+    dom_row = next(r for r in kernels if r["unit"] == dom)
+    dom_unit = per_unit[dom][0]
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "dram_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(dom)
+        except Exception:
+            traffic = None
+
+    # ------------------------------------------------ energy over a >= 2 s window of back-to-back steps
+    n_energy = max(args.steps, int(math.ceil(2.0 / max(ms / 1e3, 1e-4))))
+    barrier()
+    torch.cuda.synchronize(dev)
+    w0 = time.perf_counter()
+    for _ in range(n_energy):
+        run.step()
+    torch.cuda.synchronize(dev)
+    w1 = time.perf_counter()
+    energy_iter = sum_over_ranks(eng.sampler.window_j(w0, w1) / n_energy)
+    eclocks = eng.sampler.clocks_summary(w0, w1)
+
+    # ------------------------------------------------ collective bus bandwidth (comm unit alone)
+    comm_rows = []
+    cs = eng.exec.comm_stream
+    for name in layer.order:
+        cu = layer.programs[name].comm
+        for nc in (eng.default_ncta(),):
+            cu.fn(cs, nc)
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record(cs)
+            for _ in range(5):
+                cu.fn(cs, nc)
+            c1.record(cs)
+            c1.synchronize()
+            cms = c0.elapsed_time(c1) / 5
+            comm_rows.append({"unit": cu.name, "ncta": nc, "ms": round(cms, 4),
+                              "busbw_gbps": round(cu.algo_bytes / (cms / 1e3) / 1e9, 1)})
+    barrier()
+
+    # ------------------------------------------------ schedule sweep -> iteration frontier
+    frontier = None
+    if not args.no_sweep:
+        proto = ProfilingProtocol(warmup_s=0.2, window_s=args.sweep_window, cooldown_s=0.0)
+        f = gpu.f_max_mhz
+        per_part = {}
+        for name in layer.order:
+            prog = layer.programs[name]
+            n = len(prog.units)
+            cands = [ScheduleConfig(f, 16, LaunchTiming.sequential())]
+            for sm in (8, 16, 32):
+                cands.append(ScheduleConfig(f, sm, LaunchTiming.overlap(0, n)))
+            if n > 2:
+                cands.append(ScheduleConfig(f, 16, LaunchTiming.overlap(1, n - 1)))
+                cands.append(ScheduleConfig(f, 16, LaunchTiming.overlap(0, 2)))
+            rows = []
+            for c in cands:
+                m = eng.measure(prog.spec(), c, gpu, None, proto, None)
+                rows.append((c, m))
+            per_part[name] = rows
+        default = {n: per_part[n][2] for n in layer.order}  # overlap(0,n) @ 16 CTAs
+        seq = {n: per_part[n][0] for n in layer.order}
+        tmin = {n: min(per_part[n], key=lambda r: r[1].time_ms) for n in layer.order}
+        emin = {n: min(per_part[n], key=lambda r: r[1].total_energy_j) for n in layer.order}
+
+        def tot(choice):
+            return (sum(r[1].time_ms for r in choice.values()), sum(r[1].total_energy_j for r in choice.values()))
+
+        pts = {"nanobatching_default": tot(default), "sequential_megatron": tot(seq), "min_time": tot(tmin),
+               "min_energy": tot(emin)}
+        frontier = {k: {"time_ms": round(v[0], 4), "energy_j": round(v[1], 4)} for k, v in pts.items()}
+        frontier["chosen_min_energy"] = {n: emin[n][0].timing.encode() + f"@{emin[n][0].sm_alloc}" for n in layer.order}
+        frontier["note"] = ("frequency fixed: NVML locked clocks NOT_SUPPORTED on this pool (power.py); sweep over "
+                            "comm SM budget x launch timing, windows of " + str(args.sweep_window) + " s")
+
+    # ------------------------------------------------ CPU baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        cpu_sample(wl, args.cpu_tokens, threads)  # first call pays allocator / thread-pool warm-up
+        r = cpu_sample(wl, args.cpu_tokens, threads)
+        cpu = {"value": r["value"], "unit": "s/iter", "cores": threads, "kind": "port",
+               "sample": f"oracle/layer_ref.py fp32 fwd+bwd of 1 nanobatch x {args.cpu_tokens} tokens "
+                         f"({r['sample_s']:.2f} s), scaled x{r['scale']:.1f} by FLOPs to the full iteration"}
+
+    if rank == 0:
+        launches = run.kernels_per_step() * args.steps
+        line = {
+            "metric": METRIC, "value": ms / 1e3, "unit": "s/iter", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (weights N(0,0.02) seed 0, activations N(0,1) seed 1000+rank)",
+            "config": {
+                "workload": f"{wl.model.name} layer iteration: fwd+bwd, {wl.nanobatches} nanobatches x {wl.tokens} "
+                            f"tokens per rank, 8 partitions",
+                "model": wl.model.name, "global_batch": wl.tokens * wl.nanobatches * world, "seq_len": wl.tokens,
+                "parallelism": (f"fsdp{group_world}-loopback" if world == 1 else f"{wl.parallel}{world}"),
+                "schedule": f"nanobatching default: f_max, {eng.default_ncta()} comm CTAs, overlap(0,n)",
+                "l2": "no flush: per-step working set (layer weights + activations) > 126 MB L2",
+                "graphs": len(eng.exec.graphs), "graph_failures": len(eng.exec.graph_failures),
+            },
+            "energy_j_per_iter": energy_iter, "energy_window_steps": n_energy,
+            "avg_power_w": energy_iter / (ms / 1e3) if ms > 0 else None,
+            "tflops_per_gpu": iteration_flops(wl) / (ms / 1e3) / 1e12,
+            "roofline": {"bound": dom_row["bound"], "kernel": dom, "achieved": dom_row["achieved"],
+                         "peak": tf_sust if dom_row["bound"] == "tensor" else hbm, "unit": dom_row["unit_of"],
+                         "frac": dom_row["frac"], "traffic": traffic,
+                         "peak_kind": (f"{peak_src} sustained bf16 (kernel timed inside the step)"
+                                       if dom_row["bound"] == "tensor" else f"{peak_src} HBM copy"),
+                         "share_of_step": dom_row["share"],
+                         "algorithmic_per_launch": dom_unit.spec.flops if dom_row["bound"] == "tensor"
+                         else dom_unit.spec.bytes, "avg_launch_ms": dom_row["avg_launch_ms"]},
+            "kernels": kernels,
+            "comm": {"mode": "loopback (HBM)" if world == 1 else "cuda-ipc p2p (NVLink)", "units": comm_rows},
+            "frontier": frontier,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_s, "unit": "s/iter", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "clocks": {"sm_mhz": clocks.get("sm_mhz"), "sm_max_mhz": eng.nvml.max_sm_clock_mhz(),
+                       "reasons": sorted(set(clocks.get("reasons", [])) | set(eclocks.get("reasons", []))),
+                       "power_w_max": eclocks.get("power_w_max")},
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_kpo(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

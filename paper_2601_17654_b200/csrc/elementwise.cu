@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(256) rmsnorm_fwd_generic(const __nv_bfloat16* 
 // ===================================================================== RMSNorm backward
 // dx_i = r*w_i*dy_i - x_i * r^3/n * sum_j(w_j*dy_j*x_j)  (+ dres_i)
 // dw_j partial per CTA: sum over the CTA's rows of dy_j*x_j*r, written as fp32 [blocks, cols].
-constexpr int kNormBwdRowsPerBlock = 64;
+constexpr int kNormBwdRowsPerBlock = 16;
 constexpr int kNormBwdWarps = 8;
 
 __global__ void __launch_bounds__(kNormBwdWarps * 32)

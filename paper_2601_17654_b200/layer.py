@@ -47,6 +47,7 @@ class LaunchUnit:
     spec: KernelSpec
     fn: Callable[[torch.cuda.Stream], None]
     kind: str = "memory"  # "gemm" | "attention" | "memory"
+    n_kernels: int = 1    # device kernels one call launches
 
 
 @dataclass
@@ -55,6 +56,7 @@ class CommUnit:
     spec: KernelSpec
     fn: Callable[[torch.cuda.Stream, int], None]
     algo_bytes: float = 0.0   # bytes each rank moves over the link (busbw numerator)
+    n_kernels: int = 1
 
 
 @dataclass
@@ -241,7 +243,8 @@ class PartitionedLayer:
             acc = b > 0  # weight gradients accumulate over nanobatches
 
             def U(name, spec, fn, kind="memory"):
-                self.units[(name, b)] = LaunchUnit(name, spec, fn, kind)
+                nk = 3 if name == "attention_bwd" else 1  # pre-pass, main kernel, dq conversion
+                self.units[(name, b)] = LaunchUnit(name, spec, fn, kind, nk)
 
             # ---------------- forward
             U("norm1", _mem_spec("norm1", 4 * T * h + 2 * h + 4 * T, 3 * T * h),
@@ -342,7 +345,8 @@ class PartitionedLayer:
                     self.comm.reduce_scatter(self.dw_sym[1][name], self.dw_shard[name], ncta, stream=st)
 
         label = "+".join(f"{k}_{n}" for k, n in tensors)
-        return CommUnit(label, KernelSpec(label, comm_bytes=max(link, 1.0)), fn, algo_bytes=link)
+        return CommUnit(label, KernelSpec(label, comm_bytes=max(link, 1.0)), fn, algo_bytes=link,
+                        n_kernels=len(ops_))
 
     def _build_programs(self) -> None:
         wl = self.wl

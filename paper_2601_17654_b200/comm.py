@@ -76,13 +76,8 @@ class Communicator:
 
         rank, world = dist.get_rank(group), dist.get_world_size(group)
         device = device or torch.device("cuda", torch.cuda.current_device())
-
-        def exchange(blob: bytes) -> list[bytes]:
-            out = [None] * world
-            dist.all_gather_object(out, blob, group=group)
-            return out
-
-        return cls(rank, world, device, sym_bytes, loopback=False, handles_exchange=exchange)
+        return cls(rank, world, device, sym_bytes, loopback=False,
+                   handles_exchange=lambda blob: exchange_blobs(blob, group))
 
     # ---------------------------------------------------------------- memory
     def alloc(self, nbytes: int, align: int = 256) -> SymRegion:
@@ -152,6 +147,17 @@ class Communicator:
             self.close()
         except Exception:
             pass
+
+
+def exchange_blobs(blob: bytes, group=None) -> list[bytes]:
+    """All-gather one fixed-size IPC-handle blob per rank, in rank order (any backend)."""
+    import torch.distributed as dist
+
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, bytes(blob), group=group)
+    if len({len(b) for b in out}) != 1:
+        raise ValueError("IPC handle blobs differ in size across ranks")
+    return out
 
 
 def _s(stream) -> int:

@@ -50,7 +50,7 @@ class Observation:
 
 class Engine:
     def __init__(self, programs, gpu: GpuModel, device=None, comm=None, clock_control: bool = False,
-                 use_graphs: bool = True, launch_gate: bool = True, measurement_cls=Measurement, group=None):
+                 use_graphs: bool = True, launch_gate: bool = True, measurement_cls=Measurement):
         self.gpu = gpu
         self.device = torch.device(device or "cuda")
         self.comm = comm
@@ -64,7 +64,6 @@ class Engine:
         self.sampler = EnergySampler(self.nvml)
         self.sampler.start()
         self.measurement_cls = measurement_cls
-        self.group = group
         self.last = Observation()
         self._exec_ms: dict[tuple, float] = {}
 
@@ -88,19 +87,6 @@ class Engine:
 
     def default_ncta(self, gpu=None) -> int:
         return int((gpu or self.gpu).sm_bw_saturation)
-
-    # ------------------------------------------------------------------ group reductions
-    def _reduce(self, t_ms: float, e_j: float) -> tuple[float, float]:
-        """Time = max over ranks, energy = sum over ranks."""
-        if self.group is None:
-            return t_ms, e_j
-        import torch.distributed as dist
-
-        v = torch.tensor([t_ms], dtype=torch.float64)
-        w = torch.tensor([e_j], dtype=torch.float64)
-        dist.all_reduce(v, op=dist.ReduceOp.MAX, group=self.group)
-        dist.all_reduce(w, op=dist.ReduceOp.SUM, group=self.group)
-        return float(v), float(w)
 
     # ------------------------------------------------------------------ core window
     def _window(self, prog, config, ncta, warmup_s: float, window_s: float) -> tuple[float, float, int]:
@@ -144,21 +130,27 @@ class Engine:
         """One noise-free execution (reference simulate_schedule)."""
         gpu, prog = self._prepare(partition, config, gpu)
         t_ms, e_j, _ = self._window(prog, config, self.default_ncta(gpu), 0.05, window_s)
-        t_ms, e_j = self._reduce(t_ms, e_j)
         return self.measurement_cls.build(t_ms, e_j - gpu.p_static_w * t_ms / 1e3, gpu.p_static_w)
 
-    def measure(self, partition, config, gpu: GpuModel | None = None, thermal=None, protocol=None, state=None):
-        """Thermally-stable profiling pass (reference measure, simgpu.py:321-364)."""
-        gpu, prog = self._prepare(partition, config, gpu)
-        warmup_s = getattr(protocol, "warmup_s", 2.0)
-        window_s = getattr(protocol, "window_s", 5.0)
-        cooldown_s = getattr(protocol, "cooldown_s", 5.0)
-        t_ms, e_j, _ = self._window(prog, config, self.default_ncta(gpu), warmup_s, window_s)
-        t_ms, e_j = self._reduce(t_ms, e_j)
+    def measure_local(self, name: str, config, warmup_s: float, window_s: float, cooldown_s: float,
+                      ncta: int | None = None) -> tuple[float, float, float]:
+        """This rank's (time_ms, energy_j per execution, temperature) for a registered program;
+        the SPMD driver (spmd.py) combines ranks."""
+        prog = self.programs[name]
+        self.freq.set(config.frequency_mhz)
+        t_ms, e_j, _ = self._window(prog, config, ncta or self.default_ncta(), warmup_s, window_s)
         if cooldown_s > 0:
             time.sleep(cooldown_s)
         temp = self.nvml.temperature_c()
         self.last.temperature_c = temp
+        return t_ms, e_j, temp
+
+    def measure(self, partition, config, gpu: GpuModel | None = None, thermal=None, protocol=None, state=None):
+        """Thermally-stable profiling pass (reference measure, simgpu.py:321-364)."""
+        gpu, prog = self._prepare(partition, config, gpu)
+        t_ms, e_j, temp = self.measure_local(prog.name, config, getattr(protocol, "warmup_s", 2.0),
+                                             getattr(protocol, "window_s", 5.0), getattr(protocol, "cooldown_s", 5.0),
+                                             self.default_ncta(gpu))
         if state is not None:
             state.temperature_c = temp
         return self.measurement_cls.build(t_ms, e_j - gpu.p_static_w * t_ms / 1e3, gpu.p_static_w)
@@ -175,24 +167,13 @@ class Engine:
         return simulate_schedule
 
 
-def install(engine: Engine, schedfront_module=None) -> dict:
+def install(engine, schedfront_module=None):
     """Swap the reference's hot path for `engine` (mbo.py:30,291; oracle.py:24; compose.py:29).
-    Returns the previous bindings so callers can restore them."""
-    if schedfront_module is None:
-        import schedfront as schedfront_module  # noqa: F401
-    import importlib
+    Returns a function restoring the previous bindings."""
+    from .compat import patch_reference, reference_measurement_cls
 
-    mbo = importlib.import_module(schedfront_module.__name__ + ".mbo")
-    oracle = importlib.import_module(schedfront_module.__name__ + ".oracle")
-    compose = importlib.import_module(schedfront_module.__name__ + ".compose")
-    dom = importlib.import_module(schedfront_module.__name__ + ".domain")
-    engine.measurement_cls = dom.Measurement
-    prev = {"mbo.measure": mbo.measure, "oracle.simulate_schedule": oracle.simulate_schedule,
-            "compose.simulate_schedule": compose.simulate_schedule}
-    mbo.measure = engine.measure_fn()
-    oracle.simulate_schedule = engine.simulate_fn()
-    compose.simulate_schedule = engine.simulate_fn()
-    return prev
+    engine.measurement_cls = reference_measurement_cls(schedfront_module)
+    return patch_reference(engine.measure_fn(), engine.simulate_fn(), schedfront_module)
 
 
 __all__ = ["Engine", "Observation", "install", "InvalidConfigError", "math"]

@@ -33,7 +33,7 @@ from typing import Callable
 
 import torch
 
-from . import ops
+from . import ops, specs
 from .comm import Communicator
 from .domain import KernelSpec, PartitionSpec
 from .model import Workload
@@ -68,14 +68,6 @@ class PartitionProgram:
 
     def spec(self) -> PartitionSpec:
         return PartitionSpec(tuple(u.spec for u in self.units), self.comm.spec, self.comm_group_size, self.name)
-
-
-def _gemm_spec(name, M, N, K):
-    return KernelSpec(name, flops=2.0 * M * N * K, bytes=2.0 * (M * K + N * K + M * N))
-
-
-def _mem_spec(name, nbytes, flops=0.0):
-    return KernelSpec(name, flops=float(flops), bytes=float(nbytes))
 
 
 class PartitionedLayer:
@@ -215,176 +207,123 @@ class PartitionedLayer:
 
     def _build_units(self) -> None:
         wl = self.wl
-        T, h, d, hq, hkv, f = wl.tokens, wl.h, wl.d, wl.hq, wl.hkv, wl.ffn
+        T, h, d, hq, hkv = wl.tokens, wl.h, wl.d, wl.hq, wl.hkv
         qd = (hq + hkv) * d
         scale = 1.0 / math.sqrt(d)
         eps, theta = wl.model.norm_eps, wl.model.rope_theta
         tp = wl.parallel == "tp"
         rank0 = self.rank == 0
-        W = self.w
+        W, dw = self.w, self.dw
+        US = specs.unit_specs(wl)
         self.units: dict[tuple[str, int], LaunchUnit] = {}
-        attn_flops = 2.0 * T * T * hq * d  # causal: 4*T^2*hq*d / 2
+        kinds = {"attention_core": "attention", "attention_bwd": "attention"}
 
         for b in range(wl.nanobatches):
             a = self.nb[b]
-            ga = self.sched.slot
             # partial-sum outputs of row-parallel GEMMs (TP) live in the symmetric buffer
             if tp:
-                hp = self.partial[b % 2][("hp", b)].local().view(T, h)
-                yp = self.partial[b % 2][("yp", b)].local().view(T, h)
-                dxn2p = self.partial[b % 2][("dxn2p", b)].local().view(T, h)
-                dxn1p = self.partial[b % 2][("dxn1p", b)].local().view(T, h)
+                hp, yp, dxn2p, dxn1p = (self.partial[b % 2][(k, b)].local().view(T, h)
+                                        for k in ("hp", "yp", "dxn2p", "dxn1p"))
             else:
                 hp, yp, dxn2p, dxn1p = a["h"], a["y"], a["dxn2"], a["dxn1"]
-            a["hp"], a["yp"], a["dxn2p_t"], a["dxn1p_t"] = hp, yp, dxn2p, dxn1p
+            a["hp"], a["yp"] = hp, yp
             res_attn = a["x"] if (not tp or rank0) else None
             res_mlp = a["h"] if (not tp or rank0) else None
-            s = {k: ga() for k in ("qkv", "o", "gu", "d", "dd", "dwd", "dgu", "dwgu", "do", "dwo", "dqkv", "dwqkv")}
-            acc = b > 0  # weight gradients accumulate over nanobatches
-
-            def U(name, spec, fn, kind="memory"):
+            s = {k: self.sched.slot() for k in US if k in specs.GEMM_UNITS}
+            acc = b > 0  # weight gradients accumulate over nanobatches (epilogue C input)
+            fns = {
+                # ---------------- forward
+                "norm1": lambda st, a=a: ops.rmsnorm_fwd(a["x"], W["g1"], a["xn1"], a["rstd1"], eps, stream=st),
+                "linear_qkv": lambda st, a=a, s=s: ops.linear(a["xn1"], W["wqkv"], a["qkv"], sched=s["linear_qkv"],
+                                                              stream=st),
+                "rope": lambda st, a=a: ops.rope(a["qkv"], a["qkr"], hq + hkv, d, theta, stream=st),
+                "attention_core": lambda st, a=a: ops.attn_fwd(a["qkr"][:, :hq * d], a["qkr"][:, hq * d:],
+                                                               a["qkv"][:, qd:], a["ao"], a["lse"], T, hq, hkv, d,
+                                                               scale, stream=st),
+                "linear_proj": lambda st, a=a, s=s, hp=hp, r=res_attn: ops.linear(
+                    a["ao"], W["wo"], hp, residual=r, sched=s["linear_proj"], stream=st),
+                "norm2": lambda st, a=a: ops.rmsnorm_fwd(a["h"], W["g2"], a["xn2"], a["rstd2"], eps, stream=st),
+                "linear_up": lambda st, a=a, s=s: ops.linear(a["xn2"], W["wgu"], a["gu"], sched=s["linear_up"],
+                                                             stream=st),
+                "swiglu": lambda st, a=a: ops.swiglu_fwd(a["gu"], a["act"], stream=st),
+                "linear_down": lambda st, a=a, s=s, yp=yp, r=res_mlp: ops.linear(
+                    a["act"], W["wd"], yp, residual=r, sched=s["linear_down"], stream=st),
+                # ---------------- backward
+                "norm1_bwd": lambda st, a=a: ops.rmsnorm_bwd(a["dxn1"], a["x"], W["g1"], a["rstd1"], a["dx"],
+                                                             a["dwp1"], dres=a["dh"], stream=st),
+                "down_dgrad": lambda st, a=a, s=s: ops.linear_dgrad(a["dy"], W["wd"], a["dact"],
+                                                                    sched=s["down_dgrad"], stream=st),
+                "down_wgrad": lambda st, a=a, s=s, acc=acc: ops.linear_wgrad(
+                    a["dy"], a["act"], dw["wd"], accumulate=dw["wd"] if acc else None, sched=s["down_wgrad"],
+                    stream=st),
+                "swiglu_bwd": lambda st, a=a: ops.swiglu_bwd(a["dact"], a["gu"], a["dgu"], stream=st),
+                "gu_dgrad": lambda st, a=a, s=s, o=dxn2p: ops.linear_dgrad(a["dgu"], W["wgu"], o,
+                                                                           sched=s["gu_dgrad"], stream=st),
+                "gu_wgrad": lambda st, a=a, s=s, acc=acc: ops.linear_wgrad(
+                    a["dgu"], a["xn2"], dw["wgu"], accumulate=dw["wgu"] if acc else None, sched=s["gu_wgrad"],
+                    stream=st),
+                "norm2_bwd": lambda st, a=a: ops.rmsnorm_bwd(a["dxn2"], a["h"], W["g2"], a["rstd2"], a["dh"],
+                                                             a["dwp2"], dres=a["dy"], stream=st),
+                "o_dgrad": lambda st, a=a, s=s: ops.linear_dgrad(a["dh"], W["wo"], a["dao"], sched=s["o_dgrad"],
+                                                                 stream=st),
+                "o_wgrad": lambda st, a=a, s=s, acc=acc: ops.linear_wgrad(
+                    a["dh"], a["ao"], dw["wo"], accumulate=dw["wo"] if acc else None, sched=s["o_wgrad"], stream=st),
+                "attention_bwd": lambda st, a=a: ops.attn_bwd(
+                    a["qkr"][:, :hq * d], a["qkr"][:, hq * d:], a["qkv"][:, qd:], a["ao"], a["dao"], a["lse"],
+                    a["dqkr"][:, :hq * d], a["dqkr"][:, hq * d:], a["dqkv"][:, qd:], T, hq, hkv, d, scale,
+                    self.attn_ws, stream=st),
+                "rope_bwd": lambda st, a=a: ops.rope(a["dqkr"], a["dqkv"], hq + hkv, d, theta, inverse=True,
+                                                     stream=st),
+                "qkv_dgrad": lambda st, a=a, s=s, o=dxn1p: ops.linear_dgrad(a["dqkv"], W["wqkv"], o,
+                                                                            sched=s["qkv_dgrad"], stream=st),
+                "qkv_wgrad": lambda st, a=a, s=s, acc=acc: ops.linear_wgrad(
+                    a["dqkv"], a["xn1"], dw["wqkv"], accumulate=dw["wqkv"] if acc else None, sched=s["qkv_wgrad"],
+                    stream=st),
+            }
+            for name, fn in fns.items():
+                kind = "gemm" if name in specs.GEMM_UNITS else kinds.get(name, "memory")
                 nk = 3 if name == "attention_bwd" else 1  # pre-pass, main kernel, dq conversion
-                self.units[(name, b)] = LaunchUnit(name, spec, fn, kind, nk)
-
-            # ---------------- forward
-            U("norm1", _mem_spec("norm1", 4 * T * h + 2 * h + 4 * T, 3 * T * h),
-              lambda st, a=a: ops.rmsnorm_fwd(a["x"], W["g1"], a["xn1"], a["rstd1"], eps, stream=st))
-            U("linear_qkv", _gemm_spec("linear_qkv", T, wl.qkv_dim, h),
-              lambda st, a=a, s=s: ops.linear(a["xn1"], W["wqkv"], a["qkv"], sched=s["qkv"], stream=st), "gemm")
-            U("rope", _mem_spec("rope", 4 * T * qd, 6 * T * qd),
-              lambda st, a=a: ops.rope(a["qkv"], a["qkr"], hq + hkv, d, theta, stream=st))
-            U("attention_core", KernelSpec("attention_core", flops=attn_flops, bytes=2.0 * T * (2 * hq + 2 * hkv) * d),
-              lambda st, a=a: ops.attn_fwd(a["qkr"][:, :hq * d], a["qkr"][:, hq * d:], a["qkv"][:, qd:], a["ao"],
-                                           a["lse"], T, hq, hkv, d, scale, stream=st), "attention")
-            U("linear_proj", _gemm_spec("linear_proj", T, h, hq * d),
-              lambda st, a=a, s=s, hp=hp, r=res_attn: ops.linear(a["ao"], W["wo"], hp, residual=r, sched=s["o"],
-                                                                 stream=st), "gemm")
-            U("norm2", _mem_spec("norm2", 4 * T * h + 2 * h + 4 * T, 3 * T * h),
-              lambda st, a=a: ops.rmsnorm_fwd(a["h"], W["g2"], a["xn2"], a["rstd2"], eps, stream=st))
-            U("linear_up", _gemm_spec("linear_up", T, 2 * f, h),
-              lambda st, a=a, s=s: ops.linear(a["xn2"], W["wgu"], a["gu"], sched=s["gu"], stream=st), "gemm")
-            U("swiglu", _mem_spec("swiglu", 2 * T * 3 * f, 4 * T * f),
-              lambda st, a=a: ops.swiglu_fwd(a["gu"], a["act"], stream=st))
-            U("linear_down", _gemm_spec("linear_down", T, h, f),
-              lambda st, a=a, s=s, yp=yp, r=res_mlp: ops.linear(a["act"], W["wd"], yp, residual=r, sched=s["d"],
-                                                                stream=st), "gemm")
-            # ---------------- backward (dW accumulate over nanobatches through the epilogue C input)
-            dw = self.dw
-            U("norm1_bwd", _mem_spec("norm1_bwd", 2 * 5 * T * h, 8 * T * h),
-              lambda st, a=a: ops.rmsnorm_bwd(a["dxn1"], a["x"], W["g1"], a["rstd1"], a["dx"], a["dwp1"],
-                                              dres=a["dh"], stream=st))
-            U("down_dgrad", _gemm_spec("down_dgrad", T, f, h),
-              lambda st, a=a, s=s: ops.linear_dgrad(a["dy"], W["wd"], a["dact"], sched=s["dd"], stream=st), "gemm")
-            U("down_wgrad", _gemm_spec("down_wgrad", h, f, T),
-              lambda st, a=a, s=s, acc=acc: ops.linear_wgrad(a["dy"], a["act"], dw["wd"],
-                                                             accumulate=dw["wd"] if acc else None, sched=s["dwd"],
-                                                             stream=st), "gemm")
-            U("swiglu_bwd", _mem_spec("swiglu_bwd", 2 * T * 5 * f, 10 * T * f),
-              lambda st, a=a: ops.swiglu_bwd(a["dact"], a["gu"], a["dgu"], stream=st))
-            U("gu_dgrad", _gemm_spec("gu_dgrad", T, h, 2 * f),
-              lambda st, a=a, s=s, o=dxn2p: ops.linear_dgrad(a["dgu"], W["wgu"], o, sched=s["dgu"], stream=st), "gemm")
-            U("gu_wgrad", _gemm_spec("gu_wgrad", 2 * f, h, T),
-              lambda st, a=a, s=s, acc=acc: ops.linear_wgrad(a["dgu"], a["xn2"], dw["wgu"],
-                                                             accumulate=dw["wgu"] if acc else None, sched=s["dwgu"],
-                                                             stream=st), "gemm")
-            U("norm2_bwd", _mem_spec("norm2_bwd", 2 * 5 * T * h, 8 * T * h),
-              lambda st, a=a: ops.rmsnorm_bwd(a["dxn2"], a["h"], W["g2"], a["rstd2"], a["dh"], a["dwp2"],
-                                              dres=a["dy"], stream=st))
-            U("o_dgrad", _gemm_spec("o_dgrad", T, hq * d, h),
-              lambda st, a=a, s=s: ops.linear_dgrad(a["dh"], W["wo"], a["dao"], sched=s["do"], stream=st), "gemm")
-            U("o_wgrad", _gemm_spec("o_wgrad", h, hq * d, T),
-              lambda st, a=a, s=s, acc=acc: ops.linear_wgrad(a["dh"], a["ao"], dw["wo"],
-                                                             accumulate=dw["wo"] if acc else None, sched=s["dwo"],
-                                                             stream=st), "gemm")
-            U("attention_bwd", KernelSpec("attention_bwd", flops=2.5 * attn_flops,
-                                          bytes=2.0 * T * (4 * hq + 4 * hkv) * d + 8.0 * T * hq * d),
-              lambda st, a=a: ops.attn_bwd(a["qkr"][:, :hq * d], a["qkr"][:, hq * d:], a["qkv"][:, qd:], a["ao"],
-                                           a["dao"], a["lse"], a["dqkr"][:, :hq * d], a["dqkr"][:, hq * d:],
-                                           a["dqkv"][:, qd:], T, hq, hkv, d, scale, self.attn_ws, stream=st),
-              "attention")
-            U("rope_bwd", _mem_spec("rope_bwd", 4 * T * qd, 6 * T * qd),
-              lambda st, a=a: ops.rope(a["dqkr"], a["dqkv"], hq + hkv, d, theta, inverse=True, stream=st))
-            U("qkv_dgrad", _gemm_spec("qkv_dgrad", T, h, wl.qkv_dim),
-              lambda st, a=a, s=s, o=dxn1p: ops.linear_dgrad(a["dqkv"], W["wqkv"], o, sched=s["dqkv"], stream=st),
-              "gemm")
-            U("qkv_wgrad", _gemm_spec("qkv_wgrad", wl.qkv_dim, h, T),
-              lambda st, a=a, s=s, acc=acc: ops.linear_wgrad(a["dqkv"], a["xn1"], dw["wqkv"],
-                                                             accumulate=dw["wqkv"] if acc else None, sched=s["dwqkv"],
-                                                             stream=st), "gemm")
+                self.units[(name, b)] = LaunchUnit(name, US[name], fn, kind, nk)
 
     # ------------------------------------------------------------------ comm units
     def _ar_unit(self, src_key: tuple[str, int], out: torch.Tensor) -> CommUnit:
         name, b = src_key
         reg = self.partial[b % 2][src_key]
-        T, h, W = self.wl.tokens, self.wl.h, self.world
-        nbytes = T * h * 2
-        link = 2.0 * (W - 1) / W * nbytes  # bytes each rank sends (= receives) over the link
+        spec, link = specs.ar_spec(self.wl, src_key)
 
         def fn(st, ncta, reg=reg, out=out):
             self.comm.all_reduce(reg, self.stage, out, ncta, stream=st)
 
-        return CommUnit(f"allreduce_{name}{b}", KernelSpec(f"allreduce_{name}{b}", comm_bytes=max(link, 1.0)), fn,
-                        algo_bytes=link)
+        return CommUnit(spec.name, spec, fn, algo_bytes=link)
 
     def _fsdp_unit(self, tensors: list[tuple[str, str]]) -> CommUnit:
-        """Fused comm unit: ('rs', name) reduce-scatters the previous layer's gradient of `name`,
-        ('ag', name) all-gathers the next layer's weight `name`."""
-        W = self.world
-        link = 0.0
-        ops_ = []
-        for kind, name in tensors:
-            n = self.w[name].numel()
-            link += (W - 1) / W * n * 2
-            ops_.append((kind, name))
+        spec, link = specs.fsdp_spec(self.wl, tensors)
 
         def fn(st, ncta):
-            for kind, name in ops_:
+            for kind, name in tensors:
                 if kind == "ag":
                     self.comm.all_gather(self.shard[name], self.w_next[name], ncta, stream=st)
                 else:
                     self.comm.reduce_scatter(self.dw_sym[1][name], self.dw_shard[name], ncta, stream=st)
 
-        label = "+".join(f"{k}_{n}" for k, n in tensors)
-        return CommUnit(label, KernelSpec(label, comm_bytes=max(link, 1.0)), fn, algo_bytes=link,
-                        n_kernels=len(ops_))
+        return CommUnit(spec.name, spec, fn, algo_bytes=link, n_kernels=len(tensors))
 
     def _build_programs(self) -> None:
         wl = self.wl
-        g = wl.world
-        fwd_attn = ["norm1", "linear_qkv", "rope", "attention_core", "linear_proj"]
-        fwd_mlp = ["norm2", "linear_up", "swiglu", "linear_down"]
-        bwd_mlp = ["norm1_bwd", "down_dgrad", "down_wgrad", "swiglu_bwd", "gu_dgrad", "gu_wgrad"]
-        bwd_attn = ["norm2_bwd", "o_dgrad", "o_wgrad", "attention_bwd", "rope_bwd", "qkv_dgrad", "qkv_wgrad"]
-        nb = wl.nanobatches
-        assert nb == 2, "partition programs are built for 2 nanobatches"
-        blocks = [("fwd_attn", fwd_attn), ("fwd_mlp", fwd_mlp), ("bwd_mlp", bwd_mlp), ("bwd_attn", bwd_attn)]
-        if wl.parallel == "tp":
-            # comm of each partition = all-reduce of the previous partition's partial output
-            produced = {"fwd_attn": "hp", "fwd_mlp": "yp", "bwd_mlp": "dxn2p", "bwd_attn": "dxn1p"}
-            consumer_out = {"hp": "h", "yp": "y", "dxn2p": "dxn2", "dxn1p": "dxn1"}
-            seq = [(blk, b) for blk, _ in blocks[:2] for b in range(nb)] + [(blk, b) for blk, _ in blocks[2:]
-                                                                             for b in range(nb)]
-            for i, (blk, b) in enumerate(seq):
-                pblk, pb = seq[i - 1]  # i == 0 wraps to the last partition (steady state)
-                src = (produced[pblk], pb)
-                comm = self._ar_unit(src, self.nb[pb][consumer_out[produced[pblk]]])
-                units = [self.units[(k, b)] for k in dict(blocks)[blk]]
-                name = f"{blk}{b}"
-                self.programs[name] = PartitionProgram(name, units, comm, g)
-                self.order.append(name)
-        else:
-            comms = {
-                ("fwd_attn", 0): [("ag", "wqkv")], ("fwd_attn", 1): [("ag", "wo")],
-                ("fwd_mlp", 0): [("ag", "wgu")], ("fwd_mlp", 1): [("ag", "wd")],
-                ("bwd_mlp", 0): [("rs", "wd"), ("ag", "wd")], ("bwd_mlp", 1): [("rs", "wgu"), ("ag", "wgu")],
-                ("bwd_attn", 0): [("rs", "wo"), ("ag", "wo")], ("bwd_attn", 1): [("rs", "wqkv"), ("ag", "wqkv")],
-            }
-            for blk, names in blocks:
-                for b in range(nb):
-                    units = [self.units[(k, b)] for k in names]
-                    name = f"{blk}{b}"
-                    self.programs[name] = PartitionProgram(name, units, self._fsdp_unit(comms[(blk, b)]), g)
-                    self.order.append(name)
+        if wl.nanobatches != 2:
+            raise ValueError("partition programs are built for 2 nanobatches")
+        out_of = {"hp": "h", "yp": "y", "dxn2p": "dxn2", "dxn1p": "dxn1"}
+        plan = specs.comm_plan(wl)
+        for blk, b in specs.partition_order(wl):
+            name = f"{blk}{b}"
+            kind, arg = plan[name]
+            if kind == "ar":
+                comm = self._ar_unit(arg, self.nb[arg[1]][out_of[arg[0]]])
+            else:
+                comm = self._fsdp_unit(arg)
+            units = [self.units[(k, b)] for k in dict(specs.BLOCKS)[blk]]
+            self.programs[name] = PartitionProgram(name, units, comm, wl.world)
+            self.order.append(name)
 
     # ------------------------------------------------------------------ helpers
     def finalize_norm_grads(self, stream=None) -> None:

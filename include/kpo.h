@@ -92,6 +92,11 @@ int kpo_gemm(const void* A, const void* B, void* D, const void* C, int64_t M, in
 int kpo_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int64_t T, int hq,
                  int hkv, int d, int64_t q_stride, int64_t k_stride, int64_t v_stride, int64_t o_stride,
                  float scale, int causal, void* stream);
+/* The round-1 warp-level (mma.sync) forward, kept as a cross-check / A-B baseline for the
+ * tcgen05 kernel behind kpo_attn_fwd.  Same arguments. */
+int kpo_attn_fwd_mma(const void* q, const void* k, const void* v, void* o, float* lse, int64_t T, int hq,
+                     int hkv, int d, int64_t q_stride, int64_t k_stride, int64_t v_stride, int64_t o_stride,
+                     float scale, int causal, void* stream);
 /* dq/dk/dv: same layouts as q/k/v (strides dq_stride, dk_stride, dv_stride).
  * workspace: fp32 scratch of kpo_attn_bwd_workspace_bytes(). */
 int64_t kpo_attn_bwd_workspace_bytes(int64_t T, int hq, int hkv, int d);

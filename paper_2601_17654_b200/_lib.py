@@ -45,6 +45,8 @@ SIGNATURES = {
                         _i64, _i32, _c_void_p, _c_void_p]),
     "kpo_attn_fwd": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _i64, _i32, _i32, _i32,
                             _i64, _i64, _i64, _i64, _f32, _i32, _c_void_p]),
+    "kpo_attn_fwd_mma": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _i64, _i32, _i32, _i32,
+                                _i64, _i64, _i64, _i64, _f32, _i32, _c_void_p]),
     "kpo_attn_bwd_workspace_bytes": (_i64, [_i64, _i32, _i32, _i32]),
     "kpo_attn_bwd": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p,
                             _c_void_p, _c_void_p, _i64, _i32, _i32, _i32, _i64, _i64, _i64, _i64, _i64, _i64,

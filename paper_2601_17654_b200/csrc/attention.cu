@@ -10,6 +10,15 @@
 #include "common.cuh"
 
 namespace kpo {
+int attn_fwd_tcgen05(const void* q, const void* k, const void* v, void* o, float* lse, int64_t T, int hq, int hkv,
+                     int d, int64_t qs, int64_t ks, int64_t vs, int64_t os, float scale, int causal, cudaStream_t st);
+int attn_bwd_tcgen05_main(const void* q, const void* k, const void* v, const void* dout, const float* lse,
+                          const float* dvec, float* dq_acc, void* dk, void* dv, int64_t T, int hq, int hkv, int d,
+                          int64_t qs, int64_t ks, int64_t vs, int64_t os, int64_t dks, int64_t dvs, float scale,
+                          int causal, cudaStream_t st);
+}
+
+namespace kpo {
 namespace attn {
 
 __device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -510,7 +519,7 @@ template <int D>
 static int bwd_launch(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse,
                       void* dq, void* dk, void* dv, int64_t T, int hq, int hkv, int64_t qs, int64_t ks, int64_t vs,
                       int64_t os, int64_t dqs, int64_t dks, int64_t dvs, float scale, int causal, void* ws,
-                      cudaStream_t s) {
+                      cudaStream_t s, bool use_tc) {
   using CF = BwdCfg<D>;
   float* dq_acc = (float*)ws;
   float* dvec = dq_acc + T * hq * D;
@@ -520,6 +529,11 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* o
         (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, dvec, dq_acc, (int)T, hq, os);
     KPO_LAUNCH_CHECK();
   }
+  if (D == 128 && use_tc) {
+    int st = attn_bwd_tcgen05_main(q, k, v, dout, lse, dvec, dq_acc, dk, dv, T, hq, hkv, D, qs, ks, vs, os, dks, dvs,
+                                   scale, causal, s);
+    if (st) return st;
+  } else {
   static bool set = false;
   if (!set) {
     KPO_CUDA(cudaFuncSetAttribute(attn_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
@@ -530,6 +544,7 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* o
       (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, (const __nv_bfloat16*)v, (const __nv_bfloat16*)dout, lse, dvec,
       dq_acc, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, (int)T, hq, hkv, qs, ks, vs, os, dks, dvs, scale, causal);
   KPO_LAUNCH_CHECK();
+  }
   {
     const int64_t n = T * hq * D / 8;
     attn_bwd_post_kernel<D><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dq_acc, (__nv_bfloat16*)dq, (int)T, hq, dqs);
@@ -554,6 +569,17 @@ extern "C" int kpo_attn_fwd(const void* q, const void* k, const void* v, void* o
   KPO_CHECK_ARG(attn_args_ok(T, hq, hkv, d), "attn_fwd: need hq %% hkv == 0 and head_dim in {64, 128}");
   KPO_CHECK_ARG(q_stride % 8 == 0 && k_stride % 8 == 0 && v_stride % 8 == 0 && o_stride % 8 == 0,
                 "attn_fwd: token strides must be multiples of 8");
+  KPO_CHECK_ARG(((uintptr_t)q & 15) == 0 && ((uintptr_t)k & 15) == 0 && ((uintptr_t)v & 15) == 0,
+                "attn_fwd: q/k/v must be 16B aligned (TMA)");
+  return attn_fwd_tcgen05(q, k, v, o, lse, T, hq, hkv, d, q_stride, k_stride, v_stride, o_stride, scale, causal,
+                          (cudaStream_t)stream);
+}
+
+extern "C" int kpo_attn_fwd_mma(const void* q, const void* k, const void* v, void* o, float* lse, int64_t T, int hq,
+                                int hkv, int d, int64_t q_stride, int64_t k_stride, int64_t v_stride, int64_t o_stride,
+                                float scale, int causal, void* stream) {
+  KPO_CHECK_ARG(q && k && v && o && lse, "attn_fwd_mma: null pointer");
+  KPO_CHECK_ARG(attn_args_ok(T, hq, hkv, d), "attn_fwd_mma: need hq %% hkv == 0 and head_dim in {64, 128}");
   cudaStream_t s = (cudaStream_t)stream;
   if (d == 128)
     return attn::fwd_launch<128>(q, k, v, o, lse, T, hq, hkv, q_stride, k_stride, v_stride, o_stride, scale, causal, s);
@@ -576,7 +602,7 @@ extern "C" int kpo_attn_bwd(const void* q, const void* k, const void* v, const v
   cudaStream_t s = (cudaStream_t)stream;
   if (d == 128)
     return attn::bwd_launch<128>(q, k, v, o, dout, lse, dq, dk, dv, T, hq, hkv, q_stride, k_stride, v_stride,
-                                 o_stride, dq_stride, dk_stride, dv_stride, scale, causal, workspace, s);
+                                 o_stride, dq_stride, dk_stride, dv_stride, scale, causal, workspace, s, true);
   return attn::bwd_launch<64>(q, k, v, o, dout, lse, dq, dk, dv, T, hq, hkv, q_stride, k_stride, v_stride, o_stride,
-                              dq_stride, dk_stride, dv_stride, scale, causal, workspace, s);
+                              dq_stride, dk_stride, dv_stride, scale, causal, workspace, s, false);
 }

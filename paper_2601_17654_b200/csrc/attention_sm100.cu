@@ -1,0 +1,612 @@
+// attention_sm100.cu — causal GQA flash attention on the 5th-gen tensor cores (tcgen05 + TMEM + TMA).
+//
+// Replaces the reference's abstract "attention_core" kernel (workloads.py:47).  Forward, one CTA =
+// 128 query rows of one q head, 128-key tiles:
+//   warp 0     TMA producer: Q once, then K_j / V_j into a 2-stage smem ring (128B swizzle)
+//   warp 1     TMEM allocator + single-thread tcgen05.mma issuer:
+//                S_j = Q K_j^T  -> TMEM (double-buffered, 2 x 128 columns)
+//                O  += P_j V_j  -> TMEM (D columns), P_j from smem, V_j MN-major from smem
+//   warps 2-5  softmax: one thread owns one query row (its TMEM lane), so row max / row sum need
+//              no shuffles; P_j is written to smem in the UMMA K-major SW128 layout; O is rescaled
+//              in TMEM only when the running max grows by more than 2^8 (lazy rescaling), then
+//              normalised, converted and stored at the end together with the log-sum-exp.
+// The issue order S_0, S_1, PV_0, S_2, PV_1, ... lets the softmax of tile j overlap the tensor
+// core's work on tiles j+1 / j-1.
+#include "sm100.cuh"
+
+namespace kpo {
+namespace attn_tc {
+using namespace kpo::sm100;
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr int kThreads = 192;
+
+template <int D>
+struct Fwd {
+  static constexpr int BM = 128, BN = 128, STAGES = 2;
+  static constexpr int Q_BYTES = BM * D * 2;  // D/64 sub-tiles of [128 rows x 64] (16 KB each)
+  static constexpr int KV_BYTES = BN * D * 2;
+  static constexpr int P_BYTES = BM * BN * 2;  // 2 sub-tiles of [128 q x 64 keys]
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = OFF_Q + Q_BYTES;
+  static constexpr int OFF_V = OFF_K + STAGES * KV_BYTES;
+  static constexpr int OFF_P = OFF_V + STAGES * KV_BYTES;
+  static constexpr int OFF_BAR = OFF_P + P_BYTES;
+  static constexpr int SMEM_RAW = OFF_BAR + 256 + 1024;
+  // keep one CTA per SM (the kernel allocates all 512 TMEM columns)
+  static constexpr int SMEM = SMEM_RAW > 120 * 1024 ? SMEM_RAW : 120 * 1024;
+  static constexpr int TMEM_COLS = 512;
+  static constexpr int COL_S0 = 0, COL_S1 = 128, COL_O = 256;
+};
+
+// byte offset of the 16-byte chunk `chunk` (0..7) of row `r` in a [rows x 64] bf16 SW128 sub-tile
+__device__ __forceinline__ uint32_t sw128(int r, int chunk) {
+  return (uint32_t)(r * 128 + ((chunk ^ (r & 7)) << 4));
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                       const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ o, float* __restrict__ lse,
+                       int T, int hq, int hkv, int64_t os, float scale_log2, int causal) {
+  using C = Fwd<D>;
+  constexpr int BM = C::BM, BN = C::BN, KSUB = D / 64;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* q_full = bar + 0;
+  uint64_t* kv_full = bar + 1;   // [2]
+  uint64_t* kv_empty = bar + 3;  // [2]
+  uint64_t* s_full = bar + 5;    // [2]
+  uint64_t* s_empty = bar + 7;   // [2]
+  uint64_t* p_full = bar + 9;
+  uint64_t* pv_done = bar + 10;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mblk = gridDim.x - 1 - blockIdx.x;  // heavy (late) causal rows first
+  const int h = blockIdx.y;
+  const int kvh = h / (hq / hkv);
+  const int m0 = mblk * BM;
+  int n_tiles = (T + BN - 1) / BN;
+  if (causal) n_tiles = min(n_tiles, (m0 + BM + BN - 1) / BN);
+
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(q_full), 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&kv_full[i]), 1);
+      mbar_init(smem_u32(&kv_empty[i]), 1);
+      mbar_init(smem_u32(&s_full[i]), 1);
+      mbar_init(smem_u32(&s_empty[i]), 4);
+    }
+    mbar_init(smem_u32(p_full), 4);
+    mbar_init(smem_u32(pv_done), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc(smem_u32(tmem_slot), C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sQ = smem_u32(smem + C::OFF_Q), sK = smem_u32(smem + C::OFF_K);
+  const uint32_t sV = smem_u32(smem + C::OFF_V), sP = smem_u32(smem + C::OFF_P);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------------------------------------------------------- TMA producer
+      mbar_arrive_expect_tx(smem_u32(q_full), C::Q_BYTES);
+#pragma unroll
+      for (int kb = 0; kb < KSUB; ++kb) tma_load_2d(sQ + kb * BM * 128, &tmQ, smem_u32(q_full), h * D + kb * 64, m0);
+      for (int j = 0; j < n_tiles; ++j) {
+        const int s = j & 1;
+        mbar_wait(smem_u32(&kv_empty[s]), ((j >> 1) & 1) ^ 1);
+        const uint32_t fb = smem_u32(&kv_full[s]);
+        mbar_arrive_expect_tx(fb, 2 * C::KV_BYTES);
+#pragma unroll
+        for (int kb = 0; kb < KSUB; ++kb) {
+          tma_load_2d(sK + s * C::KV_BYTES + kb * BN * 128, &tmK, fb, kvh * D + kb * 64, j * BN);
+          tma_load_2d(sV + s * C::KV_BYTES + kb * BN * 128, &tmV, fb, kvh * D + kb * 64, j * BN);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------------------------------------------------------- MMA issuer
+      constexpr uint32_t ID_S = idesc_bf16(BM, BN, false, false);
+      constexpr uint32_t ID_O = idesc_bf16(BM, D, false, true);
+      mbar_wait(smem_u32(q_full), 0);
+      auto issue_pv = [&](int i) {
+        mbar_wait(smem_u32(p_full), i & 1);
+        tc_fence_after();
+        const uint32_t vb = sV + (i & 1) * C::KV_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < BN / 16; ++kk) {  // 16 keys per UMMA
+          const uint64_t da = smem_desc(sP + (kk >> 2) * BM * 128 + (kk & 3) * 32, 16, 1024);
+          const uint64_t db = smem_desc(vb + kk * 2048, BN * 128, 1024);
+          tc_mma(tmem + C::COL_O, da, db, ID_O, (i > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc_commit(smem_u32(pv_done));
+        tc_commit(smem_u32(&kv_empty[i & 1]));
+      };
+      for (int j = 0; j < n_tiles; ++j) {
+        const int s = j & 1;
+        mbar_wait(smem_u32(&kv_full[s]), (j >> 1) & 1);
+        mbar_wait(smem_u32(&s_empty[s]), ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t kb_base = sK + s * C::KV_BYTES;
+        const uint32_t d_s = tmem + (s ? C::COL_S1 : C::COL_S0);
+#pragma unroll
+        for (int kb = 0; kb < KSUB; ++kb) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t da = smem_desc(sQ + kb * BM * 128 + k * 32, 16, 1024);
+            const uint64_t db = smem_desc(kb_base + kb * BN * 128 + k * 32, 16, 1024);
+            tc_mma(d_s, da, db, ID_S, (kb | k) ? 1u : 0u);
+          }
+        }
+        tc_commit(smem_u32(&s_full[s]));
+        if (j > 0) issue_pv(j - 1);
+      }
+      issue_pv(n_tiles - 1);
+    }
+  } else {
+    // ---------------------------------------------------------------- softmax warps 2..5
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;  // query row within the tile == TMEM lane
+    const int q = m0 + r;
+    const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int j = 0; j < n_tiles; ++j) {
+      const int s = j & 1;
+      mbar_wait(smem_u32(&s_full[s]), (j >> 1) & 1);
+      tc_fence_after();
+      float sv[BN];
+      const uint32_t s_addr = lane_addr + (s ? C::COL_S1 : C::COL_S0);
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) tmem_ld32_nowait(s_addr + c * 32, reinterpret_cast<uint32_t*>(sv + c * 32));
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&s_empty[s]));
+      const int k0 = j * BN;
+      const bool mask = (causal && k0 + BN - 1 > m0) || (k0 + BN > T);
+      float mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < BN; ++i) {
+        float x = sv[i] * scale_log2;
+        if (mask) {
+          const int key = k0 + i;
+          if (key >= T || (causal && key > q)) x = -INFINITY;
+        }
+        sv[i] = x;
+        mx = fmaxf(mx, x);
+      }
+      float corr = 1.f;
+      bool rescale = false;
+      if (mx > m_run + 8.f) {  // lazy rescaling: only when the max grows by more than 2^8
+        corr = (m_run == -INFINITY) ? 0.f : ex2(m_run - mx);
+        rescale = (j > 0);
+        m_run = mx;
+      }
+      if (j > 0) mbar_wait(smem_u32(pv_done), (j - 1) & 1);  // P buffer free, O stable
+      if (rescale) {
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t ov[32];
+          tmem_ld32_nowait(lane_addr + C::COL_O + c * 32, ov);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * corr);
+          tmem_st32(lane_addr + C::COL_O + c * 32, ov);
+        }
+        tmem_wait_st();
+      }
+      float lsum = 0.f;
+#pragma unroll
+      for (int ch = 0; ch < BN / 8; ++ch) {  // 16-byte chunks of 8 keys
+        float p[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          p[e] = ex2(sv[ch * 8 + e] - m_run);
+          lsum += p[e];
+        }
+        uint4 u;
+        u.x = pack_bf16x2(p[0], p[1]);
+        u.y = pack_bf16x2(p[2], p[3]);
+        u.z = pack_bf16x2(p[4], p[5]);
+        u.w = pack_bf16x2(p[6], p[7]);
+        const uint32_t addr = sP + (ch >> 3) * BM * 128 + sw128(r, ch & 7);
+        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(u.x), "r"(u.y), "r"(u.z), "r"(u.w)
+                     : "memory");
+      }
+      l_run = l_run * corr + lsum;
+      fence_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(p_full));
+    }
+    // ---------------------------------------------------------------- epilogue
+    mbar_wait(smem_u32(pv_done), (n_tiles - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.f / l_run;
+    const bool row_ok = q < T;
+    __nv_bfloat16* orow = o + (int64_t)q * os + (int64_t)h * D;
+#pragma unroll 1
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t ov[32];
+      tmem_ld32_nowait(lane_addr + C::COL_O + c * 32, ov);
+      tmem_wait_ld();
+      if (row_ok) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          uint4 u;
+          u.x = pack_bf16x2(__uint_as_float(ov[v * 8 + 0]) * inv, __uint_as_float(ov[v * 8 + 1]) * inv);
+          u.y = pack_bf16x2(__uint_as_float(ov[v * 8 + 2]) * inv, __uint_as_float(ov[v * 8 + 3]) * inv);
+          u.z = pack_bf16x2(__uint_as_float(ov[v * 8 + 4]) * inv, __uint_as_float(ov[v * 8 + 5]) * inv);
+          u.w = pack_bf16x2(__uint_as_float(ov[v * 8 + 6]) * inv, __uint_as_float(ov[v * 8 + 7]) * inv);
+          *reinterpret_cast<uint4*>(orow + c * 32 + v * 8) = u;
+        }
+      }
+    }
+    if (row_ok) lse[(int64_t)h * T + q] = (m_run + __log2f(l_run)) / kLog2e;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
+}
+
+template <int D>
+int fwd_launch(const void* q, const void* k, const void* v, void* o, float* lse, int64_t T, int hq, int hkv,
+               int64_t qs, int64_t ks, int64_t vs, int64_t os, float scale, int causal, cudaStream_t st) {
+  using C = Fwd<D>;
+  CUtensorMap mq, mk, mv;
+  int e;
+  if ((e = make_map_2d(&mq, q, (uint64_t)hq * D, T, qs, 64, C::BM))) return e;
+  if ((e = make_map_2d(&mk, k, (uint64_t)hkv * D, T, ks, 64, C::BN))) return e;
+  if ((e = make_map_2d(&mv, v, (uint64_t)hkv * D, T, vs, 64, C::BN))) return e;
+  static bool set = false;
+  if (!set) {
+    KPO_CUDA(cudaFuncSetAttribute(attn_fwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    set = true;
+  }
+  dim3 grid((unsigned)((T + C::BM - 1) / C::BM), (unsigned)hq);
+  attn_fwd_tc_kernel<D><<<grid, kThreads, C::SMEM, st>>>(mq, mk, mv, (__nv_bfloat16*)o, lse, (int)T, hq, hkv, os,
+                                                         scale * kLog2e, causal);
+  KPO_LAUNCH_CHECK();
+  return KPO_OK;
+}
+
+
+// =====================================================================================
+// Backward.  One CTA = 128 keys of one kv head; it loops over every q head of the GQA group and
+// every causal 64-query tile, so dK / dV accumulate in TMEM across the whole group (no atomics).
+// Per step (64 queries):
+//   S^T  = K Q^T        M=128 keys, N=64 q, K=d      (A = K tile K-major, B = Q tile K-major)
+//   dP^T = V dO^T       M=128 keys, N=64 q, K=d
+//   softmax warps (one key row per thread): P^T = exp2(S^T*scale*log2e - lse2), dS^T = P^T (dP^T - Dq)
+//                                           -> bf16 P^T / dS^T tiles in smem (K-major SW128)
+//   dV  += P^T dO       M=128 keys, N=d,  K=64 q     (B = dO tile read MN-major)
+//   dK  += dS^T Q       M=128 keys, N=d,  K=64 q     (B = Q tile read MN-major)
+//   dQ^T = K^T dS^T     M=d=128,   N=64 q, K=128 keys (A = the K tile read MN-major, B = dS^T MN-major)
+//   dQ drain warps: dQ^T lane = head-dim index -> coalesced fp32 reductions into dq_acc[t][h][d].
+// TMEM columns: S^T 0..63, dP^T 64..127, dQ^T 128..191, dV 256..383, dK 384..511.
+template <int D>
+struct Bwd {
+  static constexpr int BN = 128, BM = 64;
+  static constexpr int KV_BYTES = BN * D * 2;
+  static constexpr int QT_BYTES = BM * D * 2;
+  static constexpr int PT_BYTES = BN * BM * 2;
+  static constexpr int OFF_K = 0, OFF_V = OFF_K + KV_BYTES, OFF_Q = OFF_V + KV_BYTES;
+  static constexpr int OFF_DO = OFF_Q + 2 * QT_BYTES, OFF_P = OFF_DO + 2 * QT_BYTES;
+  static constexpr int OFF_DS = OFF_P + PT_BYTES, OFF_STAT = OFF_DS + PT_BYTES;
+  static constexpr int OFF_BAR = OFF_STAT + 2 * 2 * BM * 4;
+  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+  static constexpr int COL_S = 0, COL_DP = 64, COL_DQ = 128, COL_DV = 256, COL_DK = 384;
+  static constexpr int THREADS = 320;  // TMA, MMA, 4 softmax warps, 4 dQ-drain warps
+};
+
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+
+template <int D>
+__global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
+    attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                       const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                       const float* __restrict__ lse, const float* __restrict__ dvec, float* __restrict__ dq_acc,
+                       __nv_bfloat16* __restrict__ dk, __nv_bfloat16* __restrict__ dv, int T, int hq, int hkv,
+                       int64_t dks, int64_t dvs, float scale, int causal) {
+  using C = Bwd<D>;
+  constexpr int BN = C::BN, BM = C::BM, KSUB = D / 64;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* kv_full = bar + 0;
+  uint64_t* qd_full = bar + 1;   // [2]
+  uint64_t* qd_empty = bar + 3;  // [2]
+  uint64_t* s_full = bar + 5;
+  uint64_t* s_empty = bar + 6;
+  uint64_t* pds_full = bar + 7;
+  uint64_t* pds_empty = bar + 8;
+  uint64_t* dq_full = bar + 9;
+  uint64_t* dq_empty = bar + 10;
+  uint64_t* acc_done = bar + 11;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  float* stat = reinterpret_cast<float*>(smem + C::OFF_STAT);  // [2][lse2 64 | dvec 64]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nblk = gridDim.x - 1 - blockIdx.x;  // early key tiles carry the most causal work
+  const int kvh = blockIdx.y;
+  const int group = hq / hkv;
+  const int n0 = nblk * BN;
+  const int m_start = causal ? n0 / BM : 0;
+  const int mq = (T + BM - 1) / BM - m_start;
+  const int steps = group * mq;
+  const float scale_log2 = scale * kLog2e;
+
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(kv_full), 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&qd_full[i]), 1);
+      mbar_init(smem_u32(&qd_empty[i]), 1);
+    }
+    mbar_init(smem_u32(s_full), 1);
+    mbar_init(smem_u32(s_empty), 4);
+    mbar_init(smem_u32(pds_full), 4);
+    mbar_init(smem_u32(pds_empty), 1);
+    mbar_init(smem_u32(dq_full), 1);
+    mbar_init(smem_u32(dq_empty), 4);
+    mbar_init(smem_u32(acc_done), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc(smem_u32(tmem_slot), 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sK = smem_u32(smem + C::OFF_K), sV = smem_u32(smem + C::OFF_V);
+  const uint32_t sQ = smem_u32(smem + C::OFF_Q), sDO = smem_u32(smem + C::OFF_DO);
+  const uint32_t sP = smem_u32(smem + C::OFF_P), sDS = smem_u32(smem + C::OFF_DS);
+
+  auto step_coords = [&](int s, int& h, int& m0) {
+    h = kvh * group + s / mq;
+    m0 = (m_start + s % mq) * BM;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA producer
+      mbar_arrive_expect_tx(smem_u32(kv_full), 2 * C::KV_BYTES);
+#pragma unroll
+      for (int kb = 0; kb < KSUB; ++kb) {
+        tma_load_2d(sK + kb * BN * 128, &tmK, smem_u32(kv_full), kvh * D + kb * 64, n0);
+        tma_load_2d(sV + kb * BN * 128, &tmV, smem_u32(kv_full), kvh * D + kb * 64, n0);
+      }
+      for (int s = 0; s < steps; ++s) {
+        const int st = s & 1;
+        int h, m0;
+        step_coords(s, h, m0);
+        mbar_wait(smem_u32(&qd_empty[st]), ((s >> 1) & 1) ^ 1);
+        const uint32_t fb = smem_u32(&qd_full[st]);
+        mbar_arrive_expect_tx(fb, 2 * C::QT_BYTES);
+#pragma unroll
+        for (int kb = 0; kb < KSUB; ++kb) {
+          tma_load_2d(sQ + st * C::QT_BYTES + kb * BM * 128, &tmQ, fb, h * D + kb * 64, m0);
+          tma_load_2d(sDO + st * C::QT_BYTES + kb * BM * 128, &tmDO, fb, h * D + kb * 64, m0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ MMA issuer
+      constexpr uint32_t ID_S = idesc_bf16(BN, BM, false, false);   // S^T, dP^T
+      constexpr uint32_t ID_G = idesc_bf16(BN, D, false, true);     // dV, dK
+      constexpr uint32_t ID_Q = idesc_bf16(D, BM, true, true);      // dQ^T
+      mbar_wait(smem_u32(kv_full), 0);
+      auto grads = [&](int j) {
+        const int st = j & 1;
+        mbar_wait(smem_u32(pds_full), j & 1);
+        tc_fence_after();
+        const uint32_t qb = sQ + st * C::QT_BYTES, ob = sDO + st * C::QT_BYTES;
+#pragma unroll
+        for (int k = 0; k < BM / 16; ++k) {
+          const uint32_t acc = (j > 0 || k > 0) ? 1u : 0u;
+          tc_mma(tmem + C::COL_DV, smem_desc(sP + k * 32, 16, 1024), smem_desc(ob + k * 2048, BM * 128, 1024), ID_G,
+                 acc);
+          tc_mma(tmem + C::COL_DK, smem_desc(sDS + k * 32, 16, 1024), smem_desc(qb + k * 2048, BM * 128, 1024), ID_G,
+                 acc);
+        }
+        mbar_wait(smem_u32(dq_empty), (j & 1) ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < BN / 16; ++k) {
+          tc_mma(tmem + C::COL_DQ, smem_desc(sK + k * 2048, BN * 128, 1024), smem_desc(sDS + k * 2048, BM * 128, 1024),
+                 ID_Q, k > 0 ? 1u : 0u);
+        }
+        tc_commit(smem_u32(dq_full));
+        tc_commit(smem_u32(pds_empty));
+        tc_commit(smem_u32(&qd_empty[st]));
+      };
+      for (int s = 0; s < steps; ++s) {
+        const int st = s & 1;
+        mbar_wait(smem_u32(&qd_full[st]), (s >> 1) & 1);
+        mbar_wait(smem_u32(s_empty), (s & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t qb = sQ + st * C::QT_BYTES, ob = sDO + st * C::QT_BYTES;
+#pragma unroll
+        for (int kb = 0; kb < KSUB; ++kb) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t acc = (kb | k) ? 1u : 0u;
+            tc_mma(tmem + C::COL_S, smem_desc(sK + kb * BN * 128 + k * 32, 16, 1024),
+                   smem_desc(qb + kb * BM * 128 + k * 32, 16, 1024), ID_S, acc);
+            tc_mma(tmem + C::COL_DP, smem_desc(sV + kb * BN * 128 + k * 32, 16, 1024),
+                   smem_desc(ob + kb * BM * 128 + k * 32, 16, 1024), ID_S, acc);
+          }
+        }
+        tc_commit(smem_u32(s_full));
+        if (s > 0) grads(s - 1);
+      }
+      if (steps > 0) grads(steps - 1);
+      tc_commit(smem_u32(acc_done));
+    }
+  } else if (warp < 6) {
+    // ------------------------------------------------------------ softmax warps 2..5 (row = key)
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const int key = n0 + r;
+    const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
+    const int tid = threadIdx.x - 64;  // 0..127
+    for (int s = 0; s < steps; ++s) {
+      int h, m0;
+      step_coords(s, h, m0);
+      float* st = stat + (s & 1) * 2 * BM;
+      {
+        const int qi = tid & (BM - 1);
+        const int q = m0 + qi;
+        if (tid < BM) st[qi] = q < T ? lse[(int64_t)h * T + q] * kLog2e : INFINITY;
+        else st[BM + qi] = q < T ? dvec[(int64_t)h * T + q] : 0.f;
+      }
+      named_bar(1, 128);
+      mbar_wait(smem_u32(s_full), s & 1);
+      tc_fence_after();
+      if (s > 0) mbar_wait(smem_u32(pds_empty), (s - 1) & 1);
+      const bool mask = (causal && m0 < n0 + BN - 1) || key >= T;
+#pragma unroll
+      for (int c = 0; c < BM / 32; ++c) {
+        float sv[32], dp[32];
+        tmem_ld32_nowait(lane_addr + C::COL_S + c * 32, reinterpret_cast<uint32_t*>(sv));
+        tmem_ld32_nowait(lane_addr + C::COL_DP + c * 32, reinterpret_cast<uint32_t*>(dp));
+        tmem_wait_ld();
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          float p[8], ds[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int qi = c * 32 + ch * 8 + e;
+            float pe = ex2(sv[ch * 8 + e] * scale_log2 - st[qi]);
+            if (mask && (key >= T || (causal && m0 + qi < key))) pe = 0.f;
+            p[e] = pe;
+            ds[e] = pe * (dp[ch * 8 + e] - st[BM + qi]);
+          }
+          const uint32_t off = sw128(r, c * 4 + ch);
+          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(sP + off), "r"(pack_bf16x2(p[0], p[1])),
+                       "r"(pack_bf16x2(p[2], p[3])), "r"(pack_bf16x2(p[4], p[5])), "r"(pack_bf16x2(p[6], p[7]))
+                       : "memory");
+          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(sDS + off), "r"(pack_bf16x2(ds[0], ds[1])),
+                       "r"(pack_bf16x2(ds[2], ds[3])), "r"(pack_bf16x2(ds[4], ds[5])), "r"(pack_bf16x2(ds[6], ds[7]))
+                       : "memory");
+        }
+      }
+      tc_fence_before();
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(smem_u32(s_empty));
+        mbar_arrive(smem_u32(pds_full));
+      }
+    }
+    // ------------------------------------------------------------ dK / dV epilogue
+    mbar_wait(smem_u32(acc_done), 0);
+    tc_fence_after();
+    const bool ok = key < T && steps > 0;
+#pragma unroll 1
+    for (int which = 0; which < 2; ++which) {
+      const uint32_t col = which ? C::COL_DV : C::COL_DK;
+      const float mul = which ? 1.f : scale;
+      __nv_bfloat16* row = which ? dv + (int64_t)key * dvs + (int64_t)kvh * D : dk + (int64_t)key * dks + (int64_t)kvh * D;
+#pragma unroll 1
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32_nowait(lane_addr + col + c * 32, v);
+        tmem_wait_ld();
+        if (ok) {
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            uint4 u;
+            u.x = pack_bf16x2(__uint_as_float(v[q4 * 8 + 0]) * mul, __uint_as_float(v[q4 * 8 + 1]) * mul);
+            u.y = pack_bf16x2(__uint_as_float(v[q4 * 8 + 2]) * mul, __uint_as_float(v[q4 * 8 + 3]) * mul);
+            u.z = pack_bf16x2(__uint_as_float(v[q4 * 8 + 4]) * mul, __uint_as_float(v[q4 * 8 + 5]) * mul);
+            u.w = pack_bf16x2(__uint_as_float(v[q4 * 8 + 6]) * mul, __uint_as_float(v[q4 * 8 + 7]) * mul);
+            *reinterpret_cast<uint4*>(row + c * 32 + q4 * 8) = u;
+          }
+        }
+      }
+      if (!ok && steps == 0 && key < T) {  // no causal work: gradients are zero
+        for (int c = 0; c < D; c += 8) *reinterpret_cast<uint4*>(row + c) = make_uint4(0, 0, 0, 0);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ dQ drain warps 6..9 (lane = head dim)
+    const int quarter = warp & 3;
+    const int dcol = quarter * 32 + lane;
+    const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
+    for (int s = 0; s < steps; ++s) {
+      int h, m0;
+      step_coords(s, h, m0);
+      mbar_wait(smem_u32(dq_full), s & 1);
+      tc_fence_after();
+      float v[BM];
+#pragma unroll
+      for (int c = 0; c < BM / 32; ++c) tmem_ld32_nowait(lane_addr + C::COL_DQ + c * 32, reinterpret_cast<uint32_t*>(v + c * 32));
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(dq_empty));
+      float* base = dq_acc + ((int64_t)m0 * hq + h) * D + dcol;
+      const int qmax = min(BM, T - m0);
+#pragma unroll
+      for (int qi = 0; qi < BM; ++qi)
+        if (qi < qmax) atomicAdd(base + (int64_t)qi * hq * D, v[qi] * scale);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+template <int D>
+int bwd_launch(const void* q, const void* k, const void* v, const void* dout, const float* lse, const float* dvec,
+               float* dq_acc, void* dk, void* dv, int64_t T, int hq, int hkv, int64_t qs, int64_t ks, int64_t vs,
+               int64_t os, int64_t dks, int64_t dvs, float scale, int causal, cudaStream_t st) {
+  using C = Bwd<D>;
+  CUtensorMap mq, mk, mv, mo;
+  int e;
+  if ((e = make_map_2d(&mq, q, (uint64_t)hq * D, T, qs, 64, C::BM))) return e;
+  if ((e = make_map_2d(&mk, k, (uint64_t)hkv * D, T, ks, 64, C::BN))) return e;
+  if ((e = make_map_2d(&mv, v, (uint64_t)hkv * D, T, vs, 64, C::BN))) return e;
+  if ((e = make_map_2d(&mo, dout, (uint64_t)hq * D, T, os, 64, C::BM))) return e;
+  static bool set = false;
+  if (!set) {
+    KPO_CUDA(cudaFuncSetAttribute(attn_bwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    set = true;
+  }
+  dim3 grid((unsigned)((T + C::BN - 1) / C::BN), (unsigned)hkv);
+  attn_bwd_tc_kernel<D><<<grid, C::THREADS, C::SMEM, st>>>(mq, mk, mv, mo, lse, dvec, dq_acc, (__nv_bfloat16*)dk,
+                                                          (__nv_bfloat16*)dv, (int)T, hq, hkv, dks, dvs, scale, causal);
+  KPO_LAUNCH_CHECK();
+  return KPO_OK;
+}
+}  // namespace attn_tc
+
+// entry used by attention.cu's kpo_attn_fwd
+int attn_fwd_tcgen05(const void* q, const void* k, const void* v, void* o, float* lse, int64_t T, int hq, int hkv,
+                     int d, int64_t qs, int64_t ks, int64_t vs, int64_t os, float scale, int causal, cudaStream_t st) {
+  if (d == 128) return attn_tc::fwd_launch<128>(q, k, v, o, lse, T, hq, hkv, qs, ks, vs, os, scale, causal, st);
+  return attn_tc::fwd_launch<64>(q, k, v, o, lse, T, hq, hkv, qs, ks, vs, os, scale, causal, st);
+}
+
+int attn_bwd_tcgen05_main(const void* q, const void* k, const void* v, const void* dout, const float* lse,
+                          const float* dvec, float* dq_acc, void* dk, void* dv, int64_t T, int hq, int hkv, int d,
+                          int64_t qs, int64_t ks, int64_t vs, int64_t os, int64_t dks, int64_t dvs, float scale,
+                          int causal, cudaStream_t st) {
+  if (d != 128) {
+    set_error("attn_bwd tcgen05 path needs head_dim 128");
+    return KPO_ERR_UNSUPPORTED;
+  }
+  return attn_tc::bwd_launch<128>(q, k, v, dout, lse, dvec, dq_acc, dk, dv, T, hq, hkv, qs, ks, vs, os, dks, dvs,
+                                  scale, causal, st);
+}
+
+}  // namespace kpo

@@ -149,6 +149,14 @@ def attn_fwd(q, k, v, o, lse, T: int, hq: int, hkv: int, d: int, scale: float, c
               k.stride(0), v.stride(0), o.stride(0), ctypes.c_float(scale), int(causal), _stream(stream))
 
 
+def attn_fwd_mma(q, k, v, o, lse, T: int, hq: int, hkv: int, d: int, scale: float, causal: bool = True,
+                 stream=None) -> None:
+    """Round-1 warp-level (mma.sync) forward: A/B baseline and cross-check only."""
+    _need_cuda(q, k, v, o, lse)
+    _lib.call("kpo_attn_fwd_mma", _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), T, hq, hkv, d, q.stride(0),
+              k.stride(0), v.stride(0), o.stride(0), ctypes.c_float(scale), int(causal), _stream(stream))
+
+
 def attn_bwd_workspace(T: int, hq: int, hkv: int, d: int, device) -> torch.Tensor:
     n = _lib.lib().kpo_attn_bwd_workspace_bytes(T, hq, hkv, d)
     return torch.empty(n, dtype=torch.uint8, device=device)

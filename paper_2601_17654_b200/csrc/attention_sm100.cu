@@ -26,12 +26,12 @@ struct Fwd {
   static constexpr int BM = 128, BN = 128, STAGES = 2;
   static constexpr int Q_BYTES = BM * D * 2;  // D/64 sub-tiles of [128 rows x 64] (16 KB each)
   static constexpr int KV_BYTES = BN * D * 2;
-  static constexpr int P_BYTES = BM * BN * 2;  // 2 sub-tiles of [128 q x 64 keys]
+  static constexpr int P_BYTES = BM * BN * 2;  // 2 sub-tiles of [128 q x 64 keys]; double-buffered
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + Q_BYTES;
   static constexpr int OFF_V = OFF_K + STAGES * KV_BYTES;
   static constexpr int OFF_P = OFF_V + STAGES * KV_BYTES;
-  static constexpr int OFF_BAR = OFF_P + P_BYTES;
+  static constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
   static constexpr int SMEM_RAW = OFF_BAR + 256 + 1024;
   // keep one CTA per SM (the kernel allocates all 512 TMEM columns)
   static constexpr int SMEM = SMEM_RAW > 120 * 1024 ? SMEM_RAW : 120 * 1024;
@@ -59,13 +59,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* kv_empty = bar + 3;  // [2]
   uint64_t* s_full = bar + 5;    // [2]
   uint64_t* s_empty = bar + 7;   // [2]
-  uint64_t* p_full = bar + 9;
-  uint64_t* pv_done = bar + 10;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  uint64_t* p_full = bar + 9;    // [2]
+  uint64_t* pv_done = bar + 11;  // [2]  PV(i) commits to pv_done[i & 1]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 13);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int mblk = gridDim.x - 1 - blockIdx.x;  // heavy (late) causal rows first
-  const int h = blockIdx.y;
+  const int mblk = gridDim.y - 1 - blockIdx.y;  // heavy (late) causal rows first, all heads of a row-tile together
+  const int h = blockIdx.x;
   const int kvh = h / (hq / hkv);
   const int m0 = mblk * BM;
   int n_tiles = (T + BN - 1) / BN;
@@ -78,9 +78,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(&kv_empty[i]), 1);
       mbar_init(smem_u32(&s_full[i]), 1);
       mbar_init(smem_u32(&s_empty[i]), 4);
+      mbar_init(smem_u32(&p_full[i]), 4);
+      mbar_init(smem_u32(&pv_done[i]), 1);
     }
-    mbar_init(smem_u32(p_full), 4);
-    mbar_init(smem_u32(pv_done), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) tmem_alloc(smem_u32(tmem_slot), C::TMEM_COLS);
@@ -116,16 +116,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t ID_O = idesc_bf16(BM, D, false, true);
       mbar_wait(smem_u32(q_full), 0);
       auto issue_pv = [&](int i) {
-        mbar_wait(smem_u32(p_full), i & 1);
+        mbar_wait(smem_u32(&p_full[i & 1]), (i >> 1) & 1);
         tc_fence_after();
         const uint32_t vb = sV + (i & 1) * C::KV_BYTES;
+        const uint32_t pb = sP + (i & 1) * C::P_BYTES;
 #pragma unroll
         for (int kk = 0; kk < BN / 16; ++kk) {  // 16 keys per UMMA
-          const uint64_t da = smem_desc(sP + (kk >> 2) * BM * 128 + (kk & 3) * 32, 16, 1024);
+          const uint64_t da = smem_desc(pb + (kk >> 2) * BM * 128 + (kk & 3) * 32, 16, 1024);
           const uint64_t db = smem_desc(vb + kk * 2048, BN * 128, 1024);
           tc_mma(tmem + C::COL_O, da, db, ID_O, (i > 0 || kk > 0) ? 1u : 0u);
         }
-        tc_commit(smem_u32(pv_done));
+        tc_commit(smem_u32(&pv_done[i & 1]));
         tc_commit(smem_u32(&kv_empty[i & 1]));
       };
       for (int j = 0; j < n_tiles; ++j) {
@@ -170,17 +171,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(smem_u32(&s_empty[s]));
       const int k0 = j * BN;
       const bool mask = (causal && k0 + BN - 1 > m0) || (k0 + BN > T);
-      float mx = -INFINITY;
+      if (mask) {
 #pragma unroll
-      for (int i = 0; i < BN; ++i) {
-        float x = sv[i] * scale_log2;
-        if (mask) {
+        for (int i = 0; i < BN; ++i) {
           const int key = k0 + i;
-          if (key >= T || (causal && key > q)) x = -INFINITY;
+          if (key >= T || (causal && key > q)) sv[i] = -INFINITY;
         }
-        sv[i] = x;
-        mx = fmaxf(mx, x);
       }
+      // row max over raw scores with 8 independent chains (scale > 0 commutes with max)
+      float pm[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) pm[e] = sv[e];
+#pragma unroll
+      for (int i = 8; i < BN; ++i) pm[i & 7] = fmaxf(pm[i & 7], sv[i]);
+      const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
+                             fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7]))) * scale_log2;
       float corr = 1.f;
       bool rescale = false;
       if (mx > m_run + 8.f) {  // lazy rescaling: only when the max grows by more than 2^8
@@ -188,8 +193,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         rescale = (j > 0);
         m_run = mx;
       }
-      if (j > 0) mbar_wait(smem_u32(pv_done), (j - 1) & 1);  // P buffer free, O stable
+      if (j >= 2) mbar_wait(smem_u32(&pv_done[s]), ((j - 2) >> 1) & 1);  // P[s] free (PV(j-2) done)
       if (rescale) {
+        mbar_wait(smem_u32(&pv_done[s ^ 1]), ((j - 1) >> 1) & 1);  // O stable (PV(j-1) done)
         tc_fence_after();
 #pragma unroll 1
         for (int c = 0; c < D / 32; ++c) {
@@ -202,32 +208,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tmem_wait_st();
       }
-      float lsum = 0.f;
+      const float neg_m = -m_run;
+      float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int ch = 0; ch < BN / 8; ++ch) {  // 16-byte chunks of 8 keys
         float p[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          p[e] = ex2(sv[ch * 8 + e] - m_run);
-          lsum += p[e];
+          p[e] = ex2(fmaf(sv[ch * 8 + e], scale_log2, neg_m));
+          ps[e] += p[e];
         }
         uint4 u;
         u.x = pack_bf16x2(p[0], p[1]);
         u.y = pack_bf16x2(p[2], p[3]);
         u.z = pack_bf16x2(p[4], p[5]);
         u.w = pack_bf16x2(p[6], p[7]);
-        const uint32_t addr = sP + (ch >> 3) * BM * 128 + sw128(r, ch & 7);
+        const uint32_t addr = sP + s * C::P_BYTES + (ch >> 3) * BM * 128 + sw128(r, ch & 7);
         asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(u.x), "r"(u.y), "r"(u.z), "r"(u.w)
                      : "memory");
       }
+      const float lsum = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
       l_run = l_run * corr + lsum;
       fence_async_smem();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(p_full));
+      if (lane == 0) mbar_arrive(smem_u32(&p_full[s]));
     }
     // ---------------------------------------------------------------- epilogue
-    mbar_wait(smem_u32(pv_done), (n_tiles - 1) & 1);
+    mbar_wait(smem_u32(&pv_done[(n_tiles - 1) & 1]), ((n_tiles - 1) >> 1) & 1);
     tc_fence_after();
     const float inv = 1.f / l_run;
     const bool row_ok = q < T;
@@ -271,7 +279,7 @@ int fwd_launch(const void* q, const void* k, const void* v, void* o, float* lse,
     KPO_CUDA(cudaFuncSetAttribute(attn_fwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     set = true;
   }
-  dim3 grid((unsigned)((T + C::BM - 1) / C::BM), (unsigned)hq);
+  dim3 grid((unsigned)hq, (unsigned)((T + C::BM - 1) / C::BM));
   attn_fwd_tc_kernel<D><<<grid, kThreads, C::SMEM, st>>>(mq, mk, mv, (__nv_bfloat16*)o, lse, (int)T, hq, hkv, os,
                                                          scale * kLog2e, causal);
   KPO_LAUNCH_CHECK();
@@ -291,7 +299,10 @@ int fwd_launch(const void* q, const void* k, const void* v, void* o, float* lse,
 //   dK  += dS^T Q       M=128 keys, N=d,  K=64 q     (B = Q tile read MN-major)
 //   dQ^T = K^T dS^T     M=d=128,   N=64 q, K=128 keys (A = the K tile read MN-major, B = dS^T MN-major)
 //   dQ drain warps: dQ^T lane = head-dim index -> coalesced fp32 reductions into dq_acc[t][h][d].
-// TMEM columns: S^T 0..63, dP^T 64..127, dQ^T 128..191, dV 256..383, dK 384..511.
+// TMEM columns: S^T 0..63, dP^T 64..127, dQ^T 128..255 (2 buffers), dV 256..383, dK 384..511.
+// Issue order: S/dP(s+1) as soon as the softmax warps have pulled S/dP(s) out of TMEM, then the
+// gradient MMAs of step s; P^T/dS^T (smem) and dQ^T (TMEM) are double-buffered so the softmax of
+// step s+1 and the dQ drain of step s overlap the tensor core.
 template <int D>
 struct Bwd {
   static constexpr int BN = 128, BM = 64;
@@ -299,11 +310,11 @@ struct Bwd {
   static constexpr int QT_BYTES = BM * D * 2;
   static constexpr int PT_BYTES = BN * BM * 2;
   static constexpr int OFF_K = 0, OFF_V = OFF_K + KV_BYTES, OFF_Q = OFF_V + KV_BYTES;
-  static constexpr int OFF_DO = OFF_Q + 2 * QT_BYTES, OFF_P = OFF_DO + 2 * QT_BYTES;
-  static constexpr int OFF_DS = OFF_P + PT_BYTES, OFF_STAT = OFF_DS + PT_BYTES;
+  static constexpr int OFF_DO = OFF_Q + 2 * QT_BYTES, OFF_P = OFF_DO + 2 * QT_BYTES;  // P^T, dS^T: 2 buffers each
+  static constexpr int OFF_DS = OFF_P + 2 * PT_BYTES, OFF_STAT = OFF_DS + 2 * PT_BYTES;
   static constexpr int OFF_BAR = OFF_STAT + 2 * 2 * BM * 4;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
-  static constexpr int COL_S = 0, COL_DP = 64, COL_DQ = 128, COL_DV = 256, COL_DK = 384;
+  static constexpr int COL_S = 0, COL_DP = 64, COL_DQ = 128, COL_DV = 256, COL_DK = 384;  // dQ^T: 128 + 64*b
   static constexpr int THREADS = 320;  // TMA, MMA, 4 softmax warps, 4 dQ-drain warps
 };
 
@@ -326,17 +337,17 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
   uint64_t* qd_empty = bar + 3;  // [2]
   uint64_t* s_full = bar + 5;
   uint64_t* s_empty = bar + 6;
-  uint64_t* pds_full = bar + 7;
-  uint64_t* pds_empty = bar + 8;
-  uint64_t* dq_full = bar + 9;
-  uint64_t* dq_empty = bar + 10;
-  uint64_t* acc_done = bar + 11;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  uint64_t* pds_full = bar + 7;    // [2]
+  uint64_t* pds_empty = bar + 9;   // [2]
+  uint64_t* dq_full = bar + 11;    // [2]
+  uint64_t* dq_empty = bar + 13;   // [2]
+  uint64_t* acc_done = bar + 15;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
   float* stat = reinterpret_cast<float*>(smem + C::OFF_STAT);  // [2][lse2 64 | dvec 64]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nblk = gridDim.x - 1 - blockIdx.x;  // early key tiles carry the most causal work
-  const int kvh = blockIdx.y;
+  const int nblk = blockIdx.y;  // early key tiles carry the most causal work: dispatched first
+  const int kvh = blockIdx.x;
   const int group = hq / hkv;
   const int n0 = nblk * BN;
   const int m_start = causal ? n0 / BM : 0;
@@ -352,10 +363,12 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
     }
     mbar_init(smem_u32(s_full), 1);
     mbar_init(smem_u32(s_empty), 4);
-    mbar_init(smem_u32(pds_full), 4);
-    mbar_init(smem_u32(pds_empty), 1);
-    mbar_init(smem_u32(dq_full), 1);
-    mbar_init(smem_u32(dq_empty), 4);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&pds_full[i]), 4);
+      mbar_init(smem_u32(&pds_empty[i]), 1);
+      mbar_init(smem_u32(&dq_full[i]), 1);
+      mbar_init(smem_u32(&dq_empty[i]), 4);
+    }
     mbar_init(smem_u32(acc_done), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -405,32 +418,32 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
       mbar_wait(smem_u32(kv_full), 0);
       auto grads = [&](int j) {
         const int st = j & 1;
-        mbar_wait(smem_u32(pds_full), j & 1);
+        mbar_wait(smem_u32(&pds_full[st]), (j >> 1) & 1);
         tc_fence_after();
         const uint32_t qb = sQ + st * C::QT_BYTES, ob = sDO + st * C::QT_BYTES;
+        const uint32_t pb = sP + st * C::PT_BYTES, db = sDS + st * C::PT_BYTES;
 #pragma unroll
         for (int k = 0; k < BM / 16; ++k) {
           const uint32_t acc = (j > 0 || k > 0) ? 1u : 0u;
-          tc_mma(tmem + C::COL_DV, smem_desc(sP + k * 32, 16, 1024), smem_desc(ob + k * 2048, BM * 128, 1024), ID_G,
+          tc_mma(tmem + C::COL_DV, smem_desc(pb + k * 32, 16, 1024), smem_desc(ob + k * 2048, BM * 128, 1024), ID_G,
                  acc);
-          tc_mma(tmem + C::COL_DK, smem_desc(sDS + k * 32, 16, 1024), smem_desc(qb + k * 2048, BM * 128, 1024), ID_G,
+          tc_mma(tmem + C::COL_DK, smem_desc(db + k * 32, 16, 1024), smem_desc(qb + k * 2048, BM * 128, 1024), ID_G,
                  acc);
         }
-        mbar_wait(smem_u32(dq_empty), (j & 1) ^ 1);
+        mbar_wait(smem_u32(&dq_empty[st]), ((j >> 1) & 1) ^ 1);
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < BN / 16; ++k) {
-          tc_mma(tmem + C::COL_DQ, smem_desc(sK + k * 2048, BN * 128, 1024), smem_desc(sDS + k * 2048, BM * 128, 1024),
-                 ID_Q, k > 0 ? 1u : 0u);
+          tc_mma(tmem + C::COL_DQ + st * BM, smem_desc(sK + k * 2048, BN * 128, 1024),
+                 smem_desc(db + k * 2048, BM * 128, 1024), ID_Q, k > 0 ? 1u : 0u);
         }
-        tc_commit(smem_u32(dq_full));
-        tc_commit(smem_u32(pds_empty));
+        tc_commit(smem_u32(&dq_full[st]));
+        tc_commit(smem_u32(&pds_empty[st]));
         tc_commit(smem_u32(&qd_empty[st]));
       };
-      for (int s = 0; s < steps; ++s) {
+      auto scores = [&](int s) {
         const int st = s & 1;
         mbar_wait(smem_u32(&qd_full[st]), (s >> 1) & 1);
-        mbar_wait(smem_u32(s_empty), (s & 1) ^ 1);
         tc_fence_after();
         const uint32_t qb = sQ + st * C::QT_BYTES, ob = sDO + st * C::QT_BYTES;
 #pragma unroll
@@ -445,9 +458,15 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
           }
         }
         tc_commit(smem_u32(s_full));
-        if (s > 0) grads(s - 1);
+      };
+      if (steps > 0) scores(0);
+      for (int s = 0; s < steps; ++s) {
+        if (s + 1 < steps) {
+          mbar_wait(smem_u32(s_empty), s & 1);  // softmax(s) has pulled S/dP(s) out of TMEM
+          scores(s + 1);
+        }
+        grads(s);
       }
-      if (steps > 0) grads(steps - 1);
       tc_commit(smem_u32(acc_done));
     }
   } else if (warp < 6) {
@@ -470,41 +489,42 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
       named_bar(1, 128);
       mbar_wait(smem_u32(s_full), s & 1);
       tc_fence_after();
-      if (s > 0) mbar_wait(smem_u32(pds_empty), (s - 1) & 1);
-      const bool mask = (causal && m0 < n0 + BN - 1) || key >= T;
+      float sv[BM], dp[BM];
 #pragma unroll
       for (int c = 0; c < BM / 32; ++c) {
-        float sv[32], dp[32];
-        tmem_ld32_nowait(lane_addr + C::COL_S + c * 32, reinterpret_cast<uint32_t*>(sv));
-        tmem_ld32_nowait(lane_addr + C::COL_DP + c * 32, reinterpret_cast<uint32_t*>(dp));
-        tmem_wait_ld();
-#pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
-          float p[8], ds[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int qi = c * 32 + ch * 8 + e;
-            float pe = ex2(sv[ch * 8 + e] * scale_log2 - st[qi]);
-            if (mask && (key >= T || (causal && m0 + qi < key))) pe = 0.f;
-            p[e] = pe;
-            ds[e] = pe * (dp[ch * 8 + e] - st[BM + qi]);
-          }
-          const uint32_t off = sw128(r, c * 4 + ch);
-          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(sP + off), "r"(pack_bf16x2(p[0], p[1])),
-                       "r"(pack_bf16x2(p[2], p[3])), "r"(pack_bf16x2(p[4], p[5])), "r"(pack_bf16x2(p[6], p[7]))
-                       : "memory");
-          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(sDS + off), "r"(pack_bf16x2(ds[0], ds[1])),
-                       "r"(pack_bf16x2(ds[2], ds[3])), "r"(pack_bf16x2(ds[4], ds[5])), "r"(pack_bf16x2(ds[6], ds[7]))
-                       : "memory");
-        }
+        tmem_ld32_nowait(lane_addr + C::COL_S + c * 32, reinterpret_cast<uint32_t*>(sv + c * 32));
+        tmem_ld32_nowait(lane_addr + C::COL_DP + c * 32, reinterpret_cast<uint32_t*>(dp + c * 32));
       }
+      tmem_wait_ld();
       tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(s_empty));
+      const int buf = s & 1;
+      mbar_wait(smem_u32(&pds_empty[buf]), ((s >> 1) & 1) ^ 1);  // grads(s-2) done with this buffer
+      const bool mask = (causal && m0 < n0 + BN - 1) || key >= T;
+      const uint32_t pb = sP + buf * C::PT_BYTES, db = sDS + buf * C::PT_BYTES;
+#pragma unroll
+      for (int ch = 0; ch < BM / 8; ++ch) {
+        float p[8], ds[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int qi = ch * 8 + e;
+          float pe = ex2(fmaf(sv[qi], scale_log2, -st[qi]));
+          if (mask && (key >= T || (causal && m0 + qi < key))) pe = 0.f;
+          p[e] = pe;
+          ds[e] = pe * (dp[qi] - st[BM + qi]);
+        }
+        const uint32_t off = sw128(r, ch);
+        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(pb + off), "r"(pack_bf16x2(p[0], p[1])),
+                     "r"(pack_bf16x2(p[2], p[3])), "r"(pack_bf16x2(p[4], p[5])), "r"(pack_bf16x2(p[6], p[7]))
+                     : "memory");
+        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(db + off), "r"(pack_bf16x2(ds[0], ds[1])),
+                     "r"(pack_bf16x2(ds[2], ds[3])), "r"(pack_bf16x2(ds[4], ds[5])), "r"(pack_bf16x2(ds[6], ds[7]))
+                     : "memory");
+      }
       fence_async_smem();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(smem_u32(s_empty));
-        mbar_arrive(smem_u32(pds_full));
-      }
+      if (lane == 0) mbar_arrive(smem_u32(&pds_full[buf]));
     }
     // ------------------------------------------------------------ dK / dV epilogue
     mbar_wait(smem_u32(acc_done), 0);
@@ -544,15 +564,17 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
     for (int s = 0; s < steps; ++s) {
       int h, m0;
       step_coords(s, h, m0);
-      mbar_wait(smem_u32(dq_full), s & 1);
+      const int buf = s & 1;
+      mbar_wait(smem_u32(&dq_full[buf]), (s >> 1) & 1);
       tc_fence_after();
       float v[BM];
 #pragma unroll
-      for (int c = 0; c < BM / 32; ++c) tmem_ld32_nowait(lane_addr + C::COL_DQ + c * 32, reinterpret_cast<uint32_t*>(v + c * 32));
+      for (int c = 0; c < BM / 32; ++c)
+        tmem_ld32_nowait(lane_addr + C::COL_DQ + buf * BM + c * 32, reinterpret_cast<uint32_t*>(v + c * 32));
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(dq_empty));
+      if (lane == 0) mbar_arrive(smem_u32(&dq_empty[buf]));
       float* base = dq_acc + ((int64_t)m0 * hq + h) * D + dcol;
       const int qmax = min(BM, T - m0);
 #pragma unroll
@@ -582,7 +604,7 @@ int bwd_launch(const void* q, const void* k, const void* v, const void* dout, co
     KPO_CUDA(cudaFuncSetAttribute(attn_bwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     set = true;
   }
-  dim3 grid((unsigned)((T + C::BN - 1) / C::BN), (unsigned)hkv);
+  dim3 grid((unsigned)hkv, (unsigned)((T + C::BN - 1) / C::BN));
   attn_bwd_tc_kernel<D><<<grid, C::THREADS, C::SMEM, st>>>(mq, mk, mv, mo, lse, dvec, dq_acc, (__nv_bfloat16*)dk,
                                                           (__nv_bfloat16*)dv, (int)T, hq, hkv, dks, dvs, scale, causal);
   KPO_LAUNCH_CHECK();

@@ -529,7 +529,7 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* o
         (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, dvec, dq_acc, (int)T, hq, os);
     KPO_LAUNCH_CHECK();
   }
-  if (D == 128 && use_tc) {
+  if (D == 128 && use_tc && T % 8 == 0) {  // tcgen05 path (bulk-copied softmax stats need 16 B rows)
     int st = attn_bwd_tcgen05_main(q, k, v, dout, lse, dvec, dq_acc, dk, dv, T, hq, hkv, D, qs, ks, vs, os, dks, dvs,
                                    scale, causal, s);
     if (st) return st;

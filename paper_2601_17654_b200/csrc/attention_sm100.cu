@@ -298,7 +298,8 @@ int fwd_launch(const void* q, const void* k, const void* v, void* o, float* lse,
 //   dV  += P^T dO       M=128 keys, N=d,  K=64 q     (B = dO tile read MN-major)
 //   dK  += dS^T Q       M=128 keys, N=d,  K=64 q     (B = Q tile read MN-major)
 //   dQ^T = K^T dS^T     M=d=128,   N=64 q, K=128 keys (A = the K tile read MN-major, B = dS^T MN-major)
-//   dQ drain warps: dQ^T lane = head-dim index -> coalesced fp32 reductions into dq_acc[t][h][d].
+//   dQ drain warps: dQ^T (lane = head-dim index) -> fp32 [q][d] smem tile -> one TMA bulk
+//   reduce-add (cp.reduce.async.bulk.tensor .add) into dq_acc[t][h][d].
 // TMEM columns: S^T 0..63, dP^T 64..127, dQ^T 128..255 (2 buffers), dV 256..383, dK 384..511.
 // Issue order: S/dP(s+1) as soon as the softmax warps have pulled S/dP(s) out of TMEM, then the
 // gradient MMAs of step s; P^T/dS^T (smem) and dQ^T (TMEM) are double-buffered so the softmax of
@@ -312,10 +313,12 @@ struct Bwd {
   static constexpr int OFF_K = 0, OFF_V = OFF_K + KV_BYTES, OFF_Q = OFF_V + KV_BYTES;
   static constexpr int OFF_DO = OFF_Q + 2 * QT_BYTES, OFF_P = OFF_DO + 2 * QT_BYTES;  // P^T, dS^T: 2 buffers each
   static constexpr int OFF_DS = OFF_P + 2 * PT_BYTES, OFF_STAT = OFF_DS + 2 * PT_BYTES;
-  static constexpr int OFF_BAR = OFF_STAT + 2 * 2 * BM * 4;
+  static constexpr int OFF_DQ = OFF_STAT + 2 * 2 * BM * 4;  // fp32 [64 q][D] staging for the TMA reduce-add
+  static constexpr int OFF_BAR = OFF_DQ + BM * D * 4;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
   static constexpr int COL_S = 0, COL_DP = 64, COL_DQ = 128, COL_DV = 256, COL_DK = 384;  // dQ^T: 128 + 64*b
-  static constexpr int THREADS = 320;  // TMA, MMA, 4 softmax warps, 4 dQ-drain warps
+  static constexpr int THREADS = 448;  // TMA, MMA, 8 softmax warps (2 per lane quarter), 4 dQ-drain warps
+  static constexpr int SM_WARPS = 8;
 };
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
@@ -324,6 +327,7 @@ template <int D>
 __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                        const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                       const __grid_constant__ CUtensorMap tmDQ,
                        const float* __restrict__ lse, const float* __restrict__ dvec, float* __restrict__ dq_acc,
                        __nv_bfloat16* __restrict__ dk, __nv_bfloat16* __restrict__ dv, int T, int hq, int hkv,
                        int64_t dks, int64_t dvs, float scale, int causal) {
@@ -362,9 +366,9 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
       mbar_init(smem_u32(&qd_empty[i]), 1);
     }
     mbar_init(smem_u32(s_full), 1);
-    mbar_init(smem_u32(s_empty), 4);
+    mbar_init(smem_u32(s_empty), C::SM_WARPS);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(smem_u32(&pds_full[i]), 4);
+      mbar_init(smem_u32(&pds_full[i]), C::SM_WARPS);
       mbar_init(smem_u32(&pds_empty[i]), 1);
       mbar_init(smem_u32(&dq_full[i]), 1);
       mbar_init(smem_u32(&dq_empty[i]), 4);
@@ -401,12 +405,16 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
         step_coords(s, h, m0);
         mbar_wait(smem_u32(&qd_empty[st]), ((s >> 1) & 1) ^ 1);
         const uint32_t fb = smem_u32(&qd_full[st]);
-        mbar_arrive_expect_tx(fb, 2 * C::QT_BYTES);
+        const uint32_t nstat = (uint32_t)min(BM, T - m0) * 4u;  // T % 8 == 0 keeps this a 16 B multiple
+        mbar_arrive_expect_tx(fb, 2 * C::QT_BYTES + 2 * nstat);
 #pragma unroll
         for (int kb = 0; kb < KSUB; ++kb) {
           tma_load_2d(sQ + st * C::QT_BYTES + kb * BM * 128, &tmQ, fb, h * D + kb * 64, m0);
           tma_load_2d(sDO + st * C::QT_BYTES + kb * BM * 128, &tmDO, fb, h * D + kb * 64, m0);
         }
+        const uint32_t sst = smem_u32(stat + st * 2 * BM);
+        bulk_load(sst, lse + (int64_t)h * T + m0, nstat, fb);
+        bulk_load(sst + BM * 4, dvec + (int64_t)h * T + m0, nstat, fb);
       }
     }
   } else if (warp == 1) {
@@ -469,52 +477,46 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
       }
       tc_commit(smem_u32(acc_done));
     }
-  } else if (warp < 6) {
-    // ------------------------------------------------------------ softmax warps 2..5 (row = key)
+  } else if (warp < 2 + C::SM_WARPS) {
+    // ------------------------------------------------------------ softmax warps 2..9
+    // row = key (TMEM lane quarter = warp % 4); the two warps of a quarter split the 64 query columns
     const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int r = quarter * 32 + lane;
     const int key = n0 + r;
     const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
-    const int tid = threadIdx.x - 64;  // 0..127
+    constexpr int HC = BM / 2;  // query columns per warp
     for (int s = 0; s < steps; ++s) {
       int h, m0;
       step_coords(s, h, m0);
-      float* st = stat + (s & 1) * 2 * BM;
-      {
-        const int qi = tid & (BM - 1);
-        const int q = m0 + qi;
-        if (tid < BM) st[qi] = q < T ? lse[(int64_t)h * T + q] * kLog2e : INFINITY;
-        else st[BM + qi] = q < T ? dvec[(int64_t)h * T + q] : 0.f;
-      }
-      named_bar(1, 128);
+      (void)h;
+      const int buf = s & 1;
+      const float* st = stat + buf * 2 * BM;  // lse*log2e is applied below; filled by the TMA warp
       mbar_wait(smem_u32(s_full), s & 1);
       tc_fence_after();
-      float sv[BM], dp[BM];
-#pragma unroll
-      for (int c = 0; c < BM / 32; ++c) {
-        tmem_ld32_nowait(lane_addr + C::COL_S + c * 32, reinterpret_cast<uint32_t*>(sv + c * 32));
-        tmem_ld32_nowait(lane_addr + C::COL_DP + c * 32, reinterpret_cast<uint32_t*>(dp + c * 32));
-      }
+      float sv[HC], dp[HC];
+      tmem_ld32_nowait(lane_addr + C::COL_S + half * HC, reinterpret_cast<uint32_t*>(sv));
+      tmem_ld32_nowait(lane_addr + C::COL_DP + half * HC, reinterpret_cast<uint32_t*>(dp));
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(s_empty));
-      const int buf = s & 1;
       mbar_wait(smem_u32(&pds_empty[buf]), ((s >> 1) & 1) ^ 1);  // grads(s-2) done with this buffer
-      const bool mask = (causal && m0 < n0 + BN - 1) || key >= T;
+      const bool mask = (causal && m0 < n0 + BN - 1) || key >= T || m0 + BM > T;
       const uint32_t pb = sP + buf * C::PT_BYTES, db = sDS + buf * C::PT_BYTES;
 #pragma unroll
-      for (int ch = 0; ch < BM / 8; ++ch) {
+      for (int ch = 0; ch < HC / 8; ++ch) {
         float p[8], ds[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const int qi = ch * 8 + e;
-          float pe = ex2(fmaf(sv[qi], scale_log2, -st[qi]));
-          if (mask && (key >= T || (causal && m0 + qi < key))) pe = 0.f;
+          const int qi = half * HC + ch * 8 + e;
+          float pe = ex2(fmaf(sv[ch * 8 + e], scale_log2, -st[qi] * kLog2e));
+          float de = pe * (dp[ch * 8 + e] - st[BM + qi]);
+          if (mask && (key >= T || m0 + qi >= T || (causal && m0 + qi < key))) pe = de = 0.f;
           p[e] = pe;
-          ds[e] = pe * (dp[qi] - st[BM + qi]);
+          ds[e] = de;
         }
-        const uint32_t off = sw128(r, ch);
+        const uint32_t off = sw128(r, half * (HC / 8) + ch);
         asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(pb + off), "r"(pack_bf16x2(p[0], p[1])),
                      "r"(pack_bf16x2(p[2], p[3])), "r"(pack_bf16x2(p[4], p[5])), "r"(pack_bf16x2(p[6], p[7]))
                      : "memory");
@@ -526,6 +528,8 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&pds_full[buf]));
     }
+    if (half) goto done_softmax;  // the first warp of each quarter writes dK / dV
+    {
     // ------------------------------------------------------------ dK / dV epilogue
     mbar_wait(smem_u32(acc_done), 0);
     tc_fence_after();
@@ -556,10 +560,13 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
         for (int c = 0; c < D; c += 8) *reinterpret_cast<uint4*>(row + c) = make_uint4(0, 0, 0, 0);
       }
     }
+    }
+  done_softmax:;
   } else {
-    // ------------------------------------------------------------ dQ drain warps 6..9 (lane = head dim)
+    // ------------------------------------------------------------ dQ drain warps 10..13 (lane = head dim)
     const int quarter = warp & 3;
     const int dcol = quarter * 32 + lane;
+    const int dtid = threadIdx.x - (2 + C::SM_WARPS) * 32;  // 0..127
     const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
     for (int s = 0; s < steps; ++s) {
       int h, m0;
@@ -575,12 +582,20 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&dq_empty[buf]));
-      float* base = dq_acc + ((int64_t)m0 * hq + h) * D + dcol;
-      const int qmax = min(BM, T - m0);
+      // staging tile free? (the previous TMA reduce has finished reading it)
+      if (dtid == 0) bulk_wait_read0();
+      named_bar(2, 128);
+      float* stg = reinterpret_cast<float*>(smem + C::OFF_DQ);
 #pragma unroll
-      for (int qi = 0; qi < BM; ++qi)
-        if (qi < qmax) atomicAdd(base + (int64_t)qi * hq * D, v[qi] * scale);
+      for (int qi = 0; qi < BM; ++qi) stg[qi * D + dcol] = v[qi] * scale;
+      fence_async_smem();
+      named_bar(2, 128);
+      if (dtid == 0) {
+        tma_reduce_add_2d(&tmDQ, smem_u32(stg), h * D, m0);
+        bulk_commit();
+      }
     }
+    if (dtid == 0) bulk_wait0();
   }
   tc_fence_before();
   __syncthreads();
@@ -593,8 +608,9 @@ int bwd_launch(const void* q, const void* k, const void* v, const void* dout, co
                float* dq_acc, void* dk, void* dv, int64_t T, int hq, int hkv, int64_t qs, int64_t ks, int64_t vs,
                int64_t os, int64_t dks, int64_t dvs, float scale, int causal, cudaStream_t st) {
   using C = Bwd<D>;
-  CUtensorMap mq, mk, mv, mo;
+  CUtensorMap mq, mk, mv, mo, mdq;
   int e;
+  if ((e = make_map_2d_f32(&mdq, dq_acc, (uint64_t)hq * D, T, (uint64_t)hq * D, D, C::BM))) return e;
   if ((e = make_map_2d(&mq, q, (uint64_t)hq * D, T, qs, 64, C::BM))) return e;
   if ((e = make_map_2d(&mk, k, (uint64_t)hkv * D, T, ks, 64, C::BN))) return e;
   if ((e = make_map_2d(&mv, v, (uint64_t)hkv * D, T, vs, 64, C::BN))) return e;
@@ -605,7 +621,7 @@ int bwd_launch(const void* q, const void* k, const void* v, const void* dout, co
     set = true;
   }
   dim3 grid((unsigned)hkv, (unsigned)((T + C::BN - 1) / C::BN));
-  attn_bwd_tc_kernel<D><<<grid, C::THREADS, C::SMEM, st>>>(mq, mk, mv, mo, lse, dvec, dq_acc, (__nv_bfloat16*)dk,
+  attn_bwd_tc_kernel<D><<<grid, C::THREADS, C::SMEM, st>>>(mq, mk, mv, mo, mdq, lse, dvec, dq_acc, (__nv_bfloat16*)dk,
                                                           (__nv_bfloat16*)dv, (int)T, hq, hkv, dks, dvs, scale, causal);
   KPO_LAUNCH_CHECK();
   return KPO_OK;

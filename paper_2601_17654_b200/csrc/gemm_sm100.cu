@@ -19,6 +19,7 @@
 //     hardware analogue of the simulator handing all SMs back once communication ends
 //     (simgpu.py:221).  The last CTA to finish resets the counter (graph-replay safe).
 #include "sm100.cuh"
+#include <stdlib.h>
 
 namespace kpo {
 namespace gemm {
@@ -34,8 +35,8 @@ struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (BN == 256) ? 4 : 6;
-  static constexpr int TMEM_COLS = 2 * BN;  // double-buffered accumulator (power of two)
+  static constexpr int STAGES = (BN == 256) ? 4 : (BN == 192 ? 5 : 6);
+  static constexpr int TMEM_COLS = (2 * BN <= 256) ? 256 : 512;  // double-buffered accumulator (power of two)
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;  // + barriers + alignment slack
 };
@@ -269,6 +270,258 @@ static int launch(const CUtensorMap& ta, const CUtensorMap& tb, void* D, const v
   return KPO_OK;
 }
 
+
+// =====================================================================================
+// CTA-pair variant (tcgen05.mma.cta_group::2): one 256 x BN tile per cluster of 2 CTAs on the
+// same TPC.  A is split by M (each CTA stages its 128 rows), B is split by N (each CTA stages BN/2
+// columns); the leader (rank 0) issues the M=256 MMAs, which read both CTAs' shared memory, and
+// each CTA's TMEM receives its 128 accumulator rows.  Per CTA this halves B's shared-memory traffic
+// per FLOP versus the 1-CTA kernel (64 B/clk instead of 96 B/clk at BN=256).
+//   * both CTAs' TMA loads complete on the leader's full[] barrier (peer bit cleared);
+//   * MMA completion is multicast (tcgen05.commit ... multicast::cluster, mask 0b11) to the
+//     empty[] / tfull[] barriers of both CTAs;
+//   * the leader fetches tile ids from the global scheduler word and broadcasts them to the peer
+//     through distributed shared memory; consumers in the peer arrive remotely on the leader's
+//     sempty[] / tempty[] barriers.
+template <int BN>
+struct Cfg2 {
+  static constexpr int A_BYTES = 128 * BK * 2;
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (BN == 256) ? 6 : 7;
+  static constexpr int TMEM_COLS = (2 * BN <= 256) ? 256 : 512;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+};
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 __nv_bfloat16* __restrict__ D, const __nv_bfloat16* __restrict__ C, int M, int N, int K,
+                 int64_t ldd, int* __restrict__ sched) {
+  using CF = Cfg2<BN>;
+  constexpr int STAGES = CF::STAGES;
+  constexpr int HB = BN / 2;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + CF::BAR_OFF);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES;
+  uint64_t* tfull = bars + 2 * STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* sfull = tempty + 2;
+  uint64_t* sempty = sfull + 2;
+  int* stile = reinterpret_cast<int*>(sempty + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stile + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int num_m = (M + 255) / 256, num_n = (N + BN - 1) / BN;
+  const int num_tiles = num_m * num_n;
+  const int num_kb = (K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&tfull[i]), 1);
+      mbar_init(smem_u32(&tempty[i]), 8);
+      mbar_init(smem_u32(&sfull[i]), 1);
+      mbar_init(smem_u32(&sempty[i]), 10);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1) tmem_alloc_pair(smem_u32(tmem_slot), CF::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t leader_sempty0 = mapa(smem_u32(&sempty[0]), 0);
+  const uint32_t leader_tempty0 = mapa(smem_u32(&tempty[0]), 0);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===================== tile scheduler (leader) + TMA producer (both CTAs)
+      int it = 0, stage = 0;
+      uint32_t phase = 0;
+      while (true) {
+        const int slot = it & 1;
+        int tile;
+        if (leader) {
+          tile = atomicAdd(&sched[0], 1);
+          mbar_wait_cluster(smem_u32(&sempty[slot]), ((it >> 1) & 1) ^ 1);
+          stile[slot] = tile;
+          st_cluster_u32(mapa(smem_u32(&stile[slot]), 1), (uint32_t)tile);
+          mbar_arrive(smem_u32(&sfull[slot]));
+          mbar_arrive_remote(mapa(smem_u32(&sfull[slot]), 1));
+        } else {
+          mbar_wait_cluster(smem_u32(&sfull[slot]), (it >> 1) & 1);
+          tile = stile[slot];
+          mbar_arrive_remote(leader_sempty0 + slot * 8);
+        }
+        ++it;
+        if (tile >= num_tiles) break;
+        int mb, nb;
+        tile_coords(tile, num_m, num_n, mb, nb);
+        const int m0 = mb * 256 + (int)rank * 128, n0 = nb * BN + (int)rank * HB;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+          const uint32_t fb = smem_u32(&full[stage]);
+          if (leader) mbar_arrive_expect_tx(fb, 2 * CF::STAGE_BYTES);
+          const uint32_t sa = smem_u32(smem + stage * CF::STAGE_BYTES);
+          const uint32_t sb = sa + CF::A_BYTES;
+          const int k0 = kb * BK;
+          if (!A_MN) {
+            tma_load_2d_pair(sa, &tmA, fb, k0, m0);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 2; ++c) tma_load_2d_pair(sa + c * (BK * 128), &tmA, fb, m0 + c * 64, k0);
+          }
+          if (!B_MN) {
+            tma_load_2d_pair(sb, &tmB, fb, k0, n0);
+          } else {
+#pragma unroll
+            for (int c = 0; c < HB / 64; ++c) tma_load_2d_pair(sb + c * (BK * 128), &tmB, fb, n0 + c * 64, k0);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+      if (leader) {
+        __threadfence();
+        const int done = atomicAdd(&sched[1], 1);
+        if (done == (int)(gridDim.x / 2) - 1) {
+          sched[0] = 0;
+          sched[1] = 0;
+          __threadfence();
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      // ===================== MMA issuer (leader only, M = 256 across the pair)
+      constexpr uint32_t IDESC = idesc_bf16(256, BN, A_MN, B_MN);
+      constexpr uint32_t A_LBO = A_MN ? BK * 128 : 16, A_SBO = 1024;
+      constexpr uint32_t B_LBO = B_MN ? BK * 128 : 16, B_SBO = 1024;
+      constexpr uint32_t A_KSTEP = A_MN ? 16 * 128 : 32;
+      constexpr uint32_t B_KSTEP = B_MN ? 16 * 128 : 32;
+      int it = 0, stage = 0, acc_it = 0;
+      uint32_t phase = 0;
+      while (true) {
+        const int slot = it & 1;
+        mbar_wait(smem_u32(&sfull[slot]), (it >> 1) & 1);
+        const int tile = stile[slot];
+        mbar_arrive(smem_u32(&sempty[slot]));
+        ++it;
+        if (tile >= num_tiles) break;
+        const int acc = acc_it & 1;
+        mbar_wait_cluster(smem_u32(&tempty[acc]), ((acc_it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(smem_u32(&full[stage]), phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * CF::STAGE_BYTES);
+          const uint32_t sb = sa + CF::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            tc_mma_pair(d_tmem, smem_desc(sa + k * A_KSTEP, A_LBO, A_SBO), smem_desc(sb + k * B_KSTEP, B_LBO, B_SBO),
+                        IDESC, (kb | k) != 0);
+          }
+          tc_commit_pair(smem_u32(&empty[stage]));
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit_pair(smem_u32(&tfull[acc]));
+        ++acc_it;
+      }
+    }
+  } else {
+    // ===================== epilogue warps 2..5 (both CTAs): this CTA's 128 rows, all BN columns
+    const int q = warp & 3;
+    int it = 0, acc_it = 0;
+    while (true) {
+      const int slot = it & 1;
+      if (leader) mbar_wait(smem_u32(&sfull[slot]), (it >> 1) & 1);
+      else mbar_wait_cluster(smem_u32(&sfull[slot]), (it >> 1) & 1);
+      const int tile = stile[slot];
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) mbar_arrive(smem_u32(&sempty[slot]));
+        else mbar_arrive_remote(leader_sempty0 + slot * 8);
+      }
+      ++it;
+      if (tile >= num_tiles) break;
+      int mb, nb;
+      tile_coords(tile, num_m, num_n, mb, nb);
+      const int acc = acc_it & 1;
+      mbar_wait(smem_u32(&tfull[acc]), (acc_it >> 1) & 1);
+      tc_fence_after();
+      const int row = mb * 256 + (int)rank * 128 + q * 32 + lane;
+      const bool row_ok = row < M;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
+        const int col0 = nb * BN + c * 32;
+        if (row_ok) {
+          __nv_bfloat16* drow = D + (int64_t)row * ldd;
+          const __nv_bfloat16* crow = C ? C + (int64_t)row * ldd : nullptr;
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int col = col0 + v * 8;
+            if (col < N) {
+              float f[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) f[j] = __uint_as_float(r[v * 8 + j]);
+              if (crow) {
+                float cf[8];
+                unpack8(*reinterpret_cast<const uint4*>(crow + col), cf);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) f[j] += cf[j];
+              }
+              *reinterpret_cast<uint4*>(drow + col) = pack8(f);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(leader_tempty0 + acc * 8);
+      ++acc_it;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc_pair(tmem_base, CF::TMEM_COLS);
+}
+
+template <int BN, bool A_MN, bool B_MN>
+static int launch2(const CUtensorMap& ta, const CUtensorMap& tb, void* D, const void* C, int64_t M, int64_t N,
+                   int64_t K, int64_t ldd, int grid, int* sched, cudaStream_t s) {
+  auto kern = gemm2_kernel<BN, A_MN, B_MN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    KPO_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2<BN>::SMEM));
+    attr_set = true;
+  }
+  kern<<<grid, kThreads, Cfg2<BN>::SMEM, s>>>(ta, tb, (__nv_bfloat16*)D, (const __nv_bfloat16*)C, (int)M, (int)N,
+                                               (int)K, ldd, sched);
+  KPO_LAUNCH_CHECK();
+  return KPO_OK;
+}
 }  // namespace gemm
 
 namespace sm100 {
@@ -348,18 +601,68 @@ extern "C" int kpo_gemm(const void* A, const void* B, void* D, const void* C, in
   KPO_CHECK_ARG(a_mn_major ? lda >= M : lda >= K, "gemm: lda too small");
   KPO_CHECK_ARG(b_mn_major ? ldb >= N : ldb >= K, "gemm: ldb too small");
   const int sms = num_sms();
-  // tile width: best SM-wave efficiency, ties -> 256
-  auto eff = [&](int bn) {
-    const int64_t tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
-    const int64_t waves = (tiles + sms - 1) / sms;
-    return (double)tiles / (double)(waves * sms) * (double)(bn == 256 ? 1.0 : 0.93);
+  // Tile choice: maximise (useful fraction of padded N) x (SM-wave fill) x (per-tile efficiency measured on
+  // B200 for the layer shapes, tools/gemm_bench.py): CTA-pair 256xBN tiles halve B's shared-memory
+  // traffic per FLOP; single-CTA BN=128 tiles are shared-memory-bandwidth bound.
+  struct Choice { bool pair; int bn; double base; };
+  const Choice choices[] = {{true, 256, 1.00}, {true, 128, 0.74}, {false, 256, 0.90}, {false, 192, 0.86},
+                            {false, 128, 0.64}};
+  auto eff = [&](const Choice& c) {
+    const int units = c.pair ? sms / 2 : sms;
+    const int bm = c.pair ? 256 : BM;
+    const int64_t nt = (N + c.bn - 1) / c.bn;
+    const int64_t tiles = ((M + bm - 1) / bm) * nt;
+    const int64_t waves = (tiles + units - 1) / units;
+    const double mfill = (double)M / (double)(((M + bm - 1) / bm) * bm);
+    return (double)N / (double)(nt * c.bn) * mfill * (double)tiles / (double)(waves * units) * c.base;
   };
-  const int bn = eff(256) >= eff(128) ? 256 : 128;
+  static const bool no_pair = getenv("KPO_GEMM_NO_PAIR") != nullptr;
+  Choice best = {false, 256, 0.0};
+  double best_eff = -1.0;
+  for (const Choice& c : choices) {
+    if (c.pair && (no_pair || M < 256)) continue;
+    const double e = eff(c);
+    if (e > best_eff * 1.01) {
+      best = c;
+      best_eff = e;
+    }
+  }
+  const int bn = best.bn;
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
   int cap = max_ctas > 0 ? max_ctas : sms;
   if (cap > sms) cap = sms;
   const int grid = (int)(tiles < cap ? tiles : cap);
 
+  // CTA-pair (cta_group::2) path: 256 x BN tiles, BN in {256, 128} chosen by the same wave model
+  if (best.pair) {
+    const int clusters = sms / 2;
+    const int bn2 = best.bn;
+    const int64_t tiles2 = ((M + 255) / 256) * ((N + bn2 - 1) / bn2);
+    int cap2 = max_ctas > 0 ? max_ctas / 2 : clusters;
+    if (cap2 < 1) cap2 = 1;
+    if (cap2 > clusters) cap2 = clusters;
+    const int grid2 = 2 * (int)(tiles2 < cap2 ? tiles2 : cap2);
+    CUtensorMap ta2, tb2;
+    int st2;
+    if (!a_mn_major) st2 = make_map_2d(&ta2, A, K, M, lda, BK, 128);
+    else st2 = make_map_2d(&ta2, A, M, K, lda, 64, BK);
+    if (st2) return st2;
+    if (!b_mn_major) st2 = make_map_2d(&tb2, B, K, N, ldb, BK, bn2 / 2);
+    else st2 = make_map_2d(&tb2, B, N, K, ldb, 64, BK);
+    if (st2) return st2;
+    cudaStream_t s2 = (cudaStream_t)stream;
+#define KPO_GEMM2_DISPATCH(BNv)                                                                                    \
+  if (!a_mn_major && !b_mn_major) return launch2<BNv, false, false>(ta2, tb2, D, C, M, N, K, ldd, grid2, sched, s2); \
+  if (!a_mn_major && b_mn_major) return launch2<BNv, false, true>(ta2, tb2, D, C, M, N, K, ldd, grid2, sched, s2);   \
+  if (a_mn_major && !b_mn_major) return launch2<BNv, true, false>(ta2, tb2, D, C, M, N, K, ldd, grid2, sched, s2);   \
+  return launch2<BNv, true, true>(ta2, tb2, D, C, M, N, K, ldd, grid2, sched, s2);
+    if (bn2 == 256) {
+      KPO_GEMM2_DISPATCH(256)
+    } else {
+      KPO_GEMM2_DISPATCH(128)
+    }
+#undef KPO_GEMM2_DISPATCH
+  }
   CUtensorMap ta, tb;
   int st;
   if (!a_mn_major) st = make_map_2d(&ta, A, K, M, lda, BK, BM);
@@ -376,6 +679,8 @@ extern "C" int kpo_gemm(const void* A, const void* B, void* D, const void* C, in
   return launch<BNv, true, true>(ta, tb, D, C, M, N, K, ldd, grid, sched, s);
   if (bn == 256) {
     KPO_GEMM_DISPATCH(256)
+  } else if (bn == 192) {
+    KPO_GEMM_DISPATCH(192)
   } else {
     KPO_GEMM_DISPATCH(128)
   }

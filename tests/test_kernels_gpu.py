@@ -13,7 +13,7 @@ def rel_err(a, b):
     return ((a - b).norm() / b.norm().clamp_min(1e-12)).item()
 
 
-@pytest.mark.parametrize("M,N,K", [(256, 256, 64), (128, 128, 128), (4096, 3072, 3072), (1000, 776, 520),
+@pytest.mark.parametrize("M,N,K", [(256, 256, 64), (128, 128, 128), (4096, 3072, 3072), (1000, 776, 520), (4096, 5120, 512), (3072, 8192, 256),
                                    (4096, 768, 4096), (384, 16384, 256)])
 @pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, False), (True, True)])
 def test_gemm_all_majors(cuda, M, N, K, a_mn, b_mn):

@@ -306,15 +306,18 @@ int fwd_launch(const void* q, const void* k, const void* v, void* o, float* lse,
 // step s+1 and the dQ drain of step s overlap the tensor core.
 template <int D>
 struct Bwd {
-  static constexpr int BN = 128, BM = 64;
+  static constexpr int BN = 128, BM = 64, QSTAGES = 3;
   static constexpr int KV_BYTES = BN * D * 2;
   static constexpr int QT_BYTES = BM * D * 2;
   static constexpr int PT_BYTES = BN * BM * 2;
+  // P^T | dS^T pair per buffer (2 buffers); once the step's MMAs are done the 32 KB pair doubles as
+  // the fp32 [64 q][D] dQ staging tile of the TMA reduce-add.
+  static constexpr int PDS_BYTES = 2 * PT_BYTES;
+  static_assert(PDS_BYTES >= BM * D * 4, "dQ staging must fit in a P/dS buffer pair");
   static constexpr int OFF_K = 0, OFF_V = OFF_K + KV_BYTES, OFF_Q = OFF_V + KV_BYTES;
-  static constexpr int OFF_DO = OFF_Q + 2 * QT_BYTES, OFF_P = OFF_DO + 2 * QT_BYTES;  // P^T, dS^T: 2 buffers each
-  static constexpr int OFF_DS = OFF_P + 2 * PT_BYTES, OFF_STAT = OFF_DS + 2 * PT_BYTES;
-  static constexpr int OFF_DQ = OFF_STAT + 2 * 2 * BM * 4;  // fp32 [64 q][D] staging for the TMA reduce-add
-  static constexpr int OFF_BAR = OFF_DQ + BM * D * 4;
+  static constexpr int OFF_DO = OFF_Q + QSTAGES * QT_BYTES, OFF_PDS = OFF_DO + QSTAGES * QT_BYTES;
+  static constexpr int OFF_STAT = OFF_PDS + 2 * PDS_BYTES;
+  static constexpr int OFF_BAR = OFF_STAT + QSTAGES * 2 * BM * 4;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
   static constexpr int COL_S = 0, COL_DP = 64, COL_DQ = 128, COL_DV = 256, COL_DK = 384;  // dQ^T: 128 + 64*b
   static constexpr int THREADS = 448;  // TMA, MMA, 8 softmax warps (2 per lane quarter), 4 dQ-drain warps
@@ -337,16 +340,16 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* kv_full = bar + 0;
-  uint64_t* qd_full = bar + 1;   // [2]
-  uint64_t* qd_empty = bar + 3;  // [2]
-  uint64_t* s_full = bar + 5;
-  uint64_t* s_empty = bar + 6;
-  uint64_t* pds_full = bar + 7;    // [2]
-  uint64_t* pds_empty = bar + 9;   // [2]
-  uint64_t* dq_full = bar + 11;    // [2]
-  uint64_t* dq_empty = bar + 13;   // [2]
-  uint64_t* acc_done = bar + 15;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+  uint64_t* qd_full = bar + 1;     // [3]
+  uint64_t* qd_empty = bar + 4;    // [3]
+  uint64_t* s_full = bar + 7;
+  uint64_t* s_empty = bar + 8;
+  uint64_t* pds_full = bar + 9;    // [2]
+  uint64_t* pds_empty = bar + 11;  // [2]  MMA commit + dQ drain (staging read by TMA)
+  uint64_t* dq_full = bar + 13;    // [2]
+  uint64_t* dq_empty = bar + 15;   // [2]
+  uint64_t* acc_done = bar + 17;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 18);
   float* stat = reinterpret_cast<float*>(smem + C::OFF_STAT);  // [2][lse2 64 | dvec 64]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -361,7 +364,7 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(smem_u32(kv_full), 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < C::QSTAGES; ++i) {
       mbar_init(smem_u32(&qd_full[i]), 1);
       mbar_init(smem_u32(&qd_empty[i]), 1);
     }
@@ -369,7 +372,7 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
     mbar_init(smem_u32(s_empty), C::SM_WARPS);
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&pds_full[i]), C::SM_WARPS);
-      mbar_init(smem_u32(&pds_empty[i]), 1);
+      mbar_init(smem_u32(&pds_empty[i]), 2);
       mbar_init(smem_u32(&dq_full[i]), 1);
       mbar_init(smem_u32(&dq_empty[i]), 4);
     }
@@ -383,7 +386,7 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t sK = smem_u32(smem + C::OFF_K), sV = smem_u32(smem + C::OFF_V);
   const uint32_t sQ = smem_u32(smem + C::OFF_Q), sDO = smem_u32(smem + C::OFF_DO);
-  const uint32_t sP = smem_u32(smem + C::OFF_P), sDS = smem_u32(smem + C::OFF_DS);
+  const uint32_t sPDS = smem_u32(smem + C::OFF_PDS);  // buffer b: P^T at b*PDS_BYTES, dS^T at +PT_BYTES
 
   auto step_coords = [&](int s, int& h, int& m0) {
     h = kvh * group + s / mq;
@@ -400,10 +403,10 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
         tma_load_2d(sV + kb * BN * 128, &tmV, smem_u32(kv_full), kvh * D + kb * 64, n0);
       }
       for (int s = 0; s < steps; ++s) {
-        const int st = s & 1;
+        const int st = s % C::QSTAGES;
         int h, m0;
         step_coords(s, h, m0);
-        mbar_wait(smem_u32(&qd_empty[st]), ((s >> 1) & 1) ^ 1);
+        mbar_wait(smem_u32(&qd_empty[st]), ((s / C::QSTAGES) & 1) ^ 1);
         const uint32_t fb = smem_u32(&qd_full[st]);
         const uint32_t nstat = (uint32_t)min(BM, T - m0) * 4u;  // T % 8 == 0 keeps this a 16 B multiple
         mbar_arrive_expect_tx(fb, 2 * C::QT_BYTES + 2 * nstat);
@@ -425,11 +428,12 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
       constexpr uint32_t ID_Q = idesc_bf16(D, BM, true, true);      // dQ^T
       mbar_wait(smem_u32(kv_full), 0);
       auto grads = [&](int j) {
-        const int st = j & 1;
+        const int st = j & 1;          // P/dS and dQ^T buffer
+        const int qs = j % C::QSTAGES;  // Q/dO stage
         mbar_wait(smem_u32(&pds_full[st]), (j >> 1) & 1);
         tc_fence_after();
-        const uint32_t qb = sQ + st * C::QT_BYTES, ob = sDO + st * C::QT_BYTES;
-        const uint32_t pb = sP + st * C::PT_BYTES, db = sDS + st * C::PT_BYTES;
+        const uint32_t qb = sQ + qs * C::QT_BYTES, ob = sDO + qs * C::QT_BYTES;
+        const uint32_t pb = sPDS + st * C::PDS_BYTES, db = pb + C::PT_BYTES;
 #pragma unroll
         for (int k = 0; k < BM / 16; ++k) {
           const uint32_t acc = (j > 0 || k > 0) ? 1u : 0u;
@@ -447,11 +451,11 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
         }
         tc_commit(smem_u32(&dq_full[st]));
         tc_commit(smem_u32(&pds_empty[st]));
-        tc_commit(smem_u32(&qd_empty[st]));
+        tc_commit(smem_u32(&qd_empty[qs]));
       };
       auto scores = [&](int s) {
-        const int st = s & 1;
-        mbar_wait(smem_u32(&qd_full[st]), (s >> 1) & 1);
+        const int st = s % C::QSTAGES;
+        mbar_wait(smem_u32(&qd_full[st]), (s / C::QSTAGES) & 1);
         tc_fence_after();
         const uint32_t qb = sQ + st * C::QT_BYTES, ob = sDO + st * C::QT_BYTES;
 #pragma unroll
@@ -491,7 +495,7 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
       step_coords(s, h, m0);
       (void)h;
       const int buf = s & 1;
-      const float* st = stat + buf * 2 * BM;  // lse*log2e is applied below; filled by the TMA warp
+      const float* st = stat + (s % C::QSTAGES) * 2 * BM;  // raw lse / D rows, filled by the TMA warp
       mbar_wait(smem_u32(s_full), s & 1);
       tc_fence_after();
       float sv[HC], dp[HC];
@@ -503,7 +507,7 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
       if (lane == 0) mbar_arrive(smem_u32(s_empty));
       mbar_wait(smem_u32(&pds_empty[buf]), ((s >> 1) & 1) ^ 1);  // grads(s-2) done with this buffer
       const bool mask = (causal && m0 < n0 + BN - 1) || key >= T || m0 + BM > T;
-      const uint32_t pb = sP + buf * C::PT_BYTES, db = sDS + buf * C::PT_BYTES;
+      const uint32_t pb = sPDS + buf * C::PDS_BYTES, db = pb + C::PT_BYTES;
 #pragma unroll
       for (int ch = 0; ch < HC / 8; ++ch) {
         float p[8], ds[8];
@@ -582,10 +586,9 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&dq_empty[buf]));
-      // staging tile free? (the previous TMA reduce has finished reading it)
-      if (dtid == 0) bulk_wait_read0();
-      named_bar(2, 128);
-      float* stg = reinterpret_cast<float*>(smem + C::OFF_DQ);
+      // stage dQ (fp32 [64 q][D]) in this step's P/dS buffer pair: every MMA that read it has completed
+      // (dq_full is committed after them); the softmax waits for our arrival before reusing it.
+      float* stg = reinterpret_cast<float*>(smem + C::OFF_PDS + buf * C::PDS_BYTES);
 #pragma unroll
       for (int qi = 0; qi < BM; ++qi) stg[qi * D + dcol] = v[qi] * scale;
       fence_async_smem();
@@ -593,6 +596,8 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
       if (dtid == 0) {
         tma_reduce_add_2d(&tmDQ, smem_u32(stg), h * D, m0);
         bulk_commit();
+        bulk_wait_read0();
+        mbar_arrive(smem_u32(&pds_empty[buf]));
       }
     }
     if (dtid == 0) bulk_wait0();

@@ -138,6 +138,69 @@ __global__ void __launch_bounds__(kNormBwdWarps * 32)
   for (int i = threadIdx.x; i < cols; i += blockDim.x) out[i] = dw_smem[i];
 }
 
+// Register-accumulating variant for cols = 256*NV: lane l owns the 8-column chunks l, l+32, ...;
+// each warp walks rows with a grid-wide stride, accumulating dw in registers, and flushes once into
+// the CTA's shared row (8-way, not per-row, contention); one partial row per CTA.
+template <int NV>
+__global__ void __launch_bounds__(256, 1)
+    rmsnorm_bwd_reg(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+                    const __nv_bfloat16* __restrict__ w, const float* __restrict__ rstd,
+                    const __nv_bfloat16* __restrict__ dres, __nv_bfloat16* __restrict__ dx,
+                    float* __restrict__ dw_partial, int64_t rows, int cols) {
+  extern __shared__ float dw_smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < cols; i += blockDim.x) dw_smem[i] = 0.f;
+  float acc[NV * 8];
+#pragma unroll
+  for (int i = 0; i < NV * 8; ++i) acc[i] = 0.f;
+  const uint4* wr = reinterpret_cast<const uint4*>(w);
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; row < rows; row += nwarps) {
+    const uint4* xr = reinterpret_cast<const uint4*>(x + row * cols);
+    const uint4* dyr = reinterpret_cast<const uint4*>(dy + row * cols);
+    const float r = rstd[row];
+    float dot = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      float a[8], b[8], g[8];
+      unpack8(ld_nc_v4(xr + lane + 32 * i), a);
+      unpack8(ld_nc_v4(dyr + lane + 32 * i), b);
+      unpack8(wr[lane + 32 * i], g);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) dot += g[j] * b[j] * a[j];
+    }
+    dot = warp_sum(dot);
+    const float c = dot * r * r * r / (float)cols;
+    uint4* dxr = reinterpret_cast<uint4*>(dx + row * cols);
+    const uint4* dresr = dres ? reinterpret_cast<const uint4*>(dres + row * cols) : nullptr;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {  // second pass re-reads x / dy from L1
+      float a[8], b[8], g[8], o[8];
+      unpack8(xr[lane + 32 * i], a);
+      unpack8(dyr[lane + 32 * i], b);
+      unpack8(wr[lane + 32 * i], g);
+      float res[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      if (dresr) unpack8(ld_nc_v4(dresr + lane + 32 * i), res);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        o[j] = r * g[j] * b[j] - a[j] * c + res[j];
+        acc[i * 8 + j] += b[j] * a[j] * r;
+      }
+      dxr[lane + 32 * i] = pack8(o);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) atomicAdd(&dw_smem[(lane + 32 * i) * 8 + j], acc[i * 8 + j]);
+  __syncthreads();
+  float* out = dw_partial + (int64_t)blockIdx.x * cols;
+  for (int i = threadIdx.x; i < cols; i += blockDim.x) out[i] = dw_smem[i];
+}
+
+static bool norm_bwd_reg_ok(int64_t cols) { return cols % 256 == 0 && cols / 256 >= 1 && cols / 256 <= 16; }
+
 // out[c] = sum_r in[r, c]; one thread per column, coalesced across the warp.
 __global__ void colsum_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
                               int64_t rows, int64_t cols) {
@@ -273,10 +336,15 @@ extern "C" int kpo_rmsnorm_fwd(const void* x, const void* w, void* y, float* rst
   return KPO_OK;
 }
 
+static int64_t norm_bwd_reg_grid(int64_t rows) {
+  const int64_t want = (rows + 7) / 8;
+  const int64_t sms = num_sms();
+  return want < sms ? (want > 0 ? want : 1) : sms;
+}
+
 extern "C" int kpo_rmsnorm_bwd_partial_rows(int64_t rows, int64_t cols, int64_t* n_partials) {
   KPO_CHECK_ARG(n_partials, "null n_partials");
-  (void)cols;
-  *n_partials = (rows + kNormBwdRowsPerBlock - 1) / kNormBwdRowsPerBlock;
+  *n_partials = norm_bwd_reg_ok(cols) ? norm_bwd_reg_grid(rows) : (rows + kNormBwdRowsPerBlock - 1) / kNormBwdRowsPerBlock;
   return KPO_OK;
 }
 
@@ -286,8 +354,31 @@ extern "C" int kpo_rmsnorm_bwd(const void* dy, const void* x, const void* w, con
   KPO_CHECK_ARG(dy && x && w && rstd && dx && dw_partial, "rmsnorm_bwd: null pointer");
   KPO_CHECK_ARG(cols > 0 && cols % 8 == 0 && cols * 4 <= 200 * 1024, "rmsnorm_bwd: bad cols");
   if (rows == 0) return KPO_OK;
-  const unsigned blocks = (unsigned)((rows + kNormBwdRowsPerBlock - 1) / kNormBwdRowsPerBlock);
   const size_t smem = (size_t)cols * sizeof(float);
+  if (norm_bwd_reg_ok(cols)) {
+    const unsigned grid = (unsigned)norm_bwd_reg_grid(rows);
+    cudaStream_t st = (cudaStream_t)stream;
+    auto Dy = (const __nv_bfloat16*)dy;
+    auto X = (const __nv_bfloat16*)x;
+    auto W = (const __nv_bfloat16*)w;
+    auto Dr = (const __nv_bfloat16*)dres;
+    auto Dx = (__nv_bfloat16*)dx;
+    switch (cols / 256) {
+#define KPO_NB_CASE(n)                                                                                    \
+  case n:                                                                                                 \
+    if (smem > 48 * 1024)                                                                                 \
+      KPO_CUDA(cudaFuncSetAttribute(rmsnorm_bwd_reg<n>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    rmsnorm_bwd_reg<n><<<grid, 256, smem, st>>>(Dy, X, W, rstd, Dr, Dx, dw_partial, rows, (int)cols);       \
+    break;
+      KPO_NB_CASE(1) KPO_NB_CASE(2) KPO_NB_CASE(3) KPO_NB_CASE(4) KPO_NB_CASE(5) KPO_NB_CASE(6) KPO_NB_CASE(7)
+      KPO_NB_CASE(8) KPO_NB_CASE(9) KPO_NB_CASE(10) KPO_NB_CASE(11) KPO_NB_CASE(12) KPO_NB_CASE(13)
+      KPO_NB_CASE(14) KPO_NB_CASE(15) KPO_NB_CASE(16)
+#undef KPO_NB_CASE
+    }
+    KPO_LAUNCH_CHECK();
+    return KPO_OK;
+  }
+  const unsigned blocks = (unsigned)((rows + kNormBwdRowsPerBlock - 1) / kNormBwdRowsPerBlock);
   if (smem > 48 * 1024)
     KPO_CUDA(cudaFuncSetAttribute(rmsnorm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   rmsnorm_bwd_kernel<<<blocks, kNormBwdWarps * 32, smem, (cudaStream_t)stream>>>(

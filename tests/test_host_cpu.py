@@ -1,0 +1,95 @@
+"""Host-side logic that needs no GPU: partition specs, profiler batching/resume, bench contract."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+from paper_2601_17654_b200 import (LaunchTiming, Measurement, ScheduleConfig, analytic_kernel_ms, b200_model, specs)
+from paper_2601_17654_b200.model import PRESETS, Workload, baseline_workload
+from paper_2601_17654_b200.profiler import ProfileTable, Profiler
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("idx", [0, 1, 2, 3])
+def test_partition_specs_shapes(idx):
+    wl = baseline_workload(idx)
+    parts = specs.partition_specs(wl)
+    assert [p.name for p in parts] == ["fwd_attn0", "fwd_attn1", "fwd_mlp0", "fwd_mlp1", "bwd_mlp0", "bwd_mlp1",
+                                       "bwd_attn0", "bwd_attn1"]
+    assert [len(p.comp_kernels) for p in parts] == [5, 5, 4, 4, 6, 6, 7, 7]
+    for p in parts:
+        assert p.comm_kernel.is_comm and p.comm_group_size == wl.world
+        kinds = {k.name: k.kind for k in p.comp_kernels}
+        for name, kind in kinds.items():
+            if name.startswith(("linear", "o_", "qkv_", "gu_", "down_", "attention")):
+                assert kind == "compute-bound", name
+            else:
+                assert kind == "memory-bound", name
+    # backward GEMM FLOPs = 2x forward GEMM FLOPs per nanobatch
+    us = specs.unit_specs(wl)
+    fwd = sum(us[k].flops for k in ("linear_qkv", "linear_proj", "linear_up", "linear_down"))
+    bwd = sum(us[k].flops for k in us if k.endswith(("_dgrad", "_wgrad")))
+    assert bwd == pytest.approx(2 * fwd)
+
+
+def test_fsdp_comm_bytes_cover_every_weight_once_per_direction():
+    wl = baseline_workload(1)
+    parts = specs.partition_specs(wl)
+    total = sum(p.comm_kernel.comm_bytes for p in parts)
+    w = sum(wl.weight_numels().values()) * 2 * (wl.world - 1) / wl.world
+    # forward all-gathers once, backward re-gathers once and reduce-scatters once
+    assert total == pytest.approx(3 * w)
+
+
+def test_tp_shapes_per_rank():
+    wl = baseline_workload(2)
+    assert (wl.hq, wl.hkv, wl.ffn, wl.qkv_dim) == (4, 1, 1792, 768)
+    assert Workload(PRESETS["llama-3-70b"], "tp", 8, 4096).hkv == 1
+
+
+def test_analytic_pruning_model_on_b200_descriptor():
+    gpu = b200_model()
+    assert gpu.num_sms == 148 and gpu.f_max_mhz == 1965.0
+    part = specs.partition_specs(baseline_workload(1))[2]
+    gemm = next(k for k in part.comp_kernels if k.name == "linear_up")
+    t = analytic_kernel_ms(gemm, gpu.f_max_mhz, gpu.num_sms, gpu)
+    assert t == pytest.approx(gemm.flops / 1640.5e12 * 1e3, rel=1e-9)
+
+
+class _FakeEngine:
+    def __init__(self):
+        self.calls = 0
+        self.last = None
+
+    def measure(self, part, cfg, gpu, thermal, protocol, state):
+        self.calls += 1
+        return Measurement.build(1.0 + cfg.sm_alloc / 100.0, 0.5, gpu.p_static_w)
+
+
+def test_profiler_collects_and_resumes(tmp_path):
+    gpu = b200_model()
+    part = specs.partition_specs(baseline_workload(1))[0]
+    cfgs = [ScheduleConfig(1965.0, sm, LaunchTiming.overlap(0, 5)) for sm in (4, 8, 16)]
+    eng = _FakeEngine()
+    t = Profiler(eng, gpu, None).collect(part, cfgs[:2])
+    assert len(t) == 2 and eng.calls == 2
+    t = Profiler(eng, gpu, None).collect(part, cfgs, table=t)  # resume: only the missing config runs
+    assert len(t) == 3 and eng.calls == 3
+    t.write(str(tmp_path / "t.jsonl"))
+    assert ProfileTable.read(str(tmp_path / "t.jsonl")).lookup(cfgs[2]).time_ms == 1.16
+
+
+def test_bench_reference_arm_contract():
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "0", "--cpu-tokens", "128"], capture_output=True, text=True, timeout=600,
+                         cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for key in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "cpu_baseline", "e2e"):
+        assert key in line, key
+    assert line["impl"] == "reference" and line["e2e"]["h2d_bytes_per_step"] == 0
+    assert line["cpu_baseline"]["kind"] == "port" and line["value"] > 0

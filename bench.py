@@ -326,6 +326,21 @@ def run_kpo(args):
                "sample": f"oracle/layer_ref.py fp32 fwd+bwd of 1 nanobatch x {args.cpu_tokens} tokens "
                          f"({r['sample_s']:.2f} s), scaled x{r['scale']:.1f} by FLOPs to the full iteration"}
 
+    # iteration-level roofline: T_lb = max(F_tc / P_tc, B_hbm / BW_hbm, B_link / BW_link)
+    specs_all = [u.spec for name in layer.order for u in layer.programs[name].units]
+    f_tc = sum(sp.flops for sp in specs_all if sp.kind == "compute-bound")
+    b_hbm = sum(sp.bytes for sp in specs_all if sp.kind == "memory-bound")
+    b_link = sum(layer.programs[name].comm.algo_bytes for name in layer.order)
+    link_bw = (hbm if world == 1 else 770.0) * 1e9  # loopback moves the "link" bytes through HBM
+    t_lb = max(f_tc / (tf_sust * 1e12), b_hbm / (hbm * 1e9), b_link / link_bw)
+    iter_roofline = {"t_lb_ms": round(t_lb * 1e3, 4), "t_meas_ms": round(ms, 4), "frac": round(t_lb * 1e3 / ms, 4),
+                     "tensor_flops": f_tc, "hbm_bytes": b_hbm, "link_bytes": b_link,
+                     "bounds_ms": {"tensor": round(f_tc / (tf_sust * 1e12) * 1e3, 4),
+                                   "hbm": round(b_hbm / (hbm * 1e9) * 1e3, 4),
+                                   "link": round(b_link / link_bw * 1e3, 4)},
+                     "peaks": f"{peak_src}: {tf_sust} TF/s sustained bf16, {hbm} GB/s HBM, "
+                              f"{'HBM (loopback)' if world == 1 else '770 GB/s NVLink per direction'}"}
+
     if rank == 0:
         launches = run.kernels_per_step() * args.steps
         line = {
@@ -354,6 +369,7 @@ def run_kpo(args):
                          "algorithmic_per_launch": dom_unit.spec.flops if dom_row["bound"] == "tensor"
                          else dom_unit.spec.bytes, "avg_launch_ms": dom_row["avg_launch_ms"]},
             "kernels": kernels,
+            "iteration_roofline": iter_roofline,
             "comm": {"mode": "loopback (HBM)" if world == 1 else "cuda-ipc p2p (NVLink)", "units": comm_rows},
             "frontier": frontier,
             "cpu_baseline": cpu,

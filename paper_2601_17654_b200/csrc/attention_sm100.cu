@@ -194,7 +194,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         m_run = mx;
       }
       if (j >= 2) mbar_wait(smem_u32(&pv_done[s]), ((j - 2) >> 1) & 1);  // P[s] free (PV(j-2) done)
-      if (rescale) {
+      // tcgen05.ld/st are warp-collective (.sync.aligned): the rescale decision must be warp-uniform;
+      // lanes that do not need it multiply by corr == 1.
+      if (__any_sync(0xffffffffu, rescale)) {
         mbar_wait(smem_u32(&pv_done[s ^ 1]), ((j - 1) >> 1) & 1);  // O stable (PV(j-1) done)
         tc_fence_after();
 #pragma unroll 1

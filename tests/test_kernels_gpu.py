@@ -158,3 +158,25 @@ def test_attention_fwd_bwd(cuda, T, hq, hkv, d):
     assert rel_err(dq, qf.grad) < 2e-2
     assert rel_err(dk, kf.grad) < 2e-2
     assert rel_err(dv, vf.grad) < 2e-2
+
+
+@pytest.mark.parametrize("T,hq,hkv", [(1024, 4, 1), (2048, 8, 2)])
+def test_attention_fwd_lazy_rescale_divergent_rows(cuda, T, hq, hkv):
+    """Scores whose row maxima jump by > 2^8 on later key tiles for SOME rows only: exercises the
+    forward's lazy O-rescale path with warp-divergent decisions (regression: a per-lane predicate
+    around warp-collective tcgen05.ld/st hung the kernel on real layer data)."""
+    from paper_2601_17654_b200 import ops
+    d = 128
+    torch.manual_seed(7)
+    qkv = torch.randn(T, (hq + 2 * hkv) * d, device=cuda)
+    ramp = (1.0 + torch.arange(T, device=cuda, dtype=torch.float32) / 128.0)[:, None]
+    qkv[:, hq * d:(hq + hkv) * d] *= ramp                       # keys grow with position
+    qkv[:, :hq * d] *= torch.rand(T, 1, device=cuda) * 4.0       # per-row query scale: some rows jump, some not
+    qkv = qkv.bfloat16()
+    q, k, v = qkv[:, :hq * d], qkv[:, hq * d:(hq + hkv) * d], qkv[:, (hq + hkv) * d:]
+    o = torch.empty(T, hq * d, device=cuda, dtype=torch.bfloat16)
+    lse = torch.empty(hq, T, device=cuda)
+    ops.attn_fwd(q, k, v, o, lse, T, hq, hkv, d, 1.0 / math.sqrt(d))
+    torch.cuda.synchronize()
+    ref = _attn_ref(q.float(), k.float(), v.float(), hq, hkv, d)
+    assert rel_err(o.view(T, hq, d).transpose(0, 1), ref) < 1e-2

@@ -352,7 +352,7 @@ def run_kpo(args):
                 "workload": f"{wl.model.name} layer iteration: fwd+bwd, {wl.nanobatches} nanobatches x {wl.tokens} "
                             f"tokens per rank, 8 partitions",
                 "model": wl.model.name, "global_batch": wl.tokens * wl.nanobatches * world, "seq_len": wl.tokens,
-                "parallelism": (f"fsdp{group_world}-loopback" if world == 1 else f"{wl.parallel}{world}"),
+                "parallelism": (f"{wl.parallel}{group_world}-loopback" if world == 1 else f"{wl.parallel}{world}"),
                 "schedule": f"nanobatching default: f_max, {eng.default_ncta()} comm CTAs, overlap(0,n)",
                 "l2": "no flush: per-step working set (layer weights + activations) > 126 MB L2",
                 "graphs": len(eng.exec.graphs), "graph_failures": len(eng.exec.graph_failures),
@@ -375,7 +375,7 @@ def run_kpo(args):
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_s, "unit": "s/iter", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
-            "clocks": {"sm_mhz": clocks.get("sm_mhz"), "sm_max_mhz": eng.nvml.max_sm_clock_mhz(),
+            "clocks": {"sm_mhz": clocks.get("sm_mhz") or eclocks.get("sm_mhz"), "sm_max_mhz": eng.nvml.max_sm_clock_mhz(),
                        "reasons": sorted(set(clocks.get("reasons", [])) | set(eclocks.get("reasons", []))),
                        "power_w_max": eclocks.get("power_w_max")},
         }

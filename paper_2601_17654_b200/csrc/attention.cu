@@ -15,7 +15,7 @@ int attn_fwd_tcgen05(const void* q, const void* k, const void* v, void* o, float
 int attn_bwd_tcgen05_main(const void* q, const void* k, const void* v, const void* dout, const float* lse,
                           const float* dvec, float* dq_acc, void* dk, void* dv, int64_t T, int hq, int hkv, int d,
                           int64_t qs, int64_t ks, int64_t vs, int64_t os, int64_t dks, int64_t dvs, float scale,
-                          int causal, cudaStream_t st);
+                          int causal, float* dkv_acc, cudaStream_t st);
 }
 
 namespace kpo {
@@ -530,9 +530,23 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* o
     KPO_LAUNCH_CHECK();
   }
   if (D == 128 && use_tc && T % 8 == 0) {  // tcgen05 path (bulk-copied softmax stats need 16 B rows)
+    // split-group mode when kv heads x key tiles cannot fill the GPU (e.g. TP8: one kv head per rank):
+    // one CTA per (q head, key tile), dK/dV reduced in fp32 then converted
+    const int64_t ntiles = (T + 127) / 128;
+    const bool split = hq > hkv && hkv * ntiles < num_sms();
+    float* dkv_acc = split ? dvec + (int64_t)hq * T : nullptr;
+    if (split) KPO_CUDA(cudaMemsetAsync(dkv_acc, 0, sizeof(float) * 2 * T * hkv * D, s));
     int st = attn_bwd_tcgen05_main(q, k, v, dout, lse, dvec, dq_acc, dk, dv, T, hq, hkv, D, qs, ks, vs, os, dks, dvs,
-                                   scale, causal, s);
+                                   scale, causal, dkv_acc, s);
     if (st) return st;
+    if (split) {
+      const int64_t n = T * hkv * D / 8;
+      attn_bwd_post_kernel<D><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dkv_acc, (__nv_bfloat16*)dk, (int)T, hkv, dks);
+      KPO_LAUNCH_CHECK();
+      attn_bwd_post_kernel<D><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dkv_acc + T * hkv * D, (__nv_bfloat16*)dv,
+                                                                           (int)T, hkv, dvs);
+      KPO_LAUNCH_CHECK();
+    }
   } else {
   static bool set = false;
   if (!set) {
@@ -587,8 +601,8 @@ extern "C" int kpo_attn_fwd_mma(const void* q, const void* k, const void* v, voi
 }
 
 extern "C" int64_t kpo_attn_bwd_workspace_bytes(int64_t T, int hq, int hkv, int d) {
-  (void)hkv;
-  return T * hq * d * 4 + (int64_t)hq * T * 4 + 256;
+  // dq_acc [T][hq][d] + D-vector [hq][T] + (split-group mode) dK/dV accumulators 2 x [T][hkv][d], fp32
+  return T * hq * d * 4 + (int64_t)hq * T * 4 + 2 * T * hkv * d * 4 + 256;
 }
 
 extern "C" int kpo_attn_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout,

@@ -335,7 +335,9 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
                        const __grid_constant__ CUtensorMap tmDQ,
                        const float* __restrict__ lse, const float* __restrict__ dvec, float* __restrict__ dq_acc,
                        __nv_bfloat16* __restrict__ dk, __nv_bfloat16* __restrict__ dv, int T, int hq, int hkv,
-                       int64_t dks, int64_t dvs, float scale, int causal) {
+                       int64_t dks, int64_t dvs, float scale, int causal, float* __restrict__ dkv_acc) {
+  // dkv_acc != nullptr: split-group mode — one CTA per (q head, key tile); dK / dV contributions are
+  // reduced into fp32 accumulators [T][hkv][D] (dK at dkv_acc, dV at dkv_acc + T*hkv*D).
   using C = Bwd<D>;
   constexpr int BN = C::BN, BM = C::BM, KSUB = D / 64;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -356,8 +358,10 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nblk = blockIdx.y;  // early key tiles carry the most causal work: dispatched first
-  const int kvh = blockIdx.x;
-  const int group = hq / hkv;
+  const bool split = dkv_acc != nullptr;
+  const int group = split ? 1 : hq / hkv;
+  const int h_first = split ? (int)blockIdx.x : (int)blockIdx.x * (hq / hkv);
+  const int kvh = split ? (int)blockIdx.x / (hq / hkv) : (int)blockIdx.x;
   const int n0 = nblk * BN;
   const int m_start = causal ? n0 / BM : 0;
   const int mq = (T + BM - 1) / BM - m_start;
@@ -391,7 +395,7 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
   const uint32_t sPDS = smem_u32(smem + C::OFF_PDS);  // buffer b: P^T at b*PDS_BYTES, dS^T at +PT_BYTES
 
   auto step_coords = [&](int s, int& h, int& m0) {
-    h = kvh * group + s / mq;
+    h = h_first + s / mq;
     m0 = (m_start + s % mq) * BM;
   };
 
@@ -550,7 +554,14 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
         uint32_t v[32];
         tmem_ld32_nowait(lane_addr + col + c * 32, v);
         tmem_wait_ld();
-        if (ok) {
+        if (ok && split) {
+          float* acc = dkv_acc + (which ? (int64_t)T * hkv * D : 0) + ((int64_t)key * hkv + kvh) * D + c * 32;
+#pragma unroll
+          for (int q4 = 0; q4 < 8; ++q4)
+            atomicAdd(reinterpret_cast<float4*>(acc + q4 * 4),
+                      make_float4(__uint_as_float(v[q4 * 4 + 0]) * mul, __uint_as_float(v[q4 * 4 + 1]) * mul,
+                                  __uint_as_float(v[q4 * 4 + 2]) * mul, __uint_as_float(v[q4 * 4 + 3]) * mul));
+        } else if (ok) {
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
             uint4 u;
@@ -562,7 +573,7 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
           }
         }
       }
-      if (!ok && steps == 0 && key < T) {  // no causal work: gradients are zero
+      if (!ok && !split && steps == 0 && key < T) {  // no causal work: gradients are zero
         for (int c = 0; c < D; c += 8) *reinterpret_cast<uint4*>(row + c) = make_uint4(0, 0, 0, 0);
       }
     }
@@ -613,7 +624,7 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
 template <int D>
 int bwd_launch(const void* q, const void* k, const void* v, const void* dout, const float* lse, const float* dvec,
                float* dq_acc, void* dk, void* dv, int64_t T, int hq, int hkv, int64_t qs, int64_t ks, int64_t vs,
-               int64_t os, int64_t dks, int64_t dvs, float scale, int causal, cudaStream_t st) {
+               int64_t os, int64_t dks, int64_t dvs, float scale, int causal, float* dkv_acc, cudaStream_t st) {
   using C = Bwd<D>;
   CUtensorMap mq, mk, mv, mo, mdq;
   int e;
@@ -627,9 +638,10 @@ int bwd_launch(const void* q, const void* k, const void* v, const void* dout, co
     KPO_CUDA(cudaFuncSetAttribute(attn_bwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     set = true;
   }
-  dim3 grid((unsigned)hkv, (unsigned)((T + C::BN - 1) / C::BN));
+  dim3 grid((unsigned)(dkv_acc ? hq : hkv), (unsigned)((T + C::BN - 1) / C::BN));
   attn_bwd_tc_kernel<D><<<grid, C::THREADS, C::SMEM, st>>>(mq, mk, mv, mo, mdq, lse, dvec, dq_acc, (__nv_bfloat16*)dk,
-                                                          (__nv_bfloat16*)dv, (int)T, hq, hkv, dks, dvs, scale, causal);
+                                                          (__nv_bfloat16*)dv, (int)T, hq, hkv, dks, dvs, scale, causal,
+                                                          dkv_acc);
   KPO_LAUNCH_CHECK();
   return KPO_OK;
 }
@@ -645,13 +657,13 @@ int attn_fwd_tcgen05(const void* q, const void* k, const void* v, void* o, float
 int attn_bwd_tcgen05_main(const void* q, const void* k, const void* v, const void* dout, const float* lse,
                           const float* dvec, float* dq_acc, void* dk, void* dv, int64_t T, int hq, int hkv, int d,
                           int64_t qs, int64_t ks, int64_t vs, int64_t os, int64_t dks, int64_t dvs, float scale,
-                          int causal, cudaStream_t st) {
+                          int causal, float* dkv_acc, cudaStream_t st) {
   if (d != 128) {
     set_error("attn_bwd tcgen05 path needs head_dim 128");
     return KPO_ERR_UNSUPPORTED;
   }
   return attn_tc::bwd_launch<128>(q, k, v, dout, lse, dvec, dq_acc, dk, dv, T, hq, hkv, qs, ks, vs, os, dks, dvs,
-                                  scale, causal, st);
+                                  scale, causal, dkv_acc, st);
 }
 
 }  // namespace kpo

@@ -82,124 +82,119 @@ __global__ void __launch_bounds__(256) rmsnorm_fwd_generic(const __nv_bfloat16* 
 }
 
 // ===================================================================== RMSNorm backward
-// dx_i = r*w_i*dy_i - x_i * r^3/n * sum_j(w_j*dy_j*x_j)  (+ dres_i)
-// dw_j partial per CTA: sum over the CTA's rows of dy_j*x_j*r, written as fp32 [blocks, cols].
-constexpr int kNormBwdRowsPerBlock = 16;
-constexpr int kNormBwdWarps = 8;
+// dx_i = r*w_i*dy_i - x_i * r^3/n * sum_j(w_j*dy_j*x_j)  (+ dres_i)     [rmsnorm_bwd_dx: one warp per row]
+// dw_j = sum_rows dy_j*x_j*r, as fp32 partial sums over 64-row slabs   [rmsnorm_bwd_dw: column-parallel,
+//        re-reads x / dy right after the dx kernel, while they are still resident in the 126 MB L2]
+constexpr int kNormBwdSlab = 64;
 
-__global__ void __launch_bounds__(kNormBwdWarps * 32)
-    rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
-                       const __nv_bfloat16* __restrict__ w, const float* __restrict__ rstd,
-                       const __nv_bfloat16* __restrict__ dres, __nv_bfloat16* __restrict__ dx,
-                       float* __restrict__ dw_partial, int64_t rows, int cols) {
-  extern __shared__ float dw_smem[];  // [cols] accumulated across warps
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nv = cols / 8;
-  for (int i = threadIdx.x; i < cols; i += blockDim.x) dw_smem[i] = 0.f;
-  __syncthreads();
-  const uint4* wr = reinterpret_cast<const uint4*>(w);
-  const int64_t row0 = (int64_t)blockIdx.x * kNormBwdRowsPerBlock;
-  for (int rr = warp; rr < kNormBwdRowsPerBlock; rr += kNormBwdWarps) {
-    const int64_t row = row0 + rr;
-    if (row >= rows) break;
-    const uint4* xr = reinterpret_cast<const uint4*>(x + row * cols);
-    const uint4* dyr = reinterpret_cast<const uint4*>(dy + row * cols);
-    const float r = rstd[row];
-    float dot = 0.f;
-    for (int i = lane; i < nv; i += 32) {
-      float a[8], b[8], g[8];
-      unpack8(xr[i], a);
-      unpack8(dyr[i], b);
-      unpack8(wr[i], g);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) dot += g[j] * b[j] * a[j];
-    }
-    dot = warp_sum(dot);
-    const float c = dot * r * r * r / (float)cols;
-    uint4* dxr = reinterpret_cast<uint4*>(dx + row * cols);
-    const uint4* dresr = dres ? reinterpret_cast<const uint4*>(dres + row * cols) : nullptr;
-    for (int i = lane; i < nv; i += 32) {
-      float a[8], b[8], g[8], o[8];
-      unpack8(xr[i], a);
-      unpack8(dyr[i], b);
-      unpack8(wr[i], g);
-      float res[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      if (dresr) unpack8(dresr[i], res);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        o[j] = r * g[j] * b[j] - a[j] * c + res[j];
-        atomicAdd(&dw_smem[i * 8 + j], b[j] * a[j] * r);
-      }
-      dxr[i] = pack8(o);
-    }
-  }
-  __syncthreads();
-  float* out = dw_partial + (int64_t)blockIdx.x * cols;
-  for (int i = threadIdx.x; i < cols; i += blockDim.x) out[i] = dw_smem[i];
-}
-
-// Register-accumulating variant for cols = 256*NV: lane l owns the 8-column chunks l, l+32, ...;
-// each warp walks rows with a grid-wide stride, accumulating dw in registers, and flushes once into
-// the CTA's shared row (8-way, not per-row, contention); one partial row per CTA.
 template <int NV>
-__global__ void __launch_bounds__(256, 1)
-    rmsnorm_bwd_reg(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
-                    const __nv_bfloat16* __restrict__ w, const float* __restrict__ rstd,
-                    const __nv_bfloat16* __restrict__ dres, __nv_bfloat16* __restrict__ dx,
-                    float* __restrict__ dw_partial, int64_t rows, int cols) {
-  extern __shared__ float dw_smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < cols; i += blockDim.x) dw_smem[i] = 0.f;
-  float acc[NV * 8];
-#pragma unroll
-  for (int i = 0; i < NV * 8; ++i) acc[i] = 0.f;
+__global__ void __launch_bounds__(256)
+    rmsnorm_bwd_dx_cached(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+                          const __nv_bfloat16* __restrict__ w, const float* __restrict__ rstd,
+                          const __nv_bfloat16* __restrict__ dres, __nv_bfloat16* __restrict__ dx, int64_t rows,
+                          int cols) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + row * cols);
+  const uint4* dyr = reinterpret_cast<const uint4*>(dy + row * cols);
   const uint4* wr = reinterpret_cast<const uint4*>(w);
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; row < rows; row += nwarps) {
-    const uint4* xr = reinterpret_cast<const uint4*>(x + row * cols);
-    const uint4* dyr = reinterpret_cast<const uint4*>(dy + row * cols);
-    const float r = rstd[row];
-    float dot = 0.f;
+  const float r = rstd[row];
+  uint4 xv[NV], dv[NV];
+  float dot = 0.f;
 #pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      float a[8], b[8], g[8];
-      unpack8(ld_nc_v4(xr + lane + 32 * i), a);
-      unpack8(ld_nc_v4(dyr + lane + 32 * i), b);
-      unpack8(wr[lane + 32 * i], g);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) dot += g[j] * b[j] * a[j];
-    }
-    dot = warp_sum(dot);
-    const float c = dot * r * r * r / (float)cols;
-    uint4* dxr = reinterpret_cast<uint4*>(dx + row * cols);
-    const uint4* dresr = dres ? reinterpret_cast<const uint4*>(dres + row * cols) : nullptr;
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {  // second pass re-reads x / dy from L1
-      float a[8], b[8], g[8], o[8];
-      unpack8(xr[lane + 32 * i], a);
-      unpack8(dyr[lane + 32 * i], b);
-      unpack8(wr[lane + 32 * i], g);
-      float res[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      if (dresr) unpack8(ld_nc_v4(dresr + lane + 32 * i), res);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        o[j] = r * g[j] * b[j] - a[j] * c + res[j];
-        acc[i * 8 + j] += b[j] * a[j] * r;
-      }
-      dxr[lane + 32 * i] = pack8(o);
-    }
+  for (int i = 0; i < NV; ++i) {
+    xv[i] = ld_nc_v4(xr + lane + 32 * i);
+    dv[i] = ld_nc_v4(dyr + lane + 32 * i);
   }
-  __syncthreads();
 #pragma unroll
-  for (int i = 0; i < NV; ++i)
+  for (int i = 0; i < NV; ++i) {
+    float a[8], b[8], g[8];
+    unpack8(xv[i], a);
+    unpack8(dv[i], b);
+    unpack8(wr[lane + 32 * i], g);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) atomicAdd(&dw_smem[(lane + 32 * i) * 8 + j], acc[i * 8 + j]);
-  __syncthreads();
-  float* out = dw_partial + (int64_t)blockIdx.x * cols;
-  for (int i = threadIdx.x; i < cols; i += blockDim.x) out[i] = dw_smem[i];
+    for (int j = 0; j < 8; ++j) dot += g[j] * b[j] * a[j];
+  }
+  dot = warp_sum(dot);
+  const float c = dot * r * r * r / (float)cols;
+  uint4* dxr = reinterpret_cast<uint4*>(dx + row * cols);
+  const uint4* dresr = dres ? reinterpret_cast<const uint4*>(dres + row * cols) : nullptr;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    float a[8], b[8], g[8], o[8];
+    unpack8(xv[i], a);
+    unpack8(dv[i], b);
+    unpack8(wr[lane + 32 * i], g);
+    float res[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (dresr) unpack8(ld_nc_v4(dresr + lane + 32 * i), res);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = r * g[j] * b[j] - a[j] * c + res[j];
+    dxr[lane + 32 * i] = pack8(o);
+  }
 }
 
-static bool norm_bwd_reg_ok(int64_t cols) { return cols % 256 == 0 && cols / 256 >= 1 && cols / 256 <= 16; }
+__global__ void __launch_bounds__(256)
+    rmsnorm_bwd_dx_generic(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+                           const __nv_bfloat16* __restrict__ w, const float* __restrict__ rstd,
+                           const __nv_bfloat16* __restrict__ dres, __nv_bfloat16* __restrict__ dx, int64_t rows,
+                           int cols) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int nv = cols / 8;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + row * cols);
+  const uint4* dyr = reinterpret_cast<const uint4*>(dy + row * cols);
+  const uint4* wr = reinterpret_cast<const uint4*>(w);
+  const float r = rstd[row];
+  float dot = 0.f;
+  for (int i = lane; i < nv; i += 32) {
+    float a[8], b[8], g[8];
+    unpack8(xr[i], a);
+    unpack8(dyr[i], b);
+    unpack8(wr[i], g);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) dot += g[j] * b[j] * a[j];
+  }
+  dot = warp_sum(dot);
+  const float c = dot * r * r * r / (float)cols;
+  uint4* dxr = reinterpret_cast<uint4*>(dx + row * cols);
+  const uint4* dresr = dres ? reinterpret_cast<const uint4*>(dres + row * cols) : nullptr;
+  for (int i = lane; i < nv; i += 32) {
+    float a[8], b[8], g[8], o[8];
+    unpack8(xr[i], a);
+    unpack8(dyr[i], b);
+    unpack8(wr[i], g);
+    float res[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (dresr) unpack8(dresr[i], res);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = r * g[j] * b[j] - a[j] * c + res[j];
+    dxr[i] = pack8(o);
+  }
+}
+
+// one thread per 8-column chunk, a 64-row slab per blockIdx.y; coalesced 16-byte loads along rows
+__global__ void __launch_bounds__(128)
+    rmsnorm_bwd_dw(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+                   const float* __restrict__ rstd, float* __restrict__ dw_partial, int64_t rows, int cols) {
+  const int chunk = blockIdx.x * blockDim.x + threadIdx.x;
+  if (chunk * 8 >= cols) return;
+  const int64_t r0 = (int64_t)blockIdx.y * kNormBwdSlab;
+  const int64_t r1 = r0 + kNormBwdSlab < rows ? r0 + kNormBwdSlab : rows;
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll 4
+  for (int64_t row = r0; row < r1; ++row) {
+    float a[8], b[8];
+    unpack8(*reinterpret_cast<const uint4*>(x + row * cols + chunk * 8), a);
+    unpack8(*reinterpret_cast<const uint4*>(dy + row * cols + chunk * 8), b);
+    const float rr = rstd[row];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] += b[j] * a[j] * rr;
+  }
+  float4* out = reinterpret_cast<float4*>(dw_partial + (int64_t)blockIdx.y * cols + chunk * 8);
+  out[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+  out[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+}
 
 // out[c] = sum_r in[r, c]; one thread per column, coalesced across the warp.
 __global__ void colsum_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
@@ -336,15 +331,10 @@ extern "C" int kpo_rmsnorm_fwd(const void* x, const void* w, void* y, float* rst
   return KPO_OK;
 }
 
-static int64_t norm_bwd_reg_grid(int64_t rows) {
-  const int64_t want = (rows + 7) / 8;
-  const int64_t sms = num_sms();
-  return want < sms ? (want > 0 ? want : 1) : sms;
-}
-
 extern "C" int kpo_rmsnorm_bwd_partial_rows(int64_t rows, int64_t cols, int64_t* n_partials) {
   KPO_CHECK_ARG(n_partials, "null n_partials");
-  *n_partials = norm_bwd_reg_ok(cols) ? norm_bwd_reg_grid(rows) : (rows + kNormBwdRowsPerBlock - 1) / kNormBwdRowsPerBlock;
+  (void)cols;
+  *n_partials = (rows + kNormBwdSlab - 1) / kNormBwdSlab;
   return KPO_OK;
 }
 
@@ -352,38 +342,32 @@ extern "C" int kpo_rmsnorm_bwd(const void* dy, const void* x, const void* w, con
                                const void* dres, void* dx, float* dw_partial, int64_t rows, int64_t cols,
                                void* stream) {
   KPO_CHECK_ARG(dy && x && w && rstd && dx && dw_partial, "rmsnorm_bwd: null pointer");
-  KPO_CHECK_ARG(cols > 0 && cols % 8 == 0 && cols * 4 <= 200 * 1024, "rmsnorm_bwd: bad cols");
+  KPO_CHECK_ARG(cols > 0 && cols % 8 == 0, "rmsnorm_bwd: cols must be a positive multiple of 8");
+  KPO_CHECK_ARG(aligned16(dy) && aligned16(x) && aligned16(w) && aligned16(dx) && (!dres || aligned16(dres)),
+                "rmsnorm_bwd: pointers must be 16B aligned");
   if (rows == 0) return KPO_OK;
-  const size_t smem = (size_t)cols * sizeof(float);
-  if (norm_bwd_reg_ok(cols)) {
-    const unsigned grid = (unsigned)norm_bwd_reg_grid(rows);
-    cudaStream_t st = (cudaStream_t)stream;
-    auto Dy = (const __nv_bfloat16*)dy;
-    auto X = (const __nv_bfloat16*)x;
-    auto W = (const __nv_bfloat16*)w;
-    auto Dr = (const __nv_bfloat16*)dres;
-    auto Dx = (__nv_bfloat16*)dx;
+  cudaStream_t st = (cudaStream_t)stream;
+  auto Dy = (const __nv_bfloat16*)dy;
+  auto X = (const __nv_bfloat16*)x;
+  auto W = (const __nv_bfloat16*)w;
+  auto Dr = (const __nv_bfloat16*)dres;
+  auto Dx = (__nv_bfloat16*)dx;
+  const dim3 grid((unsigned)((rows + 7) / 8)), block(256);
+  if (cols % 256 == 0 && cols / 256 <= 16) {
     switch (cols / 256) {
-#define KPO_NB_CASE(n)                                                                                    \
-  case n:                                                                                                 \
-    if (smem > 48 * 1024)                                                                                 \
-      KPO_CUDA(cudaFuncSetAttribute(rmsnorm_bwd_reg<n>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    rmsnorm_bwd_reg<n><<<grid, 256, smem, st>>>(Dy, X, W, rstd, Dr, Dx, dw_partial, rows, (int)cols);       \
-    break;
-      KPO_NB_CASE(1) KPO_NB_CASE(2) KPO_NB_CASE(3) KPO_NB_CASE(4) KPO_NB_CASE(5) KPO_NB_CASE(6) KPO_NB_CASE(7)
-      KPO_NB_CASE(8) KPO_NB_CASE(9) KPO_NB_CASE(10) KPO_NB_CASE(11) KPO_NB_CASE(12) KPO_NB_CASE(13)
-      KPO_NB_CASE(14) KPO_NB_CASE(15) KPO_NB_CASE(16)
+#define KPO_NB_CASE(n) \
+  case n: rmsnorm_bwd_dx_cached<n><<<grid, block, 0, st>>>(Dy, X, W, rstd, Dr, Dx, rows, (int)cols); break;
+      KPO_NB_CASE(1) KPO_NB_CASE(2) KPO_NB_CASE(3) KPO_NB_CASE(4) KPO_NB_CASE(5) KPO_NB_CASE(6) KPO_NB_CASE(8)
+      KPO_NB_CASE(10) KPO_NB_CASE(12) KPO_NB_CASE(16)
 #undef KPO_NB_CASE
+      default: rmsnorm_bwd_dx_generic<<<grid, block, 0, st>>>(Dy, X, W, rstd, Dr, Dx, rows, (int)cols);
     }
-    KPO_LAUNCH_CHECK();
-    return KPO_OK;
+  } else {
+    rmsnorm_bwd_dx_generic<<<grid, block, 0, st>>>(Dy, X, W, rstd, Dr, Dx, rows, (int)cols);
   }
-  const unsigned blocks = (unsigned)((rows + kNormBwdRowsPerBlock - 1) / kNormBwdRowsPerBlock);
-  if (smem > 48 * 1024)
-    KPO_CUDA(cudaFuncSetAttribute(rmsnorm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  rmsnorm_bwd_kernel<<<blocks, kNormBwdWarps * 32, smem, (cudaStream_t)stream>>>(
-      (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const __nv_bfloat16*)w, rstd,
-      (const __nv_bfloat16*)dres, (__nv_bfloat16*)dx, dw_partial, rows, (int)cols);
+  KPO_LAUNCH_CHECK();
+  const dim3 g2((unsigned)((cols / 8 + 127) / 128), (unsigned)((rows + kNormBwdSlab - 1) / kNormBwdSlab));
+  rmsnorm_bwd_dw<<<g2, 128, 0, st>>>(Dy, X, rstd, dw_partial, rows, (int)cols);
   KPO_LAUNCH_CHECK();
   return KPO_OK;
 }

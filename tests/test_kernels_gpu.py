@@ -134,7 +134,8 @@ def _attn_ref(q, k, v, hq, hkv, d, causal=True):
     return torch.nn.functional.scaled_dot_product_attention(qf, kf, vf, is_causal=causal)
 
 
-@pytest.mark.parametrize("T,hq,hkv,d", [(256, 4, 1, 128), (1000, 6, 2, 128), (512, 8, 8, 64), (4096, 3, 1, 128)])
+@pytest.mark.parametrize("T,hq,hkv,d", [(256, 4, 1, 128), (1000, 6, 2, 128), (512, 8, 8, 64), (4096, 3, 1, 128),
+                                      (4096, 24, 8, 128)])
 def test_attention_fwd_bwd(cuda, T, hq, hkv, d):
     from paper_2601_17654_b200 import ops
     torch.manual_seed(T + hq)

@@ -12,12 +12,22 @@ def timeit(fn, reps=20, warm=3):
     e1.record(); torch.cuda.synchronize()
     return e0.elapsed_time(e1) / reps
 
-T, h, f, qkv = 4096, 3072, 8192, 5120
+import argparse
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=1)
+args = ap.parse_args()
+T = 4096
+if args.config == 1:
+    h, f, qkv, hd = 3072, 8192, 5120, 3072
+elif args.config == 2:  # Llama-3-8B TP8, per rank
+    h, f, qkv, hd = 4096, 1792, 768, 512
+else:  # Llama-3-70B FSDP8
+    h, f, qkv, hd = 8192, 28672, 10240, 8192
 shapes = [  # name, M, N, K, a_mn, b_mn
-    ("linear_qkv", T, qkv, h, 0, 0), ("linear_proj", T, h, h, 0, 0), ("linear_up", T, 2 * f, h, 0, 0),
+    ("linear_qkv", T, qkv, h, 0, 0), ("linear_proj", T, h, hd, 0, 0), ("linear_up", T, 2 * f, h, 0, 0),
     ("linear_down", T, h, f, 0, 0), ("down_dgrad", T, f, h, 0, 1), ("down_wgrad", h, f, T, 1, 1),
-    ("gu_dgrad", T, h, 2 * f, 0, 1), ("gu_wgrad", 2 * f, h, T, 1, 1), ("o_dgrad", T, h, h, 0, 1),
-    ("o_wgrad", h, h, T, 1, 1), ("qkv_dgrad", T, h, qkv, 0, 1), ("qkv_wgrad", qkv, h, T, 1, 1)]
+    ("gu_dgrad", T, h, 2 * f, 0, 1), ("gu_wgrad", 2 * f, h, T, 1, 1), ("o_dgrad", T, hd, h, 0, 1),
+    ("o_wgrad", h, hd, T, 1, 1), ("qkv_dgrad", T, h, qkv, 0, 1), ("qkv_wgrad", qkv, h, T, 1, 1)]
 out = {}
 tot_k = tot_c = 0.0
 for name, M, N, K, amn, bmn in shapes:

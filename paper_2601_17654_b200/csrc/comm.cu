@@ -385,8 +385,16 @@ static int launch_comm(kpo_comm* c, void (*kernel)(KArgs...), int ncta, cudaStre
   cfg.blockDim = dim3(kCommThreads);
   cfg.dynamicSmemBytes = (size_t)c->smem_bytes;  // full-SM reservation: owns ncta SMs
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   int na = 0;
+  if (ncta % 2 == 0) {
+    // pack the collective's CTAs two per TPC so whole TPCs stay free for the CTA-pair GEMM
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
   if (c->launch_evt) {
     attr[na].id = cudaLaunchAttributeLaunchCompletionEvent;
     attr[na].val.launchCompletionEvent.event = c->launch_evt;

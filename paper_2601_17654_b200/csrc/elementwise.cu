@@ -83,9 +83,9 @@ __global__ void __launch_bounds__(256) rmsnorm_fwd_generic(const __nv_bfloat16* 
 
 // ===================================================================== RMSNorm backward
 // dx_i = r*w_i*dy_i - x_i * r^3/n * sum_j(w_j*dy_j*x_j)  (+ dres_i)     [rmsnorm_bwd_dx: one warp per row]
-// dw_j = sum_rows dy_j*x_j*r, as fp32 partial sums over 64-row slabs   [rmsnorm_bwd_dw: column-parallel,
+// dw_j = sum_rows dy_j*x_j*r, as fp32 partial sums over 16-row slabs   [rmsnorm_bwd_dw: column-parallel,
 //        re-reads x / dy right after the dx kernel, while they are still resident in the 126 MB L2]
-constexpr int kNormBwdSlab = 64;
+constexpr int kNormBwdSlab = 16;
 
 template <int NV>
 __global__ void __launch_bounds__(256)

@@ -61,3 +61,19 @@ res["gemm_4096x16384x3072"] = {"ms": t, "tflops": 2 * T * 16384 * 3072 / t / 1e9
 t = timeit(lambda: torch.matmul(x, w.t(), out=y))
 res["cublas_4096x16384x3072"] = {"ms": t, "tflops": 2 * T * 16384 * 3072 / t / 1e9}
 print(json.dumps(res, indent=1))
+
+# ---- memory-bound kernels standalone (config-2 shapes), GB/s of algorithmic bytes
+h, f = 3072, 8192
+x = torch.randn(T, h, device="cuda").bfloat16(); w = torch.ones(h, device="cuda").bfloat16()
+y = torch.empty_like(x); rstd = torch.empty(T, device="cuda"); dy = torch.randn_like(x); dres = torch.randn_like(x)
+dx = torch.empty_like(x); parts = torch.empty(ops.rmsnorm_partials(T, h), h, device="cuda")
+mem = {}
+t = timeit(lambda: ops.rmsnorm_fwd(x, w, y, rstd)); mem["rmsnorm_fwd"] = (t, 2 * T * h * 2)
+t = timeit(lambda: ops.rmsnorm_bwd(dy, x, w, rstd, dx, parts, dres=dres)); mem["rmsnorm_bwd"] = (t, 4 * T * h * 2)
+gu = torch.randn(T, 2 * f, device="cuda").bfloat16(); act = torch.empty(T, f, device="cuda", dtype=torch.bfloat16)
+t = timeit(lambda: ops.swiglu_fwd(gu, act)); mem["swiglu_fwd"] = (t, 3 * T * f * 2)
+dgu = torch.empty_like(gu)
+t = timeit(lambda: ops.swiglu_bwd(act, gu, dgu)); mem["swiglu_bwd"] = (t, 5 * T * f * 2)
+qkr = torch.empty(T, (hq + hkv) * d, device="cuda", dtype=torch.bfloat16)
+t = timeit(lambda: ops.rope(qkv, qkr, hq + hkv, d, 500000.0)); mem["rope"] = (t, 2 * T * (hq + hkv) * d * 2)
+print(json.dumps({k: {"ms": round(v[0], 4), "GB/s": round(v[1] / v[0] / 1e6, 1)} for k, v in mem.items()}, indent=1))

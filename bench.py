@@ -139,10 +139,19 @@ def run_kpo(args):
     from paper_2601_17654_b200.runner import LayerRunner, sequential_schedule
 
     rank, world, local = dist_env()
+    # KPO_SAME_DEVICE=1 (test only): every rank on cuda:0, gloo plumbing — exercises the N>1 path
+    # (IPC peer mapping, cross-rank barriers, max/sum reductions) on a single-GPU box.
+    same_dev = os.environ.get("KPO_SAME_DEVICE") == "1"
+    if same_dev:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if same_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    red_dev = torch.device("cpu") if same_dev else dev
     group_world = world if world > 1 else 8
     wl = baseline_workload(args.config, world=group_world, tokens=args.tokens)
     peaks = load_measured_peaks()
@@ -172,14 +181,14 @@ def run_kpo(args):
     def max_over_ranks(v: float) -> float:
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        t = torch.tensor([v], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t)
 
     def sum_over_ranks(v: float) -> float:
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        t = torch.tensor([v], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t)
 

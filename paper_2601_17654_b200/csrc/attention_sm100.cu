@@ -44,7 +44,7 @@ __device__ __forceinline__ uint32_t sw128(int r, int chunk) {
   return (uint32_t)(r * 128 + ((chunk ^ (r & 7)) << 4));
 }
 
-template <int D>
+template <int D, int POLY_MASK>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                        const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ o, float* __restrict__ lse,
@@ -217,7 +217,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         float p[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          p[e] = ex2(fmaf(sv[ch * 8 + e], scale_log2, neg_m));
+          const float xe = fmaf(sv[ch * 8 + e], scale_log2, neg_m);
+          p[e] = ((POLY_MASK >> e) & 1) ? ex2_poly(xe) : ex2(xe);
           ps[e] += p[e];
         }
         uint4 u;
@@ -276,14 +277,20 @@ int fwd_launch(const void* q, const void* k, const void* v, void* o, float* lse,
   if ((e = make_map_2d(&mq, q, (uint64_t)hq * D, T, qs, 64, C::BM))) return e;
   if ((e = make_map_2d(&mk, k, (uint64_t)hkv * D, T, ks, 64, C::BN))) return e;
   if ((e = make_map_2d(&mv, v, (uint64_t)hkv * D, T, vs, 64, C::BN))) return e;
-  static bool set = false;
-  if (!set) {
-    KPO_CUDA(cudaFuncSetAttribute(attn_fwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    set = true;
-  }
+  // POLY_MASK: which of every 8 exponentials run on the FMA pipe (ex2_poly) instead of MUFU.EX2
+  static const int mode = getenv("KPO_EXP2_POLY") ? atoi(getenv("KPO_EXP2_POLY")) : 0;  // measured: MUFU-only fastest
   dim3 grid((unsigned)hq, (unsigned)((T + C::BM - 1) / C::BM));
-  attn_fwd_tc_kernel<D><<<grid, kThreads, C::SMEM, st>>>(mq, mk, mv, (__nv_bfloat16*)o, lse, (int)T, hq, hkv, os,
-                                                         scale * kLog2e, causal);
+  auto go = [&](auto kern) -> int {
+    KPO_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    kern<<<grid, kThreads, C::SMEM, st>>>(mq, mk, mv, (__nv_bfloat16*)o, lse, (int)T, hq, hkv, os, scale * kLog2e,
+                                         causal);
+    return KPO_OK;
+  };
+  int rc;
+  if (mode == 0) rc = go(attn_fwd_tc_kernel<D, 0x00>);
+  else if (mode == 2) rc = go(attn_fwd_tc_kernel<D, 0x55>);
+  else rc = go(attn_fwd_tc_kernel<D, 0x88>);
+  if (rc) return rc;
   KPO_LAUNCH_CHECK();
   return KPO_OK;
 }

@@ -60,9 +60,10 @@ __global__ void __launch_bounds__(256) rmsnorm_fwd_generic(const __nv_bfloat16* 
   const uint4* xr = reinterpret_cast<const uint4*>(x + row * cols);
   const int nv = cols / 8;
   float ss = 0.f;
+#pragma unroll 4
   for (int i = lane; i < nv; i += 32) {
     float f[8];
-    unpack8(xr[i], f);
+    unpack8(ld_nc_v4(xr + i), f);
 #pragma unroll
     for (int j = 0; j < 8; ++j) ss += f[j] * f[j];
   }
@@ -71,6 +72,7 @@ __global__ void __launch_bounds__(256) rmsnorm_fwd_generic(const __nv_bfloat16* 
   if (lane == 0 && rstd) rstd[row] = r;
   const uint4* wr = reinterpret_cast<const uint4*>(w);
   uint4* yr = reinterpret_cast<uint4*>(y + row * cols);
+#pragma unroll 4
   for (int i = lane; i < nv; i += 32) {
     float f[8], g[8];
     unpack8(xr[i], f);
@@ -148,10 +150,11 @@ __global__ void __launch_bounds__(256)
   const uint4* wr = reinterpret_cast<const uint4*>(w);
   const float r = rstd[row];
   float dot = 0.f;
+#pragma unroll 4
   for (int i = lane; i < nv; i += 32) {
     float a[8], b[8], g[8];
-    unpack8(xr[i], a);
-    unpack8(dyr[i], b);
+    unpack8(ld_nc_v4(xr + i), a);
+    unpack8(ld_nc_v4(dyr + i), b);
     unpack8(wr[i], g);
 #pragma unroll
     for (int j = 0; j < 8; ++j) dot += g[j] * b[j] * a[j];
@@ -160,6 +163,7 @@ __global__ void __launch_bounds__(256)
   const float c = dot * r * r * r / (float)cols;
   uint4* dxr = reinterpret_cast<uint4*>(dx + row * cols);
   const uint4* dresr = dres ? reinterpret_cast<const uint4*>(dres + row * cols) : nullptr;
+#pragma unroll 4
   for (int i = lane; i < nv; i += 32) {
     float a[8], b[8], g[8], o[8];
     unpack8(xr[i], a);
@@ -353,12 +357,11 @@ extern "C" int kpo_rmsnorm_bwd(const void* dy, const void* x, const void* w, con
   auto Dr = (const __nv_bfloat16*)dres;
   auto Dx = (__nv_bfloat16*)dx;
   const dim3 grid((unsigned)((rows + 7) / 8)), block(256);
-  if (cols % 256 == 0 && cols / 256 <= 16) {
+  if (cols % 256 == 0 && cols / 256 <= 4) {  // small rows: cache in registers; large rows: two-pass re-read
     switch (cols / 256) {
 #define KPO_NB_CASE(n) \
   case n: rmsnorm_bwd_dx_cached<n><<<grid, block, 0, st>>>(Dy, X, W, rstd, Dr, Dx, rows, (int)cols); break;
-      KPO_NB_CASE(1) KPO_NB_CASE(2) KPO_NB_CASE(3) KPO_NB_CASE(4) KPO_NB_CASE(5) KPO_NB_CASE(6) KPO_NB_CASE(8)
-      KPO_NB_CASE(10) KPO_NB_CASE(12) KPO_NB_CASE(16)
+      KPO_NB_CASE(1) KPO_NB_CASE(2) KPO_NB_CASE(3) KPO_NB_CASE(4)
 #undef KPO_NB_CASE
       default: rmsnorm_bwd_dx_generic<<<grid, block, 0, st>>>(Dy, X, W, rstd, Dr, Dx, rows, (int)cols);
     }

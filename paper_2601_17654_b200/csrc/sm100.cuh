@@ -122,6 +122,16 @@ __device__ __forceinline__ float ex2(float x) {
   asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x on the FMA pipe (Cody-Waite split + degree-3 polynomial, max rel. error 8.6e-5 on [0,1)),
+// used for a fraction of the softmax exponentials so the MUFU unit is not the only exp2 engine.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float fi = floorf(x);
+  const float f = x - fi;
+  const float p = fmaf(fmaf(fmaf(0.07707918f, f, 0.22763424f), f, 0.69511687f), f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (static_cast<int>(fi) << 23));
+}
+
 // UMMA instruction descriptor: bf16 x bf16 -> f32, M x N, operand majorness.
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool b_mn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |

@@ -309,7 +309,8 @@ int fwd_launch(const void* q, const void* k, const void* v, void* o, float* lse,
 //   dQ^T = K^T dS^T     M=d=128,   N=64 q, K=128 keys (A = the K tile read MN-major, B = dS^T MN-major)
 //   dQ drain warps: dQ^T (lane = head-dim index) -> fp32 [q][d] smem tile -> one TMA bulk
 //   reduce-add (cp.reduce.async.bulk.tensor .add) into dq_acc[t][h][d].
-// TMEM columns: S^T 0..63, dP^T 64..127, dQ^T 128..255 (2 buffers), dV 256..383, dK 384..511.
+// TMEM columns: S^T 0..63, dP^T 64..127, dQ^T 128..191, P^T (2 x 32 cols of bf16 pairs, the A operand
+// of the dV MMA read straight from TMEM) 192..255, dV 256..383, dK 384..511.
 // Issue order: S/dP(s+1) as soon as the softmax warps have pulled S/dP(s) out of TMEM, then the
 // gradient MMAs of step s; P^T/dS^T (smem) and dQ^T (TMEM) are double-buffered so the softmax of
 // step s+1 and the dQ drain of step s overlap the tensor core.
@@ -318,17 +319,16 @@ struct Bwd {
   static constexpr int BN = 128, BM = 64, QSTAGES = 3;
   static constexpr int KV_BYTES = BN * D * 2;
   static constexpr int QT_BYTES = BM * D * 2;
-  static constexpr int PT_BYTES = BN * BM * 2;
-  // P^T | dS^T pair per buffer (2 buffers); once the step's MMAs are done the 32 KB pair doubles as
-  // the fp32 [64 q][D] dQ staging tile of the TMA reduce-add.
-  static constexpr int PDS_BYTES = 2 * PT_BYTES;
-  static_assert(PDS_BYTES >= BM * D * 4, "dQ staging must fit in a P/dS buffer pair");
+  static constexpr int PT_BYTES = BN * BM * 2;   // one dS^T buffer [128 keys][64 q] bf16
   static constexpr int OFF_K = 0, OFF_V = OFF_K + KV_BYTES, OFF_Q = OFF_V + KV_BYTES;
-  static constexpr int OFF_DO = OFF_Q + QSTAGES * QT_BYTES, OFF_PDS = OFF_DO + QSTAGES * QT_BYTES;
-  static constexpr int OFF_STAT = OFF_PDS + 2 * PDS_BYTES;
+  static constexpr int OFF_DO = OFF_Q + QSTAGES * QT_BYTES, OFF_DS = OFF_DO + QSTAGES * QT_BYTES;
+  static constexpr int OFF_DQ = OFF_DS + 2 * PT_BYTES;           // fp32 [64 q][D] staging for the TMA reduce-add
+  static constexpr int OFF_STAT = OFF_DQ + BM * D * 4;
   static constexpr int OFF_BAR = OFF_STAT + QSTAGES * 2 * BM * 4;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
-  static constexpr int COL_S = 0, COL_DP = 64, COL_DQ = 128, COL_DV = 256, COL_DK = 384;  // dQ^T: 128 + 64*b
+  // TMEM: S^T 0..63, dP^T 64..127, dQ^T 128..191, P^T (bf16 pairs, 2 buffers x 32 cols) 192..255,
+  //       dV 256..383, dK 384..511
+  static constexpr int COL_S = 0, COL_DP = 64, COL_DQ = 128, COL_PT = 192, COL_DV = 256, COL_DK = 384;
   static constexpr int THREADS = 448;  // TMA, MMA, 8 softmax warps (2 per lane quarter), 4 dQ-drain warps
   static constexpr int SM_WARPS = 8;
 };
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
     mbar_init(smem_u32(s_empty), C::SM_WARPS);
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&pds_full[i]), C::SM_WARPS);
-      mbar_init(smem_u32(&pds_empty[i]), 2);
+      mbar_init(smem_u32(&pds_empty[i]), 1);
       mbar_init(smem_u32(&dq_full[i]), 1);
       mbar_init(smem_u32(&dq_empty[i]), 4);
     }
@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t sK = smem_u32(smem + C::OFF_K), sV = smem_u32(smem + C::OFF_V);
   const uint32_t sQ = smem_u32(smem + C::OFF_Q), sDO = smem_u32(smem + C::OFF_DO);
-  const uint32_t sPDS = smem_u32(smem + C::OFF_PDS);  // buffer b: P^T at b*PDS_BYTES, dS^T at +PT_BYTES
+  const uint32_t sDS = smem_u32(smem + C::OFF_DS);  // dS^T buffer b at b*PT_BYTES
 
   auto step_coords = [&](int s, int& h, int& m0) {
     h = h_first + s / mq;
@@ -440,29 +440,30 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
       constexpr uint32_t ID_G = idesc_bf16(BN, D, false, true);     // dV, dK
       constexpr uint32_t ID_Q = idesc_bf16(D, BM, true, true);      // dQ^T
       mbar_wait(smem_u32(kv_full), 0);
+      constexpr uint32_t ID_GT = idesc_bf16(BN, D, false, true);   // dV with A = P^T from TMEM
       auto grads = [&](int j) {
-        const int st = j & 1;          // P/dS and dQ^T buffer
+        const int st = j & 1;          // P^T / dS^T buffer
         const int qs = j % C::QSTAGES;  // Q/dO stage
         mbar_wait(smem_u32(&pds_full[st]), (j >> 1) & 1);
         tc_fence_after();
         const uint32_t qb = sQ + qs * C::QT_BYTES, ob = sDO + qs * C::QT_BYTES;
-        const uint32_t pb = sPDS + st * C::PDS_BYTES, db = pb + C::PT_BYTES;
+        const uint32_t db = sDS + st * C::PT_BYTES;
 #pragma unroll
         for (int k = 0; k < BM / 16; ++k) {
           const uint32_t acc = (j > 0 || k > 0) ? 1u : 0u;
-          tc_mma(tmem + C::COL_DV, smem_desc(pb + k * 32, 16, 1024), smem_desc(ob + k * 2048, BM * 128, 1024), ID_G,
-                 acc);
+          tc_mma_ts(tmem + C::COL_DV, tmem + C::COL_PT + st * 32 + k * 8, smem_desc(ob + k * 2048, BM * 128, 1024),
+                    ID_GT, acc);
           tc_mma(tmem + C::COL_DK, smem_desc(db + k * 32, 16, 1024), smem_desc(qb + k * 2048, BM * 128, 1024), ID_G,
                  acc);
         }
-        mbar_wait(smem_u32(&dq_empty[st]), ((j >> 1) & 1) ^ 1);
+        mbar_wait(smem_u32(&dq_empty[0]), (j & 1) ^ 1);
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < BN / 16; ++k) {
-          tc_mma(tmem + C::COL_DQ + st * BM, smem_desc(sK + k * 2048, BN * 128, 1024),
+          tc_mma(tmem + C::COL_DQ, smem_desc(sK + k * 2048, BN * 128, 1024),
                  smem_desc(db + k * 2048, BM * 128, 1024), ID_Q, k > 0 ? 1u : 0u);
         }
-        tc_commit(smem_u32(&dq_full[st]));
+        tc_commit(smem_u32(&dq_full[0]));
         tc_commit(smem_u32(&pds_empty[st]));
         tc_commit(smem_u32(&qd_empty[qs]));
       };
@@ -520,7 +521,8 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
       if (lane == 0) mbar_arrive(smem_u32(s_empty));
       mbar_wait(smem_u32(&pds_empty[buf]), ((s >> 1) & 1) ^ 1);  // grads(s-2) done with this buffer
       const bool mask = (causal && m0 < n0 + BN - 1) || key >= T || m0 + BM > T;
-      const uint32_t pb = sPDS + buf * C::PDS_BYTES, db = pb + C::PT_BYTES;
+      const uint32_t db = sDS + buf * C::PT_BYTES;
+      uint32_t pp[HC / 2];
 #pragma unroll
       for (int ch = 0; ch < HC / 8; ++ch) {
         float p[8], ds[8];
@@ -533,14 +535,17 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
           p[e] = pe;
           ds[e] = de;
         }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) pp[ch * 4 + e] = pack_bf16x2(p[2 * e], p[2 * e + 1]);
         const uint32_t off = sw128(r, half * (HC / 8) + ch);
-        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(pb + off), "r"(pack_bf16x2(p[0], p[1])),
-                     "r"(pack_bf16x2(p[2], p[3])), "r"(pack_bf16x2(p[4], p[5])), "r"(pack_bf16x2(p[6], p[7]))
-                     : "memory");
         asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(db + off), "r"(pack_bf16x2(ds[0], ds[1])),
                      "r"(pack_bf16x2(ds[2], ds[3])), "r"(pack_bf16x2(ds[4], ds[5])), "r"(pack_bf16x2(ds[6], ds[7]))
                      : "memory");
       }
+      // P^T row (this warp's 32 queries = 16 packed columns) -> TMEM, the A operand of the dV MMA
+      tmem_st16(lane_addr + C::COL_PT + buf * 32 + half * (HC / 2), pp);
+      tmem_wait_st();
+      tc_fence_before();
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&pds_full[buf]));
@@ -595,20 +600,20 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
     for (int s = 0; s < steps; ++s) {
       int h, m0;
       step_coords(s, h, m0);
-      const int buf = s & 1;
-      mbar_wait(smem_u32(&dq_full[buf]), (s >> 1) & 1);
+      mbar_wait(smem_u32(&dq_full[0]), s & 1);
       tc_fence_after();
       float v[BM];
 #pragma unroll
       for (int c = 0; c < BM / 32; ++c)
-        tmem_ld32_nowait(lane_addr + C::COL_DQ + buf * BM + c * 32, reinterpret_cast<uint32_t*>(v + c * 32));
+        tmem_ld32_nowait(lane_addr + C::COL_DQ + c * 32, reinterpret_cast<uint32_t*>(v + c * 32));
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&dq_empty[buf]));
-      // stage dQ (fp32 [64 q][D]) in this step's P/dS buffer pair: every MMA that read it has completed
-      // (dq_full is committed after them); the softmax waits for our arrival before reusing it.
-      float* stg = reinterpret_cast<float*>(smem + C::OFF_PDS + buf * C::PDS_BYTES);
+      if (lane == 0) mbar_arrive(smem_u32(&dq_empty[0]));
+      // own fp32 staging tile: wait until the previous TMA reduce has read it
+      if (dtid == 0) bulk_wait_read0();
+      named_bar(2, 128);
+      float* stg = reinterpret_cast<float*>(smem + C::OFF_DQ);
 #pragma unroll
       for (int qi = 0; qi < BM; ++qi) stg[qi * D + dcol] = v[qi] * scale;
       fence_async_smem();
@@ -616,8 +621,6 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
       if (dtid == 0) {
         tma_reduce_add_2d(&tmDQ, smem_u32(stg), h * D, m0);
         bulk_commit();
-        bulk_wait_read0();
-        mbar_arrive(smem_u32(&pds_empty[buf]));
       }
     }
     if (dtid == 0) bulk_wait0();

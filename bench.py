@@ -223,7 +223,20 @@ def run_kpo(args):
     for _ in range(n_e2e):
         run.step_host(xs, dys, dxs)
     h1 = time.perf_counter()
-    e2e_s = max_over_ranks((h1 - h0) / n_e2e)
+    e2e_sync_s = max_over_ranks((h1 - h0) / n_e2e)
+    # pipelined: H2D of step k+1 and D2H of step k-1 overlap step k on copy-engine streams; every
+    # step's copies are still inside the timed region (first H2D .. last D2H)
+    for _ in range(2):
+        run.step_host_async(xs, dys, dxs)
+    run.drain()
+    n_pipe = max(6, args.steps)
+    barrier()
+    h0 = time.perf_counter()
+    for _ in range(n_pipe):
+        run.step_host_async(xs, dys, dxs)
+    run.drain()
+    h1 = time.perf_counter()
+    e2e_s = max_over_ranks((h1 - h0) / n_pipe)
     h2d = sum(t.numel() * t.element_size() for t in xs + dys)
     d2h = sum(t.numel() * t.element_size() for t in dxs)
 
@@ -382,7 +395,10 @@ def run_kpo(args):
             "comm": {"mode": "loopback (HBM)" if world == 1 else "cuda-ipc p2p (NVLink)", "units": comm_rows},
             "frontier": frontier,
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_s, "unit": "s/iter", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "e2e": {"value": e2e_s, "unit": "s/iter", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "api": "LayerRunner.step_host_async x K + drain(): pinned host x/dy in, dx out, copies "
+                           "pipelined on copy-engine streams (wall clock, max over ranks)",
+                    "unpipelined_value": e2e_sync_s},
             "gpu_launches": launches,
             "clocks": {"sm_mhz": clocks.get("sm_mhz") or eclocks.get("sm_mhz"), "sm_max_mhz": eng.nvml.max_sm_clock_mhz(),
                        "reasons": sorted(set(clocks.get("reasons", [])) | set(eclocks.get("reasons", []))),

@@ -342,7 +342,10 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
                        const __grid_constant__ CUtensorMap tmDQ,
                        const float* __restrict__ lse, const float* __restrict__ dvec, float* __restrict__ dq_acc,
                        __nv_bfloat16* __restrict__ dk, __nv_bfloat16* __restrict__ dv, int T, int hq, int hkv,
-                       int64_t dks, int64_t dvs, float scale, int causal, float* __restrict__ dkv_acc) {
+                       int64_t dks, int64_t dvs, float scale, int causal, float* __restrict__ dkv_acc,
+                       int ablate) {
+  // ablate (KPO_ATTN_BWD_ABLATE, measurement only; results are wrong when != 0): 1 = no dQ reduce-add,
+  // 2 = no dQ drain (TMEM -> smem), 4 = no exponentials, 8 = no dQ^T MMA
   // dkv_acc != nullptr: split-group mode — one CTA per (q head, key tile); dK / dV contributions are
   // reduced into fp32 accumulators [T][hkv][D] (dK at dkv_acc, dV at dkv_acc + T*hkv*D).
   using C = Bwd<D>;
@@ -458,10 +461,12 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
         }
         mbar_wait(smem_u32(&dq_empty[0]), (j & 1) ^ 1);
         tc_fence_after();
+        if (!(ablate & 8)) {
 #pragma unroll
-        for (int k = 0; k < BN / 16; ++k) {
-          tc_mma(tmem + C::COL_DQ, smem_desc(sK + k * 2048, BN * 128, 1024),
-                 smem_desc(db + k * 2048, BM * 128, 1024), ID_Q, k > 0 ? 1u : 0u);
+          for (int k = 0; k < BN / 16; ++k) {
+            tc_mma(tmem + C::COL_DQ, smem_desc(sK + k * 2048, BN * 128, 1024),
+                   smem_desc(db + k * 2048, BM * 128, 1024), ID_Q, k > 0 ? 1u : 0u);
+          }
         }
         tc_commit(smem_u32(&dq_full[0]));
         tc_commit(smem_u32(&pds_empty[st]));
@@ -529,7 +534,8 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const int qi = half * HC + ch * 8 + e;
-          float pe = ex2(fmaf(sv[ch * 8 + e], scale_log2, -st[qi] * kLog2e));
+          const float xe = fmaf(sv[ch * 8 + e], scale_log2, -st[qi] * kLog2e);
+          float pe = (ablate & 4) ? xe : ex2(xe);
           float de = pe * (dp[ch * 8 + e] - st[BM + qi]);
           if (mask && (key >= T || m0 + qi >= T || (causal && m0 + qi < key))) pe = de = 0.f;
           p[e] = pe;
@@ -603,6 +609,12 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
       mbar_wait(smem_u32(&dq_full[0]), s & 1);
       tc_fence_after();
       float v[BM];
+      if (ablate & 2) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&dq_empty[0]));
+        continue;
+      }
 #pragma unroll
       for (int c = 0; c < BM / 32; ++c)
         tmem_ld32_nowait(lane_addr + C::COL_DQ + c * 32, reinterpret_cast<uint32_t*>(v + c * 32));
@@ -618,7 +630,7 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
       for (int qi = 0; qi < BM; ++qi) stg[qi * D + dcol] = v[qi] * scale;
       fence_async_smem();
       named_bar(2, 128);
-      if (dtid == 0) {
+      if (dtid == 0 && !(ablate & 1)) {
         tma_reduce_add_2d(&tmDQ, smem_u32(stg), h * D, m0);
         bulk_commit();
       }
@@ -651,7 +663,7 @@ int bwd_launch(const void* q, const void* k, const void* v, const void* dout, co
   dim3 grid((unsigned)(dkv_acc ? hq : hkv), (unsigned)((T + C::BN - 1) / C::BN));
   attn_bwd_tc_kernel<D><<<grid, C::THREADS, C::SMEM, st>>>(mq, mk, mv, mo, mdq, lse, dvec, dq_acc, (__nv_bfloat16*)dk,
                                                           (__nv_bfloat16*)dv, (int)T, hq, hkv, dks, dvs, scale, causal,
-                                                          dkv_acc);
+                                                          dkv_acc, getenv("KPO_ATTN_BWD_ABLATE") ? atoi(getenv("KPO_ATTN_BWD_ABLATE")) : 0);
   KPO_LAUNCH_CHECK();
   return KPO_OK;
 }

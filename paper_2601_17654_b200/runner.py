@@ -65,6 +65,69 @@ class LayerRunner:
                 dx.copy_(a["dx"], non_blocking=True)
         st.synchronize()
 
+    # ---------------------------------------------------------------- pipelined host-buffer entry point
+    def _pipe_init(self) -> None:
+        dev = self.engine.device
+        self._h2d = torch.cuda.Stream(dev)
+        self._d2h = torch.cuda.Stream(dev)
+        # two device staging slots: slot s holds step k's inputs while step k-1 still computes, and
+        # step k's dx while step k+1 computes
+        self._stage_in = [[(torch.empty_like(a["x"]), torch.empty_like(a["dy"])) for a in self.layer.nb]
+                          for _ in range(2)]
+        self._stage_out = [[torch.empty_like(a["dx"]) for a in self.layer.nb] for _ in range(2)]
+        ev = lambda: [torch.cuda.Event(), torch.cuda.Event()]
+        self._in_ready, self._in_free, self._out_ready, self._out_free = ev(), ev(), ev(), ev()
+        self._pipe_k = 0
+        self._pipe_used = [False, False]
+
+    def step_host_async(self, xs_host: list[torch.Tensor], dys_host: list[torch.Tensor],
+                        dxs_host: list[torch.Tensor]) -> None:
+        """Enqueue one iteration from pinned host buffers without waiting for it.
+
+        The H2D of this step's inputs runs on a copy stream. It overlaps the previous step's
+        compute. The D2H of this step's dx overlaps the next step's compute. The compute stream only
+        pays two device-to-device copies into and out of the layer's graph-bound buffers. The host
+        buffers of a step must stay untouched until `drain()` (or two steps later) returns.
+        Call `drain()` to wait for every enqueued step."""
+        if not hasattr(self, "_pipe_k"):
+            self._pipe_init()
+        s = self._pipe_k & 1
+        comp = self.engine.exec.compute
+        used = self._pipe_used[s]
+        with torch.cuda.stream(self._h2d):
+            if used:
+                self._h2d.wait_event(self._in_free[s])
+            for (sx, sdy), x, dy in zip(self._stage_in[s], xs_host, dys_host):
+                sx.copy_(x, non_blocking=True)
+                sdy.copy_(dy, non_blocking=True)
+            self._in_ready[s].record(self._h2d)
+        comp.wait_event(self._in_ready[s])
+        with torch.cuda.stream(comp):
+            for a, (sx, sdy) in zip(self.layer.nb, self._stage_in[s]):
+                a["x"].copy_(sx, non_blocking=True)
+                a["dy"].copy_(sdy, non_blocking=True)
+            self._in_free[s].record(comp)
+        self.step()
+        if used:
+            comp.wait_event(self._out_free[s])
+        with torch.cuda.stream(comp):
+            for a, so in zip(self.layer.nb, self._stage_out[s]):
+                so.copy_(a["dx"], non_blocking=True)
+            self._out_ready[s].record(comp)
+        self._d2h.wait_event(self._out_ready[s])
+        with torch.cuda.stream(self._d2h):
+            for so, dx in zip(self._stage_out[s], dxs_host):
+                dx.copy_(so, non_blocking=True)
+            self._out_free[s].record(self._d2h)
+        self._pipe_used[s] = True
+        self._pipe_k += 1
+
+    def drain(self) -> None:
+        if hasattr(self, "_pipe_k"):
+            self._d2h.synchronize()
+            self._h2d.synchronize()
+        self.engine.exec.compute.synchronize()
+
     # ---------------------------------------------------------------- instrumentation
     def unit_times(self, iters: int = 3) -> dict[str, list[float]]:
         """Per-launch-unit durations (ms) inside real iterations: eager issue with CUDA events

@@ -75,3 +75,47 @@ def test_tp_shards_sum_to_full(cuda):
         comm.close()
     ref = layer_ref.layer_fwd_bwd([x], [torch.zeros_like(x)], W, wl.model)
     assert rel(sum(parts), ref["h"][0]) < TOL
+
+
+def test_pipelined_host_steps_match_synchronous(cuda):
+    """LayerRunner.step_host_async: per-step dx equals the synchronous step_host result for the
+    same inputs, with a different input per step (staging slots and copy-stream ordering)."""
+    from paper_2601_17654_b200 import b200_model
+    from paper_2601_17654_b200.comm import Communicator
+    from paper_2601_17654_b200.engine import Engine
+    from paper_2601_17654_b200.layer import PartitionedLayer
+    from paper_2601_17654_b200.runner import LayerRunner
+    wl = _small("fsdp", 4, 128)
+    comm = Communicator.loopback_group(4, 64 << 20, device=cuda)
+    L = PartitionedLayer(wl, comm)
+    eng = Engine.for_layer(L, b200_model())
+    run = LayerRunner(L, eng)
+    run.warm()
+    g = torch.Generator().manual_seed(7)
+    pin = lambda t: t.pin_memory()
+    steps = 5
+    xs = [[pin(torch.randn(a["x"].shape, generator=g).to(a["x"].dtype)) for a in L.nb] for _ in range(steps)]
+    dys = [[pin(torch.randn(a["dy"].shape, generator=g).to(a["dy"].dtype)) for a in L.nb] for _ in range(steps)]
+    # the backward of an iteration finishes the previous iteration's input norm (norm1_bwd of the
+    # "upper layer", specs.BLOCKS), so dx of step k also depends on step k-1: both sequences start
+    # from the same primed state
+    prime = [pin(torch.zeros(a["x"].shape, dtype=a["x"].dtype)) for a in L.nb]
+    scratch = [torch.empty(a["dx"].shape, dtype=a["dx"].dtype).pin_memory() for a in L.nb]
+    run.step_host(prime, prime, scratch)
+    sync_out = []
+    for k in range(steps):
+        dx = [torch.empty(a["dx"].shape, dtype=a["dx"].dtype).pin_memory() for a in L.nb]
+        run.step_host(xs[k], dys[k], dx)
+        sync_out.append([t.clone() for t in dx])
+    pipe_out = [[torch.empty(a["dx"].shape, dtype=a["dx"].dtype).pin_memory() for a in L.nb] for _ in range(steps)]
+    run.step_host(prime, prime, scratch)
+    for k in range(steps):
+        run.step_host_async(xs[k], dys[k], pipe_out[k])
+    run.drain()
+    # fp32 atomics / TMA reduce-adds in attention backward make it deterministic only up to rounding
+    for k in range(steps):
+        for a, b in zip(pipe_out[k], sync_out[k]):
+            assert rel(a, b) < 2e-3, f"step {k}"
+            assert rel(a, sync_out[(k + 1) % steps][0]) > 0.5  # not some other step's result
+    eng.close()
+    comm.close()

@@ -26,16 +26,16 @@ struct Fwd {
   static constexpr int BM = 128, BN = 128, STAGES = 2;
   static constexpr int Q_BYTES = BM * D * 2;  // D/64 sub-tiles of [128 rows x 64] (16 KB each)
   static constexpr int KV_BYTES = BN * D * 2;
-  static constexpr int P_BYTES = BM * BN * 2;  // 2 sub-tiles of [128 q x 64 keys]; double-buffered
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + Q_BYTES;
   static constexpr int OFF_V = OFF_K + STAGES * KV_BYTES;
-  static constexpr int OFF_P = OFF_V + STAGES * KV_BYTES;
-  static constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
+  static constexpr int OFF_BAR = OFF_V + STAGES * KV_BYTES;
   static constexpr int SMEM_RAW = OFF_BAR + 256 + 1024;
   // keep one CTA per SM (the kernel allocates all 512 TMEM columns)
   static constexpr int SMEM = SMEM_RAW > 120 * 1024 ? SMEM_RAW : 120 * 1024;
   static constexpr int TMEM_COLS = 512;
+  // S_j in buffer j & 1; the softmax overwrites the first 64 columns of S_j with P_j (bf16 pairs),
+  // the TMEM A operand of the P V MMA
   static constexpr int COL_S0 = 0, COL_S1 = 128, COL_O = 256;
 };
 
@@ -58,7 +58,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* kv_full = bar + 1;   // [2]
   uint64_t* kv_empty = bar + 3;  // [2]
   uint64_t* s_full = bar + 5;    // [2]
-  uint64_t* s_empty = bar + 7;   // [2]
   uint64_t* p_full = bar + 9;    // [2]
   uint64_t* pv_done = bar + 11;  // [2]  PV(i) commits to pv_done[i & 1]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 13);
@@ -77,7 +76,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(&kv_full[i]), 1);
       mbar_init(smem_u32(&kv_empty[i]), 1);
       mbar_init(smem_u32(&s_full[i]), 1);
-      mbar_init(smem_u32(&s_empty[i]), 4);
       mbar_init(smem_u32(&p_full[i]), 4);
       mbar_init(smem_u32(&pv_done[i]), 1);
     }
@@ -87,9 +85,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  // one CTA per SM owns all 512 columns, so the allocation starts at lane 0 / column 0; a constant base
+  // keeps every TMEM address of the MMA issue loops in uniform registers (no per-MMA R2UR)
+  if (*tmem_slot != 0) __trap();
+  constexpr uint32_t tmem = 0;
   const uint32_t sQ = smem_u32(smem + C::OFF_Q), sK = smem_u32(smem + C::OFF_K);
-  const uint32_t sV = smem_u32(smem + C::OFF_V), sP = smem_u32(smem + C::OFF_P);
+  const uint32_t sV = smem_u32(smem + C::OFF_V);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -115,35 +116,31 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t ID_S = idesc_bf16(BM, BN, false, false);
       constexpr uint32_t ID_O = idesc_bf16(BM, D, false, true);
       mbar_wait(smem_u32(q_full), 0);
+      const uint32_t q_k = desc_lo(sQ, 16);
       auto issue_pv = [&](int i) {
         mbar_wait(smem_u32(&p_full[i & 1]), (i >> 1) & 1);
         tc_fence_after();
-        const uint32_t vb = sV + (i & 1) * C::KV_BYTES;
-        const uint32_t pb = sP + (i & 1) * C::P_BYTES;
+        const uint32_t v_mn = desc_lo(sV + (i & 1) * C::KV_BYTES, BN * 128);
+        const uint32_t p_t = tmem + ((i & 1) ? C::COL_S1 : C::COL_S0);
 #pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk) {  // 16 keys per UMMA
-          const uint64_t da = smem_desc(pb + (kk >> 2) * BM * 128 + (kk & 3) * 32, 16, 1024);
-          const uint64_t db = smem_desc(vb + kk * 2048, BN * 128, 1024);
-          tc_mma(tmem + C::COL_O, da, db, ID_O, (i > 0 || kk > 0) ? 1u : 0u);
-        }
+        for (int kk = 0; kk < BN / 16; ++kk)  // 16 keys per UMMA, P from TMEM (8 columns of bf16 pairs)
+          tc_mma_ts_lo(tmem + C::COL_O, p_t + kk * 8, v_mn + kk * 128, ID_O, (i > 0 || kk > 0) ? 1u : 0u);
         tc_commit(smem_u32(&pv_done[i & 1]));
         tc_commit(smem_u32(&kv_empty[i & 1]));
       };
       for (int j = 0; j < n_tiles; ++j) {
         const int s = j & 1;
         mbar_wait(smem_u32(&kv_full[s]), (j >> 1) & 1);
-        mbar_wait(smem_u32(&s_empty[s]), ((j >> 1) & 1) ^ 1);
+        // buffer s holds P_{j-2}: PV_{j-2} was issued before this S_j and tcgen05.mma executes in
+        // issue order, so no wait is needed
         tc_fence_after();
-        const uint32_t kb_base = sK + s * C::KV_BYTES;
+        const uint32_t k_k = desc_lo(sK + s * C::KV_BYTES, 16);
         const uint32_t d_s = tmem + (s ? C::COL_S1 : C::COL_S0);
 #pragma unroll
         for (int kb = 0; kb < KSUB; ++kb) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const uint64_t da = smem_desc(sQ + kb * BM * 128 + k * 32, 16, 1024);
-            const uint64_t db = smem_desc(kb_base + kb * BN * 128 + k * 32, 16, 1024);
-            tc_mma(d_s, da, db, ID_S, (kb | k) ? 1u : 0u);
-          }
+          for (int k = 0; k < 4; ++k)
+            tc_mma_lo(d_s, q_k + kb * (BM * 8) + k * 2, k_k + kb * (BN * 8) + k * 2, ID_S, (kb | k) ? 1u : 0u);
         }
         tc_commit(smem_u32(&s_full[s]));
         if (j > 0) issue_pv(j - 1);
@@ -166,9 +163,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int c = 0; c < BN / 32; ++c) tmem_ld32_nowait(s_addr + c * 32, reinterpret_cast<uint32_t*>(sv + c * 32));
       tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&s_empty[s]));
       const int k0 = j * BN;
       const bool mask = (causal && k0 + BN - 1 > m0) || (k0 + BN > T);
       if (mask) {
@@ -193,7 +187,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         rescale = (j > 0);
         m_run = mx;
       }
-      if (j >= 2) mbar_wait(smem_u32(&pv_done[s]), ((j - 2) >> 1) & 1);  // P[s] free (PV(j-2) done)
       // tcgen05.ld/st are warp-collective (.sync.aligned): the rescale decision must be warp-uniform;
       // lanes that do not need it multiply by corr == 1.
       if (__any_sync(0xffffffffu, rescale)) {
@@ -213,26 +206,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float neg_m = -m_run;
       float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int ch = 0; ch < BN / 8; ++ch) {  // 16-byte chunks of 8 keys
-        float p[8];
+      for (int half = 0; half < 2; ++half) {  // 64 keys -> 32 columns of bf16 pairs over S_j
+        uint32_t pk[32];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float xe = fmaf(sv[ch * 8 + e], scale_log2, neg_m);
-          p[e] = ((POLY_MASK >> e) & 1) ? ex2_poly(xe) : ex2(xe);
-          ps[e] += p[e];
+        for (int c = 0; c < 32; ++c) {
+          float p[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int i = half * 64 + c * 2 + e;
+            const float xe = fmaf(sv[i], scale_log2, neg_m);
+            p[e] = ((POLY_MASK >> (i & 7)) & 1) ? ex2_poly(xe) : ex2(xe);
+            ps[i & 7] += p[e];
+          }
+          pk[c] = pack_bf16x2(p[0], p[1]);
         }
-        uint4 u;
-        u.x = pack_bf16x2(p[0], p[1]);
-        u.y = pack_bf16x2(p[2], p[3]);
-        u.z = pack_bf16x2(p[4], p[5]);
-        u.w = pack_bf16x2(p[6], p[7]);
-        const uint32_t addr = sP + s * C::P_BYTES + (ch >> 3) * BM * 128 + sw128(r, ch & 7);
-        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(u.x), "r"(u.y), "r"(u.z), "r"(u.w)
-                     : "memory");
+        tmem_st32(s_addr + half * 32, pk);
       }
       const float lsum = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
       l_run = l_run * corr + lsum;
-      fence_async_smem();
+      tmem_wait_st();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&p_full[s]));
@@ -345,7 +337,8 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
                        int64_t dks, int64_t dvs, float scale, int causal, float* __restrict__ dkv_acc,
                        int ablate) {
   // ablate (KPO_ATTN_BWD_ABLATE, measurement only; results are wrong when != 0): 1 = no dQ reduce-add,
-  // 2 = no dQ drain (TMEM -> smem), 4 = no exponentials, 8 = no dQ^T MMA
+  // 2 = no dQ drain (TMEM -> smem), 4 = no exponentials, 8 = no dQ^T MMA, 16 = no softmax,
+  // 32 = no Q/dO reloads, 64 = no dV/dK MMAs, 128 = no S^T/dP^T MMAs
   // dkv_acc != nullptr: split-group mode — one CTA per (q head, key tile); dK / dV contributions are
   // reduced into fp32 accumulators [T][hkv][D] (dK at dkv_acc, dV at dkv_acc + T*hkv*D).
   using C = Bwd<D>;
@@ -399,7 +392,10 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  // one CTA per SM owns all 512 columns, so the allocation starts at lane 0 / column 0; a constant base
+  // keeps every TMEM address of the MMA issue loops in uniform registers (no per-MMA R2UR)
+  if (*tmem_slot != 0) __trap();
+  constexpr uint32_t tmem = 0;
   const uint32_t sK = smem_u32(smem + C::OFF_K), sV = smem_u32(smem + C::OFF_V);
   const uint32_t sQ = smem_u32(smem + C::OFF_Q), sDO = smem_u32(smem + C::OFF_DO);
   const uint32_t sDS = smem_u32(smem + C::OFF_DS);  // dS^T buffer b at b*PT_BYTES
@@ -424,6 +420,10 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
         step_coords(s, h, m0);
         mbar_wait(smem_u32(&qd_empty[st]), ((s / C::QSTAGES) & 1) ^ 1);
         const uint32_t fb = smem_u32(&qd_full[st]);
+        if ((ablate & 32) && s >= C::QSTAGES) {  // measurement: reuse stale Q/dO tiles (no L2 traffic)
+          mbar_arrive(fb);
+          continue;
+        }
         const uint32_t nstat = (uint32_t)min(BM, T - m0) * 4u;  // T % 8 == 0 keeps this a 16 B multiple
         mbar_arrive_expect_tx(fb, 2 * C::QT_BYTES + 2 * nstat);
 #pragma unroll
@@ -444,29 +444,29 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
       constexpr uint32_t ID_Q = idesc_bf16(D, BM, true, true);      // dQ^T
       mbar_wait(smem_u32(kv_full), 0);
       constexpr uint32_t ID_GT = idesc_bf16(BN, D, false, true);   // dV with A = P^T from TMEM
+      const uint32_t k_k = desc_lo(sK, 16), v_k = desc_lo(sV, 16), k_mn = desc_lo(sK, BN * 128);
       auto grads = [&](int j) {
         const int st = j & 1;          // P^T / dS^T buffer
         const int qs = j % C::QSTAGES;  // Q/dO stage
         mbar_wait(smem_u32(&pds_full[st]), (j >> 1) & 1);
         tc_fence_after();
-        const uint32_t qb = sQ + qs * C::QT_BYTES, ob = sDO + qs * C::QT_BYTES;
-        const uint32_t db = sDS + st * C::PT_BYTES;
+        const uint32_t q_mn = desc_lo(sQ + qs * C::QT_BYTES, BM * 128), o_mn = desc_lo(sDO + qs * C::QT_BYTES, BM * 128);
+        const uint32_t ds_k = desc_lo(sDS + st * C::PT_BYTES, 16), ds_mn = desc_lo(sDS + st * C::PT_BYTES, BM * 128);
+        const uint32_t pt = tmem + C::COL_PT + st * 32;
+        if (!(ablate & 64)) {
 #pragma unroll
-        for (int k = 0; k < BM / 16; ++k) {
-          const uint32_t acc = (j > 0 || k > 0) ? 1u : 0u;
-          tc_mma_ts(tmem + C::COL_DV, tmem + C::COL_PT + st * 32 + k * 8, smem_desc(ob + k * 2048, BM * 128, 1024),
-                    ID_GT, acc);
-          tc_mma(tmem + C::COL_DK, smem_desc(db + k * 32, 16, 1024), smem_desc(qb + k * 2048, BM * 128, 1024), ID_G,
-                 acc);
+          for (int k = 0; k < BM / 16; ++k) {
+            const uint32_t acc = (j > 0 || k > 0) ? 1u : 0u;
+            tc_mma_ts_lo(tmem + C::COL_DV, pt + k * 8, o_mn + k * 128, ID_GT, acc);
+            tc_mma_lo(tmem + C::COL_DK, ds_k + k * 2, q_mn + k * 128, ID_G, acc);
+          }
         }
         mbar_wait(smem_u32(&dq_empty[0]), (j & 1) ^ 1);
         tc_fence_after();
         if (!(ablate & 8)) {
 #pragma unroll
-          for (int k = 0; k < BN / 16; ++k) {
-            tc_mma(tmem + C::COL_DQ, smem_desc(sK + k * 2048, BN * 128, 1024),
-                   smem_desc(db + k * 2048, BM * 128, 1024), ID_Q, k > 0 ? 1u : 0u);
-          }
+          for (int k = 0; k < BN / 16; ++k)
+            tc_mma_lo(tmem + C::COL_DQ, k_mn + k * 128, ds_mn + k * 128, ID_Q, k > 0 ? 1u : 0u);
         }
         tc_commit(smem_u32(&dq_full[0]));
         tc_commit(smem_u32(&pds_empty[st]));
@@ -476,16 +476,16 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
         const int st = s % C::QSTAGES;
         mbar_wait(smem_u32(&qd_full[st]), (s / C::QSTAGES) & 1);
         tc_fence_after();
-        const uint32_t qb = sQ + st * C::QT_BYTES, ob = sDO + st * C::QT_BYTES;
+        const uint32_t q_k = desc_lo(sQ + st * C::QT_BYTES, 16), o_k = desc_lo(sDO + st * C::QT_BYTES, 16);
+        if (!(ablate & 128)) {
 #pragma unroll
-        for (int kb = 0; kb < KSUB; ++kb) {
+          for (int kb = 0; kb < KSUB; ++kb) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const uint32_t acc = (kb | k) ? 1u : 0u;
-            tc_mma(tmem + C::COL_S, smem_desc(sK + kb * BN * 128 + k * 32, 16, 1024),
-                   smem_desc(qb + kb * BM * 128 + k * 32, 16, 1024), ID_S, acc);
-            tc_mma(tmem + C::COL_DP, smem_desc(sV + kb * BN * 128 + k * 32, 16, 1024),
-                   smem_desc(ob + kb * BM * 128 + k * 32, 16, 1024), ID_S, acc);
+            for (int k = 0; k < 4; ++k) {
+              const uint32_t acc = (kb | k) ? 1u : 0u;
+              tc_mma_lo(tmem + C::COL_S, k_k + kb * (BN * 8) + k * 2, q_k + kb * (BM * 8) + k * 2, ID_S, acc);
+              tc_mma_lo(tmem + C::COL_DP, v_k + kb * (BN * 8) + k * 2, o_k + kb * (BM * 8) + k * 2, ID_S, acc);
+            }
           }
         }
         tc_commit(smem_u32(s_full));
@@ -509,43 +509,61 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
     const int key = n0 + r;
     const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
     constexpr int HC = BM / 2;  // query columns per warp
-    for (int s = 0; s < steps; ++s) {
-      int h, m0;
-      step_coords(s, h, m0);
-      (void)h;
+    const float* stat_half = stat + half * HC;
+    for (int s = 0, mi = 0; s < steps; ++s, mi = (mi + 1 == mq) ? 0 : mi + 1) {
+      const int m0 = (m_start + mi) * BM;
       const int buf = s & 1;
-      const float* st = stat + (s % C::QSTAGES) * 2 * BM;  // raw lse / D rows, filled by the TMA warp
       mbar_wait(smem_u32(s_full), s & 1);
       tc_fence_after();
       float sv[HC], dp[HC];
       tmem_ld32_nowait(lane_addr + C::COL_S + half * HC, reinterpret_cast<uint32_t*>(sv));
       tmem_ld32_nowait(lane_addr + C::COL_DP + half * HC, reinterpret_cast<uint32_t*>(dp));
+      // this warp's 32 query statistics (lse, D), bulk-copied by the TMA warp with the Q/dO stage
+      const uint32_t sst = smem_u32(stat_half + (s % C::QSTAGES) * 2 * BM);
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(s_empty));
+      if (ablate & 16) {  // measurement: no softmax work at all
+        mbar_wait(smem_u32(&pds_empty[buf]), ((s >> 1) & 1) ^ 1);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&pds_full[buf]));
+        continue;
+      }
+      // CTA-uniform: does this tile need the causal / tail mask at all?
+      const bool tile_mask = (causal && m0 < n0 + BN - 1) || n0 + BN > T || m0 + BM > T;
+      uint32_t pp[HC / 2], qq[HC / 2];
+#pragma unroll
+      for (int i = 0; i < HC; i += 2) {
+        float p2[2], d2[2];
+        float nl[2], dd[2];
+        asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(nl[0]), "=f"(nl[1]) : "r"(sst + i * 4));
+        asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(dd[0]), "=f"(dd[1]) : "r"(sst + BM * 4 + i * 4));
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const float xe = fmaf(sv[i + e], scale_log2, -nl[e] * kLog2e);
+          float pe = (ablate & 4) ? xe : ex2(xe);
+          float de = pe * (dp[i + e] - dd[e]);
+          if (tile_mask) {
+            const int q = m0 + half * HC + i + e;
+            const bool z = key >= T || q >= T || (causal && q < key);
+            pe = z ? 0.f : pe;
+            de = z ? 0.f : de;
+          }
+          p2[e] = pe;
+          d2[e] = de;
+        }
+        pp[i / 2] = pack_bf16x2(p2[0], p2[1]);
+        qq[i / 2] = pack_bf16x2(d2[0], d2[1]);
+      }
       mbar_wait(smem_u32(&pds_empty[buf]), ((s >> 1) & 1) ^ 1);  // grads(s-2) done with this buffer
-      const bool mask = (causal && m0 < n0 + BN - 1) || key >= T || m0 + BM > T;
       const uint32_t db = sDS + buf * C::PT_BYTES;
-      uint32_t pp[HC / 2];
 #pragma unroll
       for (int ch = 0; ch < HC / 8; ++ch) {
-        float p[8], ds[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int qi = half * HC + ch * 8 + e;
-          const float xe = fmaf(sv[ch * 8 + e], scale_log2, -st[qi] * kLog2e);
-          float pe = (ablate & 4) ? xe : ex2(xe);
-          float de = pe * (dp[ch * 8 + e] - st[BM + qi]);
-          if (mask && (key >= T || m0 + qi >= T || (causal && m0 + qi < key))) pe = de = 0.f;
-          p[e] = pe;
-          ds[e] = de;
-        }
-#pragma unroll
-        for (int e = 0; e < 4; ++e) pp[ch * 4 + e] = pack_bf16x2(p[2 * e], p[2 * e + 1]);
         const uint32_t off = sw128(r, half * (HC / 8) + ch);
-        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(db + off), "r"(pack_bf16x2(ds[0], ds[1])),
-                     "r"(pack_bf16x2(ds[2], ds[3])), "r"(pack_bf16x2(ds[4], ds[5])), "r"(pack_bf16x2(ds[6], ds[7]))
+        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(db + off), "r"(qq[ch * 4]), "r"(qq[ch * 4 + 1]),
+                     "r"(qq[ch * 4 + 2]), "r"(qq[ch * 4 + 3])
                      : "memory");
       }
       // P^T row (this warp's 32 queries = 16 packed columns) -> TMEM, the A operand of the dV MMA

@@ -149,6 +149,32 @@ __device__ __forceinline__ float ex2_poly(float x) {
   return __int_as_float(__float_as_int(p) + (static_cast<int>(fi) << 23));
 }
 
+// Split UMMA descriptors for the issue loops.  Every tile here is SWIZZLE_128B with SBO = 1024, so
+// the high word is one constant; the low word is (start >> 4) | (LBO >> 4) << 16 and moves by
+// (byte offset >> 4).  Building the low word once per buffer and adding constants keeps the MMA
+// issuer in uniform registers: a full smem_desc() per tcgen05.mma costs ~50 extra issue cycles
+// (measured, tools/ubench_tc.cu), more than an M=128 N=64 MMA takes on the tensor core.
+constexpr uint32_t kDescHiSw128 = 0x40004040u;
+__device__ __forceinline__ uint32_t desc_lo(uint32_t addr, uint32_t lbo) { return (addr >> 4) + ((lbo >> 4) << 16); }
+__device__ __forceinline__ void tc_mma_lo(uint32_t tmem_d, uint32_t a_lo, uint32_t b_lo, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 da, db;\n\t"
+      "mov.b64 da, {%1, %5};\n\t"
+      "mov.b64 db, {%2, %5};\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], da, db, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(acc), "n"(kDescHiSw128));
+}
+__device__ __forceinline__ void tc_mma_ts_lo(uint32_t tmem_d, uint32_t tmem_a, uint32_t b_lo, uint32_t idesc,
+                                             uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 db;\n\t"
+      "mov.b64 db, {%2, %5};\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], db, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "r"(b_lo), "r"(idesc), "r"(acc), "n"(kDescHiSw128));
+}
+
 // UMMA instruction descriptor: bf16 x bf16 -> f32, M x N, operand majorness.
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool b_mn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |

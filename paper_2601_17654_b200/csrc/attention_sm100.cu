@@ -23,7 +23,10 @@ constexpr int kThreads = 192;
 
 template <int D>
 struct Fwd {
-  static constexpr int BM = 128, BN = 128, STAGES = 2;
+  // K and V have separate 3-stage rings: K_j is released as soon as S_j is done, V_j after P_j V_j,
+  // so the next tiles' loads start early enough to hide the L2 latency (measured: with one 2-stage
+  // K+V ring the S MMAs waited on the loads ~1/4 of the time)
+  static constexpr int BM = 128, BN = 128, STAGES = 3;
   static constexpr int Q_BYTES = BM * D * 2;  // D/64 sub-tiles of [128 rows x 64] (16 KB each)
   static constexpr int KV_BYTES = BN * D * 2;
   static constexpr int OFF_Q = 0;
@@ -55,12 +58,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* q_full = bar + 0;
-  uint64_t* kv_full = bar + 1;   // [2]
-  uint64_t* kv_empty = bar + 3;  // [2]
-  uint64_t* s_full = bar + 5;    // [2]
-  uint64_t* p_full = bar + 9;    // [2]
-  uint64_t* pv_done = bar + 11;  // [2]  PV(i) commits to pv_done[i & 1]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 13);
+  uint64_t* k_full = bar + 1;    // [3]
+  uint64_t* k_empty = bar + 4;   // [3]
+  uint64_t* v_full = bar + 7;    // [3]
+  uint64_t* v_empty = bar + 10;  // [3]
+  uint64_t* s_full = bar + 13;   // [2]
+  uint64_t* p_full = bar + 15;   // [2]
+  uint64_t* pv_done = bar + 17;  // [2]  PV(i) commits to pv_done[i & 1]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 19);
+  constexpr int KS = C::STAGES;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mblk = gridDim.y - 1 - blockIdx.y;  // heavy (late) causal rows first, all heads of a row-tile together
@@ -72,9 +78,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(smem_u32(q_full), 1);
+    for (int i = 0; i < KS; ++i) {
+      mbar_init(smem_u32(&k_full[i]), 1);
+      mbar_init(smem_u32(&k_empty[i]), 1);
+      mbar_init(smem_u32(&v_full[i]), 1);
+      mbar_init(smem_u32(&v_empty[i]), 1);
+    }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(smem_u32(&kv_full[i]), 1);
-      mbar_init(smem_u32(&kv_empty[i]), 1);
       mbar_init(smem_u32(&s_full[i]), 1);
       mbar_init(smem_u32(&p_full[i]), 4);
       mbar_init(smem_u32(&pv_done[i]), 1);
@@ -98,16 +108,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive_expect_tx(smem_u32(q_full), C::Q_BYTES);
 #pragma unroll
       for (int kb = 0; kb < KSUB; ++kb) tma_load_2d(sQ + kb * BM * 128, &tmQ, smem_u32(q_full), h * D + kb * 64, m0);
-      for (int j = 0; j < n_tiles; ++j) {
-        const int s = j & 1;
-        mbar_wait(smem_u32(&kv_empty[s]), ((j >> 1) & 1) ^ 1);
-        const uint32_t fb = smem_u32(&kv_full[s]);
-        mbar_arrive_expect_tx(fb, 2 * C::KV_BYTES);
+      for (int j = 0, s = 0, ph = 0; j < n_tiles; ++j) {
+        mbar_wait(smem_u32(&k_empty[s]), ph ^ 1);
+        uint32_t fb = smem_u32(&k_full[s]);
+        mbar_arrive_expect_tx(fb, C::KV_BYTES);
 #pragma unroll
-        for (int kb = 0; kb < KSUB; ++kb) {
+        for (int kb = 0; kb < KSUB; ++kb)
           tma_load_2d(sK + s * C::KV_BYTES + kb * BN * 128, &tmK, fb, kvh * D + kb * 64, j * BN);
+        mbar_wait(smem_u32(&v_empty[s]), ph ^ 1);
+        fb = smem_u32(&v_full[s]);
+        mbar_arrive_expect_tx(fb, C::KV_BYTES);
+#pragma unroll
+        for (int kb = 0; kb < KSUB; ++kb)
           tma_load_2d(sV + s * C::KV_BYTES + kb * BN * 128, &tmV, fb, kvh * D + kb * 64, j * BN);
-        }
+        if (++s == KS) s = 0, ph ^= 1;
       }
     }
   } else if (warp == 1) {
@@ -118,23 +132,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(smem_u32(q_full), 0);
       const uint32_t q_k = desc_lo(sQ, 16);
       auto issue_pv = [&](int i) {
+        const int vs = i % KS;
+        mbar_wait(smem_u32(&v_full[vs]), (i / KS) & 1);
         mbar_wait(smem_u32(&p_full[i & 1]), (i >> 1) & 1);
         tc_fence_after();
-        const uint32_t v_mn = desc_lo(sV + (i & 1) * C::KV_BYTES, BN * 128);
+        const uint32_t v_mn = desc_lo(sV + vs * C::KV_BYTES, BN * 128);
         const uint32_t p_t = tmem + ((i & 1) ? C::COL_S1 : C::COL_S0);
 #pragma unroll
         for (int kk = 0; kk < BN / 16; ++kk)  // 16 keys per UMMA, P from TMEM (8 columns of bf16 pairs)
           tc_mma_ts_lo(tmem + C::COL_O, p_t + kk * 8, v_mn + kk * 128, ID_O, (i > 0 || kk > 0) ? 1u : 0u);
         tc_commit(smem_u32(&pv_done[i & 1]));
-        tc_commit(smem_u32(&kv_empty[i & 1]));
+        tc_commit(smem_u32(&v_empty[vs]));
       };
       for (int j = 0; j < n_tiles; ++j) {
-        const int s = j & 1;
-        mbar_wait(smem_u32(&kv_full[s]), (j >> 1) & 1);
+        const int s = j & 1, ks = j % KS;
+        mbar_wait(smem_u32(&k_full[ks]), (j / KS) & 1);
         // buffer s holds P_{j-2}: PV_{j-2} was issued before this S_j and tcgen05.mma executes in
         // issue order, so no wait is needed
         tc_fence_after();
-        const uint32_t k_k = desc_lo(sK + s * C::KV_BYTES, 16);
+        const uint32_t k_k = desc_lo(sK + ks * C::KV_BYTES, 16);
         const uint32_t d_s = tmem + (s ? C::COL_S1 : C::COL_S0);
 #pragma unroll
         for (int kb = 0; kb < KSUB; ++kb) {
@@ -143,6 +159,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_mma_lo(d_s, q_k + kb * (BM * 8) + k * 2, k_k + kb * (BN * 8) + k * 2, ID_S, (kb | k) ? 1u : 0u);
         }
         tc_commit(smem_u32(&s_full[s]));
+        tc_commit(smem_u32(&k_empty[ks]));
         if (j > 0) issue_pv(j - 1);
       }
       issue_pv(n_tiles - 1);

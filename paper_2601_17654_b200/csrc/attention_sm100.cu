@@ -19,21 +19,22 @@ namespace attn_tc {
 using namespace kpo::sm100;
 
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;  // TMA warp, MMA warp, 8 softmax warps (two per TMEM lane quarter)
 
 template <int D>
 struct Fwd {
-  // K and V have separate 3-stage rings: K_j is released as soon as S_j is done, V_j after P_j V_j,
-  // so the next tiles' loads start early enough to hide the L2 latency (measured: with one 2-stage
-  // K+V ring the S MMAs waited on the loads ~1/4 of the time)
-  static constexpr int BM = 128, BN = 128, STAGES = 3;
+  // K and V have separate rings (3 and 2 stages): K_j is released as soon as S_j is done, V_j after
+  // P_j V_j, so the next tiles' loads start early enough to hide the L2 latency (measured: with one
+  // 2-stage K+V ring the S MMAs waited on the loads ~1/4 of the time)
+  static constexpr int BM = 128, BN = 128, STAGES = 3, VSTAGES = 2;
   static constexpr int Q_BYTES = BM * D * 2;  // D/64 sub-tiles of [128 rows x 64] (16 KB each)
   static constexpr int KV_BYTES = BN * D * 2;
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + Q_BYTES;
   static constexpr int OFF_V = OFF_K + STAGES * KV_BYTES;
-  static constexpr int OFF_BAR = OFF_V + STAGES * KV_BYTES;
-  static constexpr int SMEM_RAW = OFF_BAR + 256 + 1024;
+  static constexpr int OFF_BAR = OFF_V + VSTAGES * KV_BYTES;
+  static constexpr int OFF_XCH = OFF_BAR + 256;  // [2 parities][2 halves][128 rows] fp32 row-max exchange
+  static constexpr int SMEM_RAW = OFF_XCH + 2 * 2 * 128 * 4 + 1024;
   // keep one CTA per SM (the kernel allocates all 512 TMEM columns)
   static constexpr int SMEM = SMEM_RAW > 120 * 1024 ? SMEM_RAW : 120 * 1024;
   static constexpr int TMEM_COLS = 512;
@@ -41,6 +42,8 @@ struct Fwd {
   // the TMEM A operand of the P V MMA
   static constexpr int COL_S0 = 0, COL_S1 = 128, COL_O = 256;
 };
+
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
 // byte offset of the 16-byte chunk `chunk` (0..7) of row `r` in a [rows x 64] bf16 SW128 sub-tile
 __device__ __forceinline__ uint32_t sw128(int r, int chunk) {
@@ -66,7 +69,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* p_full = bar + 15;   // [2]
   uint64_t* pv_done = bar + 17;  // [2]  PV(i) commits to pv_done[i & 1]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 19);
-  constexpr int KS = C::STAGES;
+  constexpr int KS = C::STAGES, VS = C::VSTAGES;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mblk = gridDim.y - 1 - blockIdx.y;  // heavy (late) causal rows first, all heads of a row-tile together
@@ -81,12 +84,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < KS; ++i) {
       mbar_init(smem_u32(&k_full[i]), 1);
       mbar_init(smem_u32(&k_empty[i]), 1);
+    }
+    for (int i = 0; i < VS; ++i) {
       mbar_init(smem_u32(&v_full[i]), 1);
       mbar_init(smem_u32(&v_empty[i]), 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&s_full[i]), 1);
-      mbar_init(smem_u32(&p_full[i]), 4);
+      mbar_init(smem_u32(&p_full[i]), 8);
       mbar_init(smem_u32(&pv_done[i]), 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -108,20 +113,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive_expect_tx(smem_u32(q_full), C::Q_BYTES);
 #pragma unroll
       for (int kb = 0; kb < KSUB; ++kb) tma_load_2d(sQ + kb * BM * 128, &tmQ, smem_u32(q_full), h * D + kb * 64, m0);
-      for (int j = 0, s = 0, ph = 0; j < n_tiles; ++j) {
+      for (int j = 0, s = 0, ph = 0, v = 0, vph = 0; j < n_tiles; ++j) {
         mbar_wait(smem_u32(&k_empty[s]), ph ^ 1);
         uint32_t fb = smem_u32(&k_full[s]);
         mbar_arrive_expect_tx(fb, C::KV_BYTES);
 #pragma unroll
         for (int kb = 0; kb < KSUB; ++kb)
           tma_load_2d(sK + s * C::KV_BYTES + kb * BN * 128, &tmK, fb, kvh * D + kb * 64, j * BN);
-        mbar_wait(smem_u32(&v_empty[s]), ph ^ 1);
-        fb = smem_u32(&v_full[s]);
+        mbar_wait(smem_u32(&v_empty[v]), vph ^ 1);
+        fb = smem_u32(&v_full[v]);
         mbar_arrive_expect_tx(fb, C::KV_BYTES);
 #pragma unroll
         for (int kb = 0; kb < KSUB; ++kb)
-          tma_load_2d(sV + s * C::KV_BYTES + kb * BN * 128, &tmV, fb, kvh * D + kb * 64, j * BN);
+          tma_load_2d(sV + v * C::KV_BYTES + kb * BN * 128, &tmV, fb, kvh * D + kb * 64, j * BN);
         if (++s == KS) s = 0, ph ^= 1;
+        if (++v == VS) v = 0, vph ^= 1;
       }
     }
   } else if (warp == 1) {
@@ -132,8 +138,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(smem_u32(q_full), 0);
       const uint32_t q_k = desc_lo(sQ, 16);
       auto issue_pv = [&](int i) {
-        const int vs = i % KS;
-        mbar_wait(smem_u32(&v_full[vs]), (i / KS) & 1);
+        const int vs = i % VS;
+        mbar_wait(smem_u32(&v_full[vs]), (i / VS) & 1);
         mbar_wait(smem_u32(&p_full[i & 1]), (i >> 1) & 1);
         tc_fence_after();
         const uint32_t v_mn = desc_lo(sV + vs * C::KV_BYTES, BN * 128);
@@ -165,28 +171,37 @@ __global__ void __launch_bounds__(kThreads, 1)
       issue_pv(n_tiles - 1);
     }
   } else {
-    // ---------------------------------------------------------------- softmax warps 2..5
+    // ---------------------------------------------------------------- softmax warps 2..9
+    // Two warps per TMEM lane quarter (warp % 4): the row's 128 keys are split in two halves of 64, so
+    // every SM sub-partition runs two softmax warps and one's MUFU / FMA latency hides under the
+    // other's.  The halves exchange their row max through shared memory once per tile (named barrier
+    // per quarter); the row sums stay per half and are combined in the epilogue.
     const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int r = quarter * 32 + lane;  // query row within the tile == TMEM lane
     const int q = m0 + r;
     const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
+    float* xch = reinterpret_cast<float*>(smem + C::OFF_XCH);  // [parity][half][row]
+    const int bar_id = 1 + quarter;
     float m_run = -INFINITY, l_run = 0.f;
     for (int j = 0; j < n_tiles; ++j) {
       const int s = j & 1;
       mbar_wait(smem_u32(&s_full[s]), (j >> 1) & 1);
       tc_fence_after();
-      float sv[BN];
+      constexpr int HN = BN / 2;
+      float sv[HN];
       const uint32_t s_addr = lane_addr + (s ? C::COL_S1 : C::COL_S0);
 #pragma unroll
-      for (int c = 0; c < BN / 32; ++c) tmem_ld32_nowait(s_addr + c * 32, reinterpret_cast<uint32_t*>(sv + c * 32));
+      for (int c = 0; c < HN / 32; ++c)
+        tmem_ld32_nowait(s_addr + half * HN + c * 32, reinterpret_cast<uint32_t*>(sv + c * 32));
       tmem_wait_ld();
-      const int k0 = j * BN;
-      const bool mask = (causal && k0 + BN - 1 > m0) || (k0 + BN > T);
+      const int k0 = j * BN + half * HN;
+      const bool mask = (causal && j * BN + BN - 1 > m0) || (j * BN + BN > T);  // CTA-uniform
       if (mask) {
 #pragma unroll
-        for (int i = 0; i < BN; ++i) {
+        for (int i = 0; i < HN; ++i) {
           const int key = k0 + i;
-          if (key >= T || (causal && key > q)) sv[i] = -INFINITY;
+          sv[i] = (key >= T || (causal && key > q)) ? -INFINITY : sv[i];
         }
       }
       // row max over raw scores with 8 independent chains (scale > 0 commutes with max)
@@ -194,9 +209,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int e = 0; e < 8; ++e) pm[e] = sv[e];
 #pragma unroll
-      for (int i = 8; i < BN; ++i) pm[i & 7] = fmaxf(pm[i & 7], sv[i]);
-      const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
-                             fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7]))) * scale_log2;
+      for (int i = 8; i < HN; ++i) pm[i & 7] = fmaxf(pm[i & 7], sv[i]);
+      float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])), fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
+      xch[(s * 2 + half) * BM + r] = mx;
+      named_bar(bar_id, 64);
+      mx = fmaxf(mx, xch[(s * 2 + (half ^ 1)) * BM + r]) * scale_log2;
       float corr = 1.f;
       bool rescale = false;
       if (mx > m_run + 8.f) {  // lazy rescaling: only when the max grows by more than 2^8
@@ -205,40 +222,37 @@ __global__ void __launch_bounds__(kThreads, 1)
         m_run = mx;
       }
       // tcgen05.ld/st are warp-collective (.sync.aligned): the rescale decision must be warp-uniform;
-      // lanes that do not need it multiply by corr == 1.
+      // lanes that do not need it multiply by corr == 1.  Each half rescales its 64 output columns.
       if (__any_sync(0xffffffffu, rescale)) {
         mbar_wait(smem_u32(&pv_done[s ^ 1]), ((j - 1) >> 1) & 1);  // O stable (PV(j-1) done)
         tc_fence_after();
 #pragma unroll 1
-        for (int c = 0; c < D / 32; ++c) {
+        for (int c = 0; c < D / 64; ++c) {
           uint32_t ov[32];
-          tmem_ld32_nowait(lane_addr + C::COL_O + c * 32, ov);
+          const uint32_t oa = lane_addr + C::COL_O + half * (D / 2) + c * 32;
+          tmem_ld32_nowait(oa, ov);
           tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * corr);
-          tmem_st32(lane_addr + C::COL_O + c * 32, ov);
+          tmem_st32(oa, ov);
         }
-        tmem_wait_st();
       }
       const float neg_m = -m_run;
       float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      uint32_t pk[32];  // this half's 64 keys -> 32 columns of bf16 pairs over S_j
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {  // 64 keys -> 32 columns of bf16 pairs over S_j
-        uint32_t pk[32];
+      for (int c = 0; c < 32; ++c) {
+        float p[2];
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          float p[2];
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int i = half * 64 + c * 2 + e;
-            const float xe = fmaf(sv[i], scale_log2, neg_m);
-            p[e] = ((POLY_MASK >> (i & 7)) & 1) ? ex2_poly(xe) : ex2(xe);
-            ps[i & 7] += p[e];
-          }
-          pk[c] = pack_bf16x2(p[0], p[1]);
+        for (int e = 0; e < 2; ++e) {
+          const int i = c * 2 + e;
+          const float xe = fmaf(sv[i], scale_log2, neg_m);
+          p[e] = ((POLY_MASK >> (i & 7)) & 1) ? ex2_poly(xe) : ex2(xe);
+          ps[i & 7] += p[e];
         }
-        tmem_st32(s_addr + half * 32, pk);
+        pk[c] = pack_bf16x2(p[0], p[1]);
       }
+      tmem_st32(s_addr + half * 32, pk);
       const float lsum = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
       l_run = l_run * corr + lsum;
       tmem_wait_st();
@@ -247,15 +261,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(smem_u32(&p_full[s]));
     }
     // ---------------------------------------------------------------- epilogue
+    // combine the two halves' row sums (the exchange buffer is free: both warps are past their last
+    // max exchange once they meet at this barrier)
+    named_bar(bar_id, 64);
+    xch[half * BM + r] = l_run;
+    named_bar(bar_id, 64);
+    const float l_tot = l_run + xch[(half ^ 1) * BM + r];
     mbar_wait(smem_u32(&pv_done[(n_tiles - 1) & 1]), ((n_tiles - 1) >> 1) & 1);
     tc_fence_after();
-    const float inv = 1.f / l_run;
+    const float inv = 1.f / l_tot;
     const bool row_ok = q < T;
-    __nv_bfloat16* orow = o + (int64_t)q * os + (int64_t)h * D;
+    __nv_bfloat16* orow = o + (int64_t)q * os + (int64_t)h * D + half * (D / 2);
 #pragma unroll 1
-    for (int c = 0; c < D / 32; ++c) {
+    for (int c = 0; c < D / 64; ++c) {
       uint32_t ov[32];
-      tmem_ld32_nowait(lane_addr + C::COL_O + c * 32, ov);
+      tmem_ld32_nowait(lane_addr + C::COL_O + half * (D / 2) + c * 32, ov);
       tmem_wait_ld();
       if (row_ok) {
 #pragma unroll
@@ -269,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-    if (row_ok) lse[(int64_t)h * T + q] = (m_run + __log2f(l_run)) / kLog2e;
+    if (row_ok && half == 0) lse[(int64_t)h * T + q] = (m_run + __log2f(l_tot)) / kLog2e;
   }
   tc_fence_before();
   __syncthreads();
@@ -342,7 +362,6 @@ struct Bwd {
   static constexpr int SM_WARPS = 8;
 };
 
-__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
 template <int D>
 __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)

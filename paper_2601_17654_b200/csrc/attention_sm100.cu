@@ -318,6 +318,8 @@ int fwd_launch(const void* q, const void* k, const void* v, void* o, float* lse,
   int rc;
   if (mode == 0) rc = go(attn_fwd_tc_kernel<D, 0x00>);
   else if (mode == 2) rc = go(attn_fwd_tc_kernel<D, 0x55>);
+  else if (mode == 3) rc = go(attn_fwd_tc_kernel<D, 0x80>);
+  else if (mode == 4) rc = go(attn_fwd_tc_kernel<D, 0x92>);
   else rc = go(attn_fwd_tc_kernel<D, 0x88>);
   if (rc) return rc;
   KPO_LAUNCH_CHECK();

@@ -105,6 +105,14 @@ __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t* r) {
         "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
   asm volatile(
@@ -125,6 +133,11 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
       "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
 }
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tmem_alloc(uint32_t slot_smem_addr, uint32_t cols) {
@@ -139,14 +152,19 @@ __device__ __forceinline__ float ex2(float x) {
   asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// 2^x on the FMA pipe (Cody-Waite split + degree-3 polynomial, max rel. error 8.6e-5 on [0,1)),
-// used for a fraction of the softmax exponentials so the MUFU unit is not the only exp2 engine.
+// 2^x on the FMA / ALU pipes only (no MUFU, FRND or F2I, which share the XU pipe with MUFU.EX2):
+// round-to-nearest through the 1.5 * 2^23 magic constant, f in [-0.5, 0.5], degree-5 polynomial
+// (max rel. error ~2e-7 on [-0.5, 0.5]), exponent added as an integer.  Used for a fraction of the
+// softmax exponentials so the MUFU unit is not the only exp2 engine (measured, tools/ubench_xu.cu:
+// MUFU 16 / clk / SM, this 11.5 / clk / SM, half-half mix 18.4).  Inputs below -126 flush to ~0.
 __device__ __forceinline__ float ex2_poly(float x) {
   x = fmaxf(x, -126.f);
-  const float fi = floorf(x);
-  const float f = x - fi;
-  const float p = fmaf(fmaf(fmaf(0.07707918f, f, 0.22763424f), f, 0.69511687f), f, 1.0f);
-  return __int_as_float(__float_as_int(p) + (static_cast<int>(fi) << 23));
+  const float j = x + 12582912.f;
+  const float f = x - (j - 12582912.f);
+  float p = fmaf(fmaf(fmaf(fmaf(0.0013333558f, f, 0.0096181291f), f, 0.0555041087f), f, 0.2402265070f), f,
+                 0.6931471806f);
+  p = fmaf(p, f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(j) << 23));
 }
 
 // Split UMMA descriptors for the issue loops.  Every tile here is SWIZZLE_128B with SBO = 1024, so

@@ -106,6 +106,27 @@ int kpo_attn_bwd(const void* q, const void* k, const void* v, const void* o, con
                  int64_t dq_stride, int64_t dk_stride, int64_t dv_stride, float scale, int causal,
                  void* workspace, void* stream);
 
+/* ---------------------------------------------------------------- non-partition work */
+/* The work of a microbatch outside its partitions, which the reference costs analytically from
+ * per-microbatch "non_partition_kernels" (reference pkg/src/schedfront/cli.py:171-175,227-241 ->
+ * MicrobatchSpec.non_partition_costs, compose.py:79-102).  Here it is real kernels measured on the
+ * hardware: embedding gather / scatter-add and the fused LM-head cross-entropy (the LM-head GEMMs
+ * are kpo_gemm).  ids / labels are int32 [tokens]. */
+/* out[t,:] = table[ids[t],:] (bf16, [vocab, hidden]); out-of-range ids give a zero row and set
+ * *bad_flag (device int) to 1. */
+int kpo_embedding_fwd(const int32_t* ids, const void* table, void* out, int64_t tokens, int64_t hidden,
+                      int64_t vocab, int* bad_flag, void* stream);
+/* dtable[ids[t],:] += dy[t,:] into an fp32 [vocab, hidden] gradient table (fp32 vector reductions;
+ * repeated ids are summed in arbitrary order).  Out-of-range ids are skipped. */
+int kpo_embedding_bwd(const int32_t* ids, const void* dy, float* dtable, int64_t tokens, int64_t hidden,
+                      int64_t vocab, void* stream);
+/* Fused softmax cross-entropy over bf16 logits [tokens, vocab] (row stride ld elements):
+ * loss[t] = logsumexp(x_t) - x_t[labels[t]] (fp32, natural log), and
+ * dlogits[t,:] = (softmax(x_t) - onehot(labels[t])) * grad_scale in bf16.  dlogits may alias logits.
+ * Rows whose label == ignore_index (or is out of range) get loss 0 and zero gradients. */
+int kpo_cross_entropy(const void* logits, void* dlogits, const int32_t* labels, float* loss, int64_t tokens,
+                      int64_t vocab, int64_t ld, float grad_scale, int ignore_index, void* stream);
+
 /* ---------------------------------------------------------------- SM-budgeted collectives */
 /* A communicator owns one symmetric buffer per rank (IPC-exported) plus per-CTA flag words.
  * world > 1, loopback == 0: one process per GPU; exchange kpo_comm_ipc_handle() blobs (out of band,

@@ -24,10 +24,11 @@ class ModelConfig:
     n_layers: int
     rope_theta: float = 500000.0
     norm_eps: float = 1e-5
+    vocab: int = 128256  # Llama-3 tokenizer; GPT preset: 50257 padded to a multiple of 64
 
 
 PRESETS = {
-    "gpt-h1024": ModelConfig("gpt-h1024", 1024, 4096, 16, 16, 64, 24, rope_theta=10000.0),
+    "gpt-h1024": ModelConfig("gpt-h1024", 1024, 4096, 16, 16, 64, 24, rope_theta=10000.0, vocab=50304),
     "llama-3.2-3b": ModelConfig("llama-3.2-3b", 3072, 8192, 24, 8, 128, 28),
     "llama-3-8b": ModelConfig("llama-3-8b", 4096, 14336, 32, 8, 128, 32),
     "llama-3-70b": ModelConfig("llama-3-70b", 8192, 28672, 64, 8, 128, 80),

@@ -169,3 +169,35 @@ def attn_bwd(q, k, v, o, dout, lse, dq, dk, dv, T, hq, hkv, d, scale, workspace,
     _lib.call("kpo_attn_bwd", _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(dout), _ptr(lse), _ptr(dq), _ptr(dk),
               _ptr(dv), T, hq, hkv, d, q.stride(0), k.stride(0), v.stride(0), o.stride(0), dq.stride(0),
               dk.stride(0), dv.stride(0), ctypes.c_float(scale), int(causal), _ptr(workspace), _stream(stream))
+
+
+# ------------------------------------------------------------------ non-partition work (nonpart.cu)
+def embedding_fwd(ids: torch.Tensor, table: torch.Tensor, out: torch.Tensor, bad_flag: torch.Tensor,
+                  stream=None) -> None:
+    """out[t] = table[ids[t]]; ids int32 [T], table bf16 [V, h]; bad_flag int32 [1] set on bad ids."""
+    _need_cuda(ids, table, out, bad_flag)
+    if ids.dtype != torch.int32 or bad_flag.dtype != torch.int32:
+        raise ValueError("embedding ids / bad_flag must be int32")
+    _lib.call("kpo_embedding_fwd", _ptr(ids), _ptr(table), _ptr(out), ids.numel(), table.shape[1], table.shape[0],
+              _ptr(bad_flag), _stream(stream))
+
+
+def embedding_bwd(ids: torch.Tensor, dy: torch.Tensor, dtable: torch.Tensor, stream=None) -> None:
+    """dtable[ids[t]] += dy[t] (fp32 gradient table [V, h])."""
+    _need_cuda(ids, dy, dtable)
+    if ids.dtype != torch.int32 or dtable.dtype != torch.float32:
+        raise ValueError("embedding_bwd: ids int32, dtable fp32")
+    _lib.call("kpo_embedding_bwd", _ptr(ids), _ptr(dy), _ptr(dtable), ids.numel(), dtable.shape[1],
+              dtable.shape[0], _stream(stream))
+
+
+def cross_entropy(logits: torch.Tensor, labels: torch.Tensor, loss: torch.Tensor, dlogits: torch.Tensor,
+                  grad_scale: float = 1.0, ignore_index: int = -100, stream=None) -> None:
+    """Fused softmax cross-entropy: loss[t] (fp32) and dlogits = (softmax - onehot) * grad_scale (bf16,
+    may be `logits` itself)."""
+    _need_cuda(logits, labels, loss, dlogits)
+    if labels.dtype != torch.int32:
+        raise ValueError("labels must be int32")
+    T, V = logits.shape
+    _lib.call("kpo_cross_entropy", _ptr(logits), _ptr(dlogits), _ptr(labels), _ptr(loss), T, V, logits.stride(0),
+              ctypes.c_float(grad_scale), ignore_index, _stream(stream))

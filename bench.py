@@ -124,6 +124,54 @@ def run_reference(args):
     return 0
 
 
+# ---------------------------------------------------------------------------- microbatch composition
+def run_microbatch(args, wl, eng, gpu, layer, per_part, hbm, tf_sust, torch):
+    from paper_2601_17654_b200.device import ProfilingProtocol
+    from paper_2601_17654_b200.nonpartition import NonPartitionWork, measure_costs, unit_times
+
+    work = NonPartitionWork(wl, eng.device)
+    proto = ProfilingProtocol(warmup_s=0.2, window_s=args.sweep_window, cooldown_s=0.0)
+    costs = {n: measure_costs(eng, work.programs[n], [gpu.f_max_mhz], proto) for n in ("np_fwd", "np_bwd")}
+    ut = unit_times(work)
+    units = {}
+    for name in ("np_fwd", "np_bwd"):
+        for u in work.programs[name].units:
+            ms = ut[u.name]
+            if u.kind == "gemm":
+                units[u.name] = {"ms": round(ms, 4), "tflops": round(u.spec.flops / ms / 1e9, 1),
+                                 "frac": round(u.spec.flops / ms / 1e9 / tf_sust, 4)}
+            else:
+                units[u.name] = {"ms": round(ms, 4), "gbs": round(u.spec.bytes / ms / 1e6, 1),
+                                 "frac": round(u.spec.bytes / ms / 1e6 / hbm, 4)}
+    out = {"non_partition_costs": {n: {str(f): [round(t, 4), round(e, 4)] for f, (t, e) in c.items()}
+                                   for n, c in costs.items()},
+           "non_partition_units": units, "n_layers": wl.model.n_layers, "vocab": wl.model.vocab}
+    del work
+    torch.cuda.empty_cache()
+    try:
+        ref = os.path.join(ROOT, "baseline", "_ref")
+        if os.path.isdir(ref) and ref not in sys.path:
+            sys.path.append(ref)
+        from schedfront.compose import MicrobatchSpec, build_per_frequency_frontiers, microbatch_frontier
+    except ImportError:
+        out["composition"] = "skipped: reference package (baseline/_ref) not importable on this box"
+        return out
+    per_freq = build_per_frequency_frontiers({n: [(c, m) for c, m in rows] for n, rows in per_part.items()})
+    L = wl.model.n_layers
+    comp = {}
+    for mb, blocks, npn in (("fwd", ("fwd_attn", "fwd_mlp"), "np_fwd"), ("bwd", ("bwd_mlp", "bwd_attn"), "np_bwd")):
+        seq = [f"{blk}{b}" for blk in blocks for b in range(wl.nanobatches)] * L
+        spec = MicrobatchSpec(f"{wl.model.name}-{mb}", tuple(seq), costs[npn])
+        front = microbatch_frontier(spec, per_freq, gpu.p_static_w)
+        comp[mb] = [{"time_ms": round(p.time_ms, 3), "energy_j": round(p.energy_j, 3),
+                     "choices": {t: c.timing.encode() + f"@{c.sm_alloc}" for t, c in p.payload.choices}}
+                    for p in front.points]
+    out["composition"] = {"api": "schedfront.compose.microbatch_frontier (reference, unmodified)",
+                          "microbatch": f"{L} layers x partitions + measured non-partition work, 1 pipeline stage",
+                          "frontiers": comp}
+    return out
+
+
 # ---------------------------------------------------------------------------- GPU arm
 def run_kpo(args):
     import torch
@@ -338,6 +386,13 @@ def run_kpo(args):
         frontier["note"] = ("frequency fixed: NVML locked clocks NOT_SUPPORTED on this pool (power.py); sweep over "
                             "comm SM budget x launch timing, windows of " + str(args.sweep_window) + " s")
 
+    # ------------------------------------------------ non-partition work + microbatch composition
+    # (SURVEY §8f item 1): embedding / final norm / LM head / loss measured on the hardware, and
+    # the reference's own microbatch_frontier composing the measured partition candidates with it
+    microbatch = None
+    if not args.no_sweep:
+        microbatch = run_microbatch(args, wl, eng, gpu, layer, per_part, hbm, tf_sust, torch)
+
     # ------------------------------------------------ CPU baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -394,6 +449,7 @@ def run_kpo(args):
             "iteration_roofline": iter_roofline,
             "comm": {"mode": "loopback (HBM)" if world == 1 else "cuda-ipc p2p (NVLink)", "units": comm_rows},
             "frontier": frontier,
+            "microbatch": microbatch,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_s, "unit": "s/iter", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "api": "LayerRunner.step_host_async x K + drain(): pinned host x/dy in, dx out, copies "

@@ -155,3 +155,22 @@ def microbatch_spec(name: str, partition_sequence, costs: dict[float, tuple[floa
     if spec_cls is None:
         from schedfront.compose import MicrobatchSpec as spec_cls  # noqa: N813
     return spec_cls(name, tuple(partition_sequence), dict(costs))
+
+
+def unit_times(work: NonPartitionWork, iters: int = 3, stream=None) -> dict[str, float]:
+    """Average per-unit durations (ms) with CUDA events on the launching stream."""
+    st = stream or torch.cuda.Stream(work.device)
+    marks = []
+    for _ in range(iters):
+        for name in ("np_fwd", "np_bwd"):
+            for u in work.programs[name].units:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                u.fn(st)
+                e1.record(st)
+                marks.append((u.name, e0, e1))
+    st.synchronize()
+    out: dict[str, float] = {}
+    for n, e0, e1 in marks:
+        out[n] = out.get(n, 0.0) + e0.elapsed_time(e1) / iters
+    return out

@@ -96,7 +96,9 @@ __device__ __forceinline__ void cta_slice(size_t n, size_t& b, size_t& e) {
 }
 
 constexpr int kCommThreads = 512;
-constexpr int kUnroll = 4;
+// 16 x 16 B loads in flight per thread = 128 KB per CTA: a CTA's copy rate is in-flight bytes /
+// latency (measured with 4 in flight: ~28 GB/s per CTA on loopback HBM, i.e. latency-bound)
+constexpr int kUnroll = 16;
 
 // Copy n 16-byte vectors src -> dst, kUnroll loads in flight per thread.
 __device__ __forceinline__ void copy_vecs(uint4* __restrict__ dst, const uint4* __restrict__ src, size_t b,
@@ -105,22 +107,47 @@ __device__ __forceinline__ void copy_vecs(uint4* __restrict__ dst, const uint4* 
   for (; i + (kUnroll - 1) * kCommThreads < e; i += kUnroll * kCommThreads) {
     uint4 v[kUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) v[u] = ld_volatile_v4(src + i + u * kCommThreads);
+    for (int u = 0; u < kUnroll; ++u) v[u] = ld_weak_v4(src + i + u * kCommThreads);
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) st_v4(dst + i + u * kCommThreads, v[u]);
   }
-  for (; i < e; i += kCommThreads) st_v4(dst + i, ld_volatile_v4(src + i));
+  for (; i < e; i += kCommThreads) st_v4(dst + i, ld_weak_v4(src + i));
 }
 
 // dst[i] = sum_p src_p[i] (bf16, fp32 accumulate, p = 0..world-1 in order); optional 2nd dst.
 template <int W>
 __device__ __forceinline__ void reduce_vecs(uint4* __restrict__ dst, uint4* __restrict__ dst2,
                                             const CommArgs& a, size_t src_off_bytes, size_t b, size_t e) {
-  for (size_t i = b + threadIdx.x; i < e; i += kCommThreads) {
+  // R independent vectors per thread per iteration: R * W loads in flight
+  constexpr int R = W <= 2 ? 8 : (W <= 4 ? 4 : 2);
+  size_t i = b + threadIdx.x;
+  for (; i + (R - 1) * kCommThreads < e; i += R * kCommThreads) {
+    uint4 v[R][W];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int p = 0; p < W; ++p)
+        v[r][p] = ld_weak_v4(reinterpret_cast<const uint4*>(a.peer[p] + src_off_bytes) + i + r * kCommThreads);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      float acc[8], f[8];
+      unpack8(v[r][0], acc);
+#pragma unroll
+      for (int p = 1; p < W; ++p) {
+        unpack8(v[r][p], f);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] += f[j];
+      }
+      const uint4 o = pack8(acc);
+      st_v4(dst + i + r * kCommThreads, o);
+      if (dst2) st_v4(dst2 + i + r * kCommThreads, o);
+    }
+  }
+  for (; i < e; i += kCommThreads) {
     uint4 v[W];
 #pragma unroll
     for (int p = 0; p < W; ++p)
-      v[p] = ld_volatile_v4(reinterpret_cast<const uint4*>(a.peer[p] + src_off_bytes) + i);
+      v[p] = ld_weak_v4(reinterpret_cast<const uint4*>(a.peer[p] + src_off_bytes) + i);
     float acc[8], f[8];
     unpack8(v[0], acc);
 #pragma unroll

@@ -110,3 +110,36 @@ def test_measured_costs_feed_reference_composition(cuda, schedfront):
     pts = list(front.points)
     assert len(pts) == 1
     assert abs(pts[0].time_ms - (1.0 + t)) < 1e-9 and abs(pts[0].payload.dyn_energy_j - (2.0 + e)) < 1e-9
+
+
+def test_clock_controller_drives_real_microbatches(cuda):
+    """freqctl on hardware: the non-partition programs as 'microbatches' with assigned clocks.  Where
+    NVML refuses locked clocks (this pool) the sequence runs at the current clock and no switch is
+    recorded; where it permits them every frequency change is one recorded switch."""
+    from paper_2601_17654_b200 import b200_model
+    from paper_2601_17654_b200.engine import Engine
+    from paper_2601_17654_b200.freqctl import MicrobatchClockController
+    from paper_2601_17654_b200.model import ModelConfig, Workload
+    from paper_2601_17654_b200.nonpartition import NonPartitionWork
+    m = ModelConfig("tiny", hidden=512, ffn=1024, n_heads=8, n_kv_heads=2, head_dim=64, n_layers=1, vocab=8192)
+    npw = NonPartitionWork(Workload(m, "fsdp", 2, tokens=256), cuda)
+    eng = Engine(npw.programs, b200_model(), device=cuda, clock_control=True)
+    progs = [npw.programs["np_fwd"], npw.programs["np_bwd"]] * 2
+    st = eng.exec.compute
+
+    def enqueue(i):
+        for u in progs[i].units:
+            u.fn(st)
+        ev = torch.cuda.Event()
+        ev.record(st)
+        return ev
+
+    f0 = eng.gpu.f_max_mhz
+    freqs = [f0, f0 - 300.0, f0 - 300.0, f0]
+    res = MicrobatchClockController(eng.freq, eng.nvml.sm_clock_mhz).run(freqs, enqueue, "async")
+    eng.close()
+    if eng.freq.available:
+        assert [s.index for s in res.switches] == [0, 1, 3]
+    else:
+        assert res.switches == [] and res.clock_control.startswith("unavailable")
+    assert res.total_s > 0

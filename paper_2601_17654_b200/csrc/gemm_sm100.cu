@@ -179,12 +179,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * CF::STAGE_BYTES);
           const uint32_t sb = sa + CF::A_BYTES;
+          static_assert(A_SBO == 1024 && B_SBO == 1024, "split descriptors assume SBO 1024 / SWIZZLE_128B");
+          const uint32_t a_lo = desc_lo(sa, A_LBO), b_lo = desc_lo(sb, B_LBO);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t da = smem_desc(sa + k * A_KSTEP, A_LBO, A_SBO);
-            const uint64_t db = smem_desc(sb + k * B_KSTEP, B_LBO, B_SBO);
-            tc_mma(d_tmem, da, db, IDESC, (kb | k) != 0);
-          }
+          for (int k = 0; k < BK / 16; ++k)
+            tc_mma_lo(d_tmem, a_lo + k * (A_KSTEP >> 4), b_lo + k * (B_KSTEP >> 4), IDESC, (kb | k) != 0);
           tc_commit(smem_u32(&empty[stage]));
           if (++stage == STAGES) {
             stage = 0;
@@ -431,11 +430,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + stage * CF::STAGE_BYTES);
           const uint32_t sb = sa + CF::A_BYTES;
+          static_assert(A_SBO == 1024 && B_SBO == 1024, "split descriptors assume SBO 1024 / SWIZZLE_128B");
+          const uint32_t a_lo = desc_lo(sa, A_LBO), b_lo = desc_lo(sb, B_LBO);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            tc_mma_pair(d_tmem, smem_desc(sa + k * A_KSTEP, A_LBO, A_SBO), smem_desc(sb + k * B_KSTEP, B_LBO, B_SBO),
-                        IDESC, (kb | k) != 0);
-          }
+          for (int k = 0; k < BK / 16; ++k)
+            tc_mma_pair_lo(d_tmem, a_lo + k * (A_KSTEP >> 4), b_lo + k * (B_KSTEP >> 4), IDESC, (kb | k) != 0);
           tc_commit_pair(smem_u32(&empty[stage]));
           if (++stage == STAGES) {
             stage = 0;

@@ -193,6 +193,17 @@ __device__ __forceinline__ void tc_mma_ts_lo(uint32_t tmem_d, uint32_t tmem_a, u
       "r"(tmem_a), "r"(b_lo), "r"(idesc), "r"(acc), "n"(kDescHiSw128));
 }
 
+__device__ __forceinline__ void tc_mma_pair_lo(uint32_t tmem_d, uint32_t a_lo, uint32_t b_lo, uint32_t idesc,
+                                               uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 da, db;\n\t"
+      "mov.b64 da, {%1, %5};\n\t"
+      "mov.b64 db, {%2, %5};\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(acc), "n"(kDescHiSw128));
+}
+
 // UMMA instruction descriptor: bf16 x bf16 -> f32, M x N, operand majorness.
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool b_mn) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |

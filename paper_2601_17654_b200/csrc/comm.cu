@@ -14,7 +14,7 @@
 //   * synchronisation is per CTA: CTA c of every rank exchanges epoch flags with CTA c of every
 //     peer (release/acquire at system scope), so no grid-wide barrier is needed and the epoch
 //     counters live on the device — a captured CUDA graph can be replayed indefinitely.
-#include "common.cuh"
+#include "sm100.cuh"
 #include <vector>
 #include <cstring>
 
@@ -45,8 +45,18 @@ struct CommArgs {
   uint32_t* peer_flags[KPO_MAX_WORLD];
   uint32_t* epoch;
   int rank, world, loopback;
+  int bulk;                    // copy phases through TMA bulk copies (else 16-byte LSU copies)
   int64_t* trace;              // [ncta*4] or null
 };
+
+// TMA bulk copies beat the 16-byte LSU copies from 0.5 MB per CTA up (measured A/B with
+// tools/comm_ab.sh: all-gather +8% at 1 MB per CTA, +27-38% at 4-16 MB per CTA; all-reduce +10-22%);
+// tiny messages keep the LSU path (no ring fill latency).  KPO_COMM_BULK=0/1 forces either path.
+inline int choose_bulk(size_t bytes_per_cta) {
+  const char* env = getenv("KPO_COMM_BULK");
+  if (env) return atoi(env) != 0;
+  return bytes_per_cta >= ((size_t)256 << 10);
+}
 
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -114,6 +124,77 @@ __device__ __forceinline__ void copy_vecs(uint4* __restrict__ dst, const uint4* 
   for (; i < e; i += kCommThreads) st_v4(dst + i, ld_weak_v4(src + i));
 }
 
+// ---------------------------------------------------------------- TMA bulk copies
+// Copies move through a shared-memory ring with cp.async.bulk (global -> shared, completing on an
+// mbarrier; shared -> global, tracked by a bulk group), issued by one thread.  Measured per CTA
+// (tools/ubench_copy.cu): ~50 GB/s against ~35 GB/s with 16-byte loads / stores, so a collective
+// needs fewer SMs for the same bandwidth.  The ring is the CTA's dynamic shared memory, which it
+// reserves anyway to own its SM.
+constexpr int kBulkChunk = 16384;
+constexpr int kBulkStages = 12;
+struct BulkSeg {
+  char* dst;
+  const char* src;
+  size_t bytes;
+};
+
+// Thread 0 only.  Copies segs[0..n) (bytes multiples of 16, 16-byte aligned) through the ring.
+__device__ void bulk_copy_segs(const BulkSeg* segs, int n, uint8_t* ring, uint64_t* full) {
+  using namespace kpo::sm100;
+  // chunk enumeration over the segments
+  int seg = 0;
+  size_t off = 0;
+  auto next = [&](const char*& src, char*& dst, uint32_t& len) -> bool {
+    while (seg < n && off >= segs[seg].bytes) {
+      ++seg;
+      off = 0;
+    }
+    if (seg >= n) return false;
+    const size_t rem = segs[seg].bytes - off;
+    len = (uint32_t)(rem < (size_t)kBulkChunk ? rem : (size_t)kBulkChunk);
+    src = segs[seg].src + off;
+    dst = segs[seg].dst + off;
+    off += len;
+    return true;
+  };
+  char* dsts[kBulkStages];
+  uint32_t lens[kBulkStages];
+  int loaded = 0;
+  // async-proxy reads must observe the generic-proxy writes the acquire barrier made visible
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  for (; loaded < kBulkStages; ++loaded) {
+    const char* src;
+    if (!next(src, dsts[loaded], lens[loaded])) break;
+    mbar_arrive_expect_tx(smem_u32(&full[loaded]), lens[loaded]);
+    bulk_load(smem_u32(ring + loaded * kBulkChunk), src, lens[loaded], smem_u32(&full[loaded]));
+  }
+  for (int c = 0; c < loaded; ++c) {
+    const int st = c % kBulkStages;
+    mbar_wait(smem_u32(&full[st]), (uint32_t)(c / kBulkStages) & 1u);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dsts[st]),
+                 "r"(smem_u32(ring + st * kBulkChunk)), "r"(lens[st])
+                 : "memory");
+    bulk_commit();
+    // refill the stage of chunk c-1 once its store has read shared memory (at most chunk c's
+    // store group may still be reading)
+    if (c >= 1) {
+      const int ps = (c - 1) % kBulkStages;
+      const char* src;
+      char* d;
+      uint32_t len;
+      if (next(src, d, len)) {
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        dsts[ps] = d;
+        lens[ps] = len;
+        mbar_arrive_expect_tx(smem_u32(&full[ps]), len);
+        bulk_load(smem_u32(ring + ps * kBulkChunk), src, len, smem_u32(&full[ps]));
+        ++loaded;
+      }
+    }
+  }
+  bulk_wait0();  // every store performed (and every load consumed) before the CTA's release barrier
+}
+
 // dst[i] = sum_p src_p[i] (bf16, fp32 accumulate, p = 0..world-1 in order); optional 2nd dst.
 template <int W>
 __device__ __forceinline__ void reduce_vecs(uint4* __restrict__ dst, uint4* __restrict__ dst2,
@@ -176,9 +257,22 @@ __device__ __forceinline__ void reduce_vecs_dyn(uint4* __restrict__ dst, uint4* 
   }
 }
 
+__shared__ __align__(8) uint64_t bulk_bars[kBulkStages];
+__device__ __forceinline__ uint8_t* bulk_ring() {
+  extern __shared__ __align__(1024) uint8_t comm_dyn_smem[];
+  return comm_dyn_smem;
+}
+__device__ __forceinline__ void bulk_init() {
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kBulkStages; ++i) kpo::sm100::mbar_init(kpo::sm100::smem_u32(&bulk_bars[i]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+}
+
 __global__ void __launch_bounds__(kCommThreads, 1)
     all_gather_kernel(CommArgs a, size_t sym_off, char* __restrict__ out, size_t bytes_per_rank) {
   trace_enter(a);
+  bulk_init();
   __shared__ uint32_t base_epoch;
   if (threadIdx.x == 0) base_epoch = a.epoch[blockIdx.x];
   __syncthreads();
@@ -187,10 +281,21 @@ __global__ void __launch_bounds__(kCommThreads, 1)
   const size_t nvec = bytes_per_rank / 16;
   size_t b, e;
   cta_slice(nvec, b, e);
-  for (int k = 0; k < a.world; ++k) {
-    const int p = (a.rank + k) % a.world;  // stagger peers across ranks
-    copy_vecs(reinterpret_cast<uint4*>(out + (size_t)p * bytes_per_rank),
-              reinterpret_cast<const uint4*>(a.peer[p] + sym_off), b, e);
+  if (a.bulk) {
+    if (threadIdx.x == 0 && e > b) {
+      BulkSeg segs[KPO_MAX_WORLD];
+      for (int k = 0; k < a.world; ++k) {
+        const int p = (a.rank + k) % a.world;  // stagger peers across ranks
+        segs[k] = {out + (size_t)p * bytes_per_rank + b * 16, a.peer[p] + sym_off + b * 16, (e - b) * 16};
+      }
+      bulk_copy_segs(segs, a.world, bulk_ring(), bulk_bars);
+    }
+  } else {
+    for (int k = 0; k < a.world; ++k) {
+      const int p = (a.rank + k) % a.world;  // stagger peers across ranks
+      copy_vecs(reinterpret_cast<uint4*>(out + (size_t)p * bytes_per_rank),
+                reinterpret_cast<const uint4*>(a.peer[p] + sym_off), b, e);
+    }
   }
   cta_barrier(a, e0 + 2);  // nobody reuses its shard buffer before every peer has read it
   if (threadIdx.x == 0) a.epoch[blockIdx.x] = e0 + 2;
@@ -217,6 +322,7 @@ __global__ void __launch_bounds__(kCommThreads, 1)
 __global__ void __launch_bounds__(kCommThreads, 1)
     all_reduce_kernel(CommArgs a, size_t sym_off, size_t stage_off, char* __restrict__ out, size_t count) {
   trace_enter(a);
+  bulk_init();
   __shared__ uint32_t base_epoch;
   if (threadIdx.x == 0) base_epoch = a.epoch[blockIdx.x];
   __syncthreads();
@@ -232,11 +338,23 @@ __global__ void __launch_bounds__(kCommThreads, 1)
                   reinterpret_cast<uint4*>(out + my_chunk_bytes), a, sym_off + my_chunk_bytes, b, e);
   cta_barrier(a, e0 + 2);  // slice blockIdx.x of every rank's chunk is reduced
   // phase 2: gather the other ranks' reduced chunks (same slice) from their stage buffers
-  for (int k = 1; k < a.world; ++k) {
-    const int p = (a.rank + k) % a.world;
-    const size_t off = (size_t)p * chunk * 2;
-    copy_vecs(reinterpret_cast<uint4*>(out + off),
-              reinterpret_cast<const uint4*>(a.peer[p] + stage_off + off), b, e);
+  if (a.bulk) {
+    if (threadIdx.x == 0 && e > b) {
+      BulkSeg segs[KPO_MAX_WORLD];
+      for (int k = 1; k < a.world; ++k) {
+        const int p = (a.rank + k) % a.world;
+        const size_t off = (size_t)p * chunk * 2 + b * 16;
+        segs[k - 1] = {out + off, a.peer[p] + stage_off + off, (e - b) * 16};
+      }
+      bulk_copy_segs(segs, a.world - 1, bulk_ring(), bulk_bars);
+    }
+  } else {
+    for (int k = 1; k < a.world; ++k) {
+      const int p = (a.rank + k) % a.world;
+      const size_t off = (size_t)p * chunk * 2;
+      copy_vecs(reinterpret_cast<uint4*>(out + off),
+                reinterpret_cast<const uint4*>(a.peer[p] + stage_off + off), b, e);
+    }
   }
   cta_barrier(a, e0 + 3);
   if (threadIdx.x == 0) a.epoch[blockIdx.x] = e0 + 3;
@@ -388,6 +506,7 @@ static int prep_args(kpo_comm* c, int ncta, CommArgs& a) {
   }
   KPO_CHECK_ARG(ncta >= 1 && ncta <= kpo_comm_max_ctas(c), "collective: ncta %d out of [1, %d]", ncta,
                 kpo_comm_max_ctas(c));
+  a.bulk = 0;
   for (int p = 0; p < KPO_MAX_WORLD; ++p) {
     a.peer[p] = p < c->world ? c->peer[p] : nullptr;
     a.peer_flags[p] = p < c->world ? (uint32_t*)(c->peer[p] + c->flag_off) : nullptr;
@@ -441,6 +560,7 @@ extern "C" int kpo_all_gather(kpo_comm* c, size_t sym_off, void* out, size_t byt
   if (st) return st;
   KPO_CHECK_ARG(out && bytes_per_rank % 16 == 0 && sym_off % 16 == 0, "all_gather: 16B alignment required");
   KPO_CHECK_ARG(sym_off + bytes_per_rank <= c->sym_bytes, "all_gather: source exceeds symmetric buffer");
+  a.bulk = choose_bulk(bytes_per_rank * (size_t)c->world / (size_t)ncta);
   return launch_comm(c, all_gather_kernel, ncta, (cudaStream_t)stream, a, sym_off, (char*)out, bytes_per_rank);
 }
 
@@ -464,5 +584,6 @@ extern "C" int kpo_all_reduce(kpo_comm* c, size_t sym_off, size_t stage_off, voi
                 "all_reduce: buffers exceed symmetric buffer");
   KPO_CHECK_ARG(stage_off >= sym_off + count * 2 || sym_off >= stage_off + count * 2,
                 "all_reduce: stage and input regions overlap");
+  a.bulk = choose_bulk(count * 2 / (size_t)ncta);
   return launch_comm(c, all_reduce_kernel, ncta, (cudaStream_t)stream, a, sym_off, stage_off, (char*)out, count);
 }

@@ -24,8 +24,20 @@ def _bits(t):
     return t.cpu().view(torch.int16).numpy().view(np.uint16)
 
 
-@pytest.mark.parametrize("count,ncta", [(8, 1), (4096, 3), (1 << 20, 16), (123456 * 8, 148)])
-def test_all_gather_bitexact(cuda, count, ncta):
+@pytest.fixture(params=["auto", "lsu", "bulk"])
+def copy_path(request, monkeypatch):
+    """Copy engine of the gather phases: size-based choice, forced 16-byte LSU, forced TMA bulk."""
+    if request.param == "lsu":
+        monkeypatch.setenv("KPO_COMM_BULK", "0")
+    elif request.param == "bulk":
+        monkeypatch.setenv("KPO_COMM_BULK", "1")
+    else:
+        monkeypatch.delenv("KPO_COMM_BULK", raising=False)
+    return request.param
+
+
+@pytest.mark.parametrize("count,ncta", [(8, 1), (4096, 3), (1 << 20, 16), (123456 * 8, 148), (3 << 20, 2)])
+def test_all_gather_bitexact(cuda, count, ncta, copy_path):
     c = _comm(cuda, count * 2 + 4096)
     reg = c.alloc(count * 2)
     shards = [_rand_bf16(count, p) for p in range(W)]
@@ -55,8 +67,8 @@ def test_reduce_scatter_bitexact(cuda, count, ncta):
     c.close()
 
 
-@pytest.mark.parametrize("count,ncta", [(W * 8, 1), (W * 4096, 7), (4096 * 3072, 24)])
-def test_all_reduce_bitexact(cuda, count, ncta):
+@pytest.mark.parametrize("count,ncta", [(W * 8, 1), (W * 4096, 7), (4096 * 3072, 24), (4096 * 3072, 2)])
+def test_all_reduce_bitexact(cuda, count, ncta, copy_path):
     c = _comm(cuda, 2 * count * 2 + 8192)
     src = c.alloc(count * 2)
     stage = c.alloc(count * 2)

@@ -30,7 +30,7 @@ __global__ void __launch_bounds__(32, 1) copy_tma(const char* __restrict__ src, 
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   const int nchunks = (int)((e > b ? e - b : 0) / CHUNK);
   // prologue: fill the ring
-  for (int c = 0; c < STAGES && c < nchunks; ++c) {
+  for (int c = 0; c < STAGES - 1 && c < nchunks; ++c) {
     mbar_arrive_expect_tx(smem_u32(&bar[c]), CHUNK);
     bulk_load(smem_u32(smem + c * CHUNK), src + b + (size_t)c * CHUNK, CHUNK, smem_u32(&bar[c]));
   }
@@ -41,13 +41,19 @@ __global__ void __launch_bounds__(32, 1) copy_tma(const char* __restrict__ src, 
                  "r"(smem_u32(smem + s * CHUNK)), "r"(CHUNK)
                  : "memory");
     bulk_commit();
-    const int nc = c + STAGES;
-    if (nc < nchunks) {
-      // the stage is refilled once its store has read the shared memory
-      asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(STAGES - 1) : "memory");
-      // (conservative: waits until at most STAGES-1 stores are pending, i.e. this stage's is done)
-      mbar_arrive_expect_tx(smem_u32(&bar[s]), CHUNK);
-      bulk_load(smem_u32(smem + s * CHUNK), src + b + (size_t)nc * CHUNK, CHUNK, smem_u32(&bar[s]));
+    // refill the stage of chunk c-1 (its store was committed one iteration ago): at most one store
+    // group (chunk c's) may still be reading shared memory
+    const int pc = c - 1, nc = pc + STAGES;
+    if (c == 0 && STAGES - 1 < nchunks) {  // last prologue chunk goes into the one free stage
+      mbar_arrive_expect_tx(smem_u32(&bar[STAGES - 1]), CHUNK);
+      bulk_load(smem_u32(smem + (STAGES - 1) * CHUNK), src + b + (size_t)(STAGES - 1) * CHUNK, CHUNK,
+                smem_u32(&bar[STAGES - 1]));
+    }
+    if (pc >= 0 && nc < nchunks) {
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      const int ps = pc % STAGES;
+      mbar_arrive_expect_tx(smem_u32(&bar[ps]), CHUNK);
+      bulk_load(smem_u32(smem + ps * CHUNK), src + b + (size_t)nc * CHUNK, CHUNK, smem_u32(&bar[ps]));
     }
   }
   bulk_wait0();
@@ -73,7 +79,7 @@ int main() {
     cudaEventElapsedTime(&ms, e0, e1);
     return ms / 5;
   };
-  constexpr int CH = 16384, ST = 12;
+  constexpr int CH = 16384, ST = 13;
   cudaFuncSetAttribute(copy_tma<CH, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, CH * ST);
   cudaFuncSetAttribute(copy_lsu, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   for (int g : {1, 4, 8, 16, 32, 64, 148}) {
@@ -81,6 +87,19 @@ int main() {
     float t = timeit([&] { copy_tma<CH, ST><<<g, 32, CH * ST>>>(src, dst, bytes); });
     printf("ctas %3d  lsu %7.1f GB/s (%.1f per CTA)   tma-bulk %7.1f GB/s (%.1f per CTA)\n", g, bytes / a / 1e6,
            bytes / a / 1e6 / g, bytes / t / 1e6, bytes / t / 1e6 / g);
+  }
+  // verify the last TMA copy
+  cudaMemset(dst, 0, bytes);
+  {
+    unsigned char* h = (unsigned char*)malloc(bytes);
+    for (size_t i = 0; i < bytes; ++i) h[i] = (unsigned char)(i * 131 + 7);
+    cudaMemcpy(src, h, bytes, cudaMemcpyHostToDevice);
+    copy_tma<CH, ST><<<16, 32, CH * ST>>>(src, dst, bytes);
+    unsigned char* g = (unsigned char*)malloc(bytes);
+    cudaMemcpy(g, dst, bytes, cudaMemcpyDeviceToHost);
+    size_t bad = 0;
+    for (size_t i = 0; i < bytes; ++i) bad += g[i] != h[i];
+    printf("tma copy verify: %zu bad bytes\n", bad);
   }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;

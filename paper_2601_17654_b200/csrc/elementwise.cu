@@ -177,6 +177,107 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Fused single-pass backward for rows of 256*NV columns (hidden 1024..4096): each warp keeps its row
+// of x and dy in registers (2*NV uint4 per lane), computes dx, and accumulates dgamma for its columns
+// over the rows it owns; the CTA's 4 warps reduce their dgamma through shared memory into one fp32
+// partial row per CTA.  x and dy are read from HBM once (the split dx + dgamma kernels read them
+// twice).  Every warp owns exactly `rows_per_warp` consecutive rows.
+template <int NV>
+__global__ void __launch_bounds__(128)
+    rmsnorm_bwd_fused(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+                      const __nv_bfloat16* __restrict__ w, const float* __restrict__ rstd,
+                      const __nv_bfloat16* __restrict__ dres, __nv_bfloat16* __restrict__ dx,
+                      float* __restrict__ dw_partial, int64_t rows, int rows_per_warp) {
+  constexpr int cols = NV * 256;
+  extern __shared__ float red[];  // [4 warps][cols] dgamma accumulators (each warp owns its row)
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t r0 = ((int64_t)blockIdx.x * 4 + wid) * rows_per_warp;
+  float* acc = red + wid * cols;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    float4* a4 = reinterpret_cast<float4*>(acc + (lane + 32 * i) * 8);
+    a4[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    a4[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const uint4* wr = reinterpret_cast<const uint4*>(w);
+  for (int k = 0; k < rows_per_warp; ++k) {
+    const int64_t row = r0 + k;
+    if (row >= rows) break;
+    const uint4* xr = reinterpret_cast<const uint4*>(x + row * cols);
+    const uint4* dyr = reinterpret_cast<const uint4*>(dy + row * cols);
+    uint4 xv[NV], dv[NV];  // the row stays packed in registers (bf16)
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      xv[i] = ld_nc_v4(xr + lane + 32 * i);
+      dv[i] = ld_nc_v4(dyr + lane + 32 * i);
+    }
+    const float r = rstd[row];
+    float dot = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      float a[8], b[8], g[8];
+      unpack8(xv[i], a);
+      unpack8(dv[i], b);
+      unpack8(wr[lane + 32 * i], g);
+      float4* a4 = reinterpret_cast<float4*>(acc + (lane + 32 * i) * 8);
+      float4 p = a4[0], q = a4[1];
+      p.x += b[0] * a[0] * r; p.y += b[1] * a[1] * r; p.z += b[2] * a[2] * r; p.w += b[3] * a[3] * r;
+      q.x += b[4] * a[4] * r; q.y += b[5] * a[5] * r; q.z += b[6] * a[6] * r; q.w += b[7] * a[7] * r;
+      a4[0] = p;
+      a4[1] = q;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) dot += g[j] * b[j] * a[j];
+    }
+    dot = warp_sum(dot);
+    const float c = dot * r * r * r / (float)cols;
+    uint4* dxr = reinterpret_cast<uint4*>(dx + row * cols);
+    const uint4* dresr = dres ? reinterpret_cast<const uint4*>(dres + row * cols) : nullptr;
+    // opaque redefinition: the second pass unpacks the packed row again instead of keeping the
+    // unpacked floats of the first pass alive (which would not fit in registers for NV >= 12)
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+      asm volatile("" : "+r"(xv[i].x), "+r"(xv[i].y), "+r"(xv[i].z), "+r"(xv[i].w), "+r"(dv[i].x), "+r"(dv[i].y),
+                   "+r"(dv[i].z), "+r"(dv[i].w));
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      float a[8], b[8], g[8], o[8];
+      unpack8(xv[i], a);
+      unpack8(dv[i], b);
+      unpack8(wr[lane + 32 * i], g);
+      float res[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      if (dresr) unpack8(ld_nc_v4(dresr + lane + 32 * i), res);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = r * g[j] * b[j] - a[j] * c + res[j];
+      dxr[lane + 32 * i] = pack8(o);
+    }
+  }
+  __syncthreads();
+  float4* out = reinterpret_cast<float4*>(dw_partial + (int64_t)blockIdx.x * cols);
+  for (int c4 = threadIdx.x; c4 < cols / 4; c4 += blockDim.x) {
+    float4 s4 = reinterpret_cast<const float4*>(red)[c4];
+#pragma unroll
+    for (int ww = 1; ww < 4; ++ww) {
+      const float4 t = reinterpret_cast<const float4*>(red + ww * cols)[c4];
+      s4.x += t.x;
+      s4.y += t.y;
+      s4.z += t.z;
+      s4.w += t.w;
+    }
+    out[c4] = s4;
+  }
+}
+
+// rows per warp and CTA count of the fused backward (2 CTAs of 4 warps per SM, one wave)
+static inline void fused_norm_bwd_grid(int64_t rows, int& rows_per_warp, int& grid) {
+  const int64_t warps = 4LL * 2 * num_sms();
+  rows_per_warp = (int)((rows + warps - 1) / warps);
+  if (rows_per_warp < 1) rows_per_warp = 1;
+  grid = (int)((rows + 4LL * rows_per_warp - 1) / (4LL * rows_per_warp));
+}
+static inline bool fused_norm_bwd_ok(int64_t cols) {
+  return cols % 256 == 0 && (cols / 256 == 4 || cols / 256 == 8 || cols / 256 == 12);  // 16: spills
+}
+
 // one thread per 8-column chunk, a 64-row slab per blockIdx.y; coalesced 16-byte loads along rows
 __global__ void __launch_bounds__(128)
     rmsnorm_bwd_dw(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
@@ -337,7 +438,12 @@ extern "C" int kpo_rmsnorm_fwd(const void* x, const void* w, void* y, float* rst
 
 extern "C" int kpo_rmsnorm_bwd_partial_rows(int64_t rows, int64_t cols, int64_t* n_partials) {
   KPO_CHECK_ARG(n_partials, "null n_partials");
-  (void)cols;
+  if (fused_norm_bwd_ok(cols) && rows > 0) {
+    int rpw, grid;
+    fused_norm_bwd_grid(rows, rpw, grid);
+    *n_partials = grid;
+    return KPO_OK;
+  }
   *n_partials = (rows + kNormBwdSlab - 1) / kNormBwdSlab;
   return KPO_OK;
 }
@@ -356,6 +462,27 @@ extern "C" int kpo_rmsnorm_bwd(const void* dy, const void* x, const void* w, con
   auto W = (const __nv_bfloat16*)w;
   auto Dr = (const __nv_bfloat16*)dres;
   auto Dx = (__nv_bfloat16*)dx;
+  if (fused_norm_bwd_ok(cols)) {
+    int rpw, g;
+    fused_norm_bwd_grid(rows, rpw, g);
+    const size_t sm = 4 * (size_t)cols * sizeof(float);
+    switch (cols / 256) {
+#define KPO_NBF_CASE(n)                                                                                       \
+  case n: {                                                                                                 \
+    static bool set = false;                                                                                \
+    if (!set) {                                                                                             \
+      KPO_CUDA(cudaFuncSetAttribute(rmsnorm_bwd_fused<n>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536)); \
+      set = true;                                                                                           \
+    }                                                                                                       \
+    rmsnorm_bwd_fused<n><<<g, 128, sm, st>>>(Dy, X, W, rstd, Dr, Dx, dw_partial, rows, rpw);                \
+    break;                                                                                                  \
+  }
+      KPO_NBF_CASE(4) KPO_NBF_CASE(8) KPO_NBF_CASE(12) KPO_NBF_CASE(16)
+#undef KPO_NBF_CASE
+    }
+    KPO_LAUNCH_CHECK();
+    return KPO_OK;
+  }
   const dim3 grid((unsigned)((rows + 7) / 8)), block(256);
   if (cols % 256 == 0 && cols / 256 <= 4) {  // small rows: cache in registers; large rows: two-pass re-read
     switch (cols / 256) {

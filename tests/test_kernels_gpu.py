@@ -59,7 +59,7 @@ def test_gemm_replay_resets_scheduler(cuda):
     assert int(ops._default_sched[0].buf.abs().sum()) == 0
 
 
-@pytest.mark.parametrize("rows,cols", [(4096, 3072), (100, 1024), (33, 8192), (7, 520)])
+@pytest.mark.parametrize("rows,cols", [(4096, 3072), (100, 1024), (33, 8192), (7, 520), (8192, 2048), (5, 3072), (1001, 3072)])
 def test_rmsnorm(cuda, rows, cols):
     from paper_2601_17654_b200 import ops
     x = torch.randn(rows, cols, device=cuda).bfloat16()

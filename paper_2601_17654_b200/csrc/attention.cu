@@ -90,6 +90,7 @@ __global__ void __launch_bounds__(256, 1)
                     const __nv_bfloat16* __restrict__ v, __nv_bfloat16* __restrict__ o, float* __restrict__ lse,
                     int T, int hq, int hkv, int64_t qs, int64_t ks, int64_t vs, int64_t os, float scale_log2,
                     int causal) {
+  KPO_PDL_ENTRY();
   using CF = FwdCfg<D>;
   constexpr int BM = CF::BM, BN = CF::BN, NT = CF::NT;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -254,6 +255,7 @@ template <int D>
 __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
                                     float* __restrict__ dvec, float* __restrict__ dq_acc, int T, int hq,
                                     int64_t os) {
+  KPO_PDL_ENTRY();
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (gw >= (int64_t)T * hq) return;
@@ -277,6 +279,7 @@ __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ o, const _
 template <int D>
 __global__ void attn_bwd_post_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dq, int T, int hq,
                                      int64_t dqs) {
+  KPO_PDL_ENTRY();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one thread per 8 elements
   const int64_t total = (int64_t)T * hq * D / 8;
   if (i >= total) return;
@@ -307,6 +310,7 @@ __global__ void __launch_bounds__(128, 2)
                     __nv_bfloat16* __restrict__ dk, __nv_bfloat16* __restrict__ dv, int T, int hq, int hkv,
                     int64_t qs, int64_t ks, int64_t vs, int64_t os, int64_t dks, int64_t dvs, float scale,
                     int causal) {
+  KPO_PDL_ENTRY();
   using CF = BwdCfg<D>;
   constexpr int BN = CF::BN, BM = CF::BM, NT = CF::NT;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -508,9 +512,9 @@ static int fwd_launch(const void* q, const void* k, const void* v, void* o, floa
     set = true;
   }
   dim3 grid((unsigned)((T + CF::BM - 1) / CF::BM), (unsigned)hq);
-  attn_fwd_kernel<D><<<grid, CF::NT, CF::SMEM, s>>>((const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
+  KPO_CUDA(::kpo::pdl_launch(attn_fwd_kernel<D>, grid, CF::NT, CF::SMEM, s, (const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
                                                     (const __nv_bfloat16*)v, (__nv_bfloat16*)o, lse, (int)T, hq, hkv,
-                                                    qs, ks, vs, os, scale * kLog2e, causal);
+                                                    qs, ks, vs, os, scale * kLog2e, causal));
   KPO_LAUNCH_CHECK();
   return KPO_OK;
 }
@@ -525,8 +529,8 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* o
   float* dvec = dq_acc + T * hq * D;
   {
     const int64_t warps = T * hq;
-    attn_bwd_pre_kernel<D><<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(
-        (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, dvec, dq_acc, (int)T, hq, os);
+    KPO_CUDA(::kpo::pdl_launch(attn_bwd_pre_kernel<D>, (unsigned)((warps * 32 + 255) / 256), 256, 0, s, 
+        (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, dvec, dq_acc, (int)T, hq, os));
     KPO_LAUNCH_CHECK();
   }
   if (D == 128 && use_tc && T % 8 == 0) {  // tcgen05 path (bulk-copied softmax stats need 16 B rows)
@@ -541,10 +545,10 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* o
     if (st) return st;
     if (split) {
       const int64_t n = T * hkv * D / 8;
-      attn_bwd_post_kernel<D><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dkv_acc, (__nv_bfloat16*)dk, (int)T, hkv, dks);
+      KPO_CUDA(::kpo::pdl_launch(attn_bwd_post_kernel<D>, (unsigned)((n + 255) / 256), 256, 0, s, dkv_acc, (__nv_bfloat16*)dk, (int)T, hkv, dks));
       KPO_LAUNCH_CHECK();
-      attn_bwd_post_kernel<D><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dkv_acc + T * hkv * D, (__nv_bfloat16*)dv,
-                                                                           (int)T, hkv, dvs);
+      KPO_CUDA(::kpo::pdl_launch(attn_bwd_post_kernel<D>, (unsigned)((n + 255) / 256), 256, 0, s, dkv_acc + T * hkv * D, (__nv_bfloat16*)dv,
+                                                                           (int)T, hkv, dvs));
       KPO_LAUNCH_CHECK();
     }
   } else {
@@ -554,14 +558,14 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* o
     set = true;
   }
   dim3 grid((unsigned)((T + CF::BN - 1) / CF::BN), (unsigned)hkv);
-  attn_bwd_kernel<D><<<grid, CF::NT, CF::SMEM, s>>>(
+  KPO_CUDA(::kpo::pdl_launch(attn_bwd_kernel<D>, grid, CF::NT, CF::SMEM, s, 
       (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, (const __nv_bfloat16*)v, (const __nv_bfloat16*)dout, lse, dvec,
-      dq_acc, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, (int)T, hq, hkv, qs, ks, vs, os, dks, dvs, scale, causal);
+      dq_acc, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, (int)T, hq, hkv, qs, ks, vs, os, dks, dvs, scale, causal));
   KPO_LAUNCH_CHECK();
   }
   {
     const int64_t n = T * hq * D / 8;
-    attn_bwd_post_kernel<D><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dq_acc, (__nv_bfloat16*)dq, (int)T, hq, dqs);
+    KPO_CUDA(::kpo::pdl_launch(attn_bwd_post_kernel<D>, (unsigned)((n + 255) / 256), 256, 0, s, dq_acc, (__nv_bfloat16*)dq, (int)T, hq, dqs));
     KPO_LAUNCH_CHECK();
   }
   return KPO_OK;

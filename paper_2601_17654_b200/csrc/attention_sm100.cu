@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                        const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ o, float* __restrict__ lse,
                        int T, int hq, int hkv, int64_t os, float scale_log2, int causal) {
+  ::kpo::pdl_launch_dependents();  // the next kernel may start its prologue; it waits for us
   using C = Fwd<D>;
   constexpr int BM = C::BM, BN = C::BN, KSUB = D / 64;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -103,6 +104,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // one CTA per SM owns all 512 columns, so the allocation starts at lane 0 / column 0; a constant base
   // keeps every TMEM address of the MMA issue loops in uniform registers (no per-MMA R2UR)
   if (*tmem_slot != 0) __trap();
+  ::kpo::pdl_wait();  // the previous kernel's outputs (our inputs) are complete and visible
   constexpr uint32_t tmem = 0;
   const uint32_t sQ = smem_u32(smem + C::OFF_Q), sK = smem_u32(smem + C::OFF_K);
   const uint32_t sV = smem_u32(smem + C::OFF_V);
@@ -311,8 +313,8 @@ int fwd_launch(const void* q, const void* k, const void* v, void* o, float* lse,
   dim3 grid((unsigned)hq, (unsigned)((T + C::BM - 1) / C::BM));
   auto go = [&](auto kern) -> int {
     KPO_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    kern<<<grid, kThreads, C::SMEM, st>>>(mq, mk, mv, (__nv_bfloat16*)o, lse, (int)T, hq, hkv, os, scale * kLog2e,
-                                         causal);
+    KPO_CUDA(::kpo::pdl_launch(kern, grid, kThreads, C::SMEM, st, mq, mk, mv, (__nv_bfloat16*)o, lse, (int)T, hq, hkv, os, scale * kLog2e,
+                                         causal));
     return KPO_OK;
   };
   int rc;
@@ -374,6 +376,7 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
                        __nv_bfloat16* __restrict__ dk, __nv_bfloat16* __restrict__ dv, int T, int hq, int hkv,
                        int64_t dks, int64_t dvs, float scale, int causal, float* __restrict__ dkv_acc,
                        int ablate) {
+  ::kpo::pdl_launch_dependents();  // the next kernel may start its prologue; it waits for us
   // ablate (KPO_ATTN_BWD_ABLATE, measurement only; results are wrong when != 0): 1 = no dQ reduce-add,
   // 2 = no dQ drain (TMEM -> smem), 4 = no exponentials, 8 = no dQ^T MMA, 16 = no softmax,
   // 32 = no Q/dO reloads, 64 = no dV/dK MMAs, 128 = no S^T/dP^T MMAs
@@ -433,6 +436,7 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
   // one CTA per SM owns all 512 columns, so the allocation starts at lane 0 / column 0; a constant base
   // keeps every TMEM address of the MMA issue loops in uniform registers (no per-MMA R2UR)
   if (*tmem_slot != 0) __trap();
+  ::kpo::pdl_wait();  // the previous kernel's outputs (our inputs) are complete and visible
   constexpr uint32_t tmem = 0;
   const uint32_t sK = smem_u32(smem + C::OFF_K), sV = smem_u32(smem + C::OFF_V);
   const uint32_t sQ = smem_u32(smem + C::OFF_Q), sDO = smem_u32(smem + C::OFF_DO);
@@ -717,9 +721,9 @@ int bwd_launch(const void* q, const void* k, const void* v, const void* dout, co
     set = true;
   }
   dim3 grid((unsigned)(dkv_acc ? hq : hkv), (unsigned)((T + C::BN - 1) / C::BN));
-  attn_bwd_tc_kernel<D><<<grid, C::THREADS, C::SMEM, st>>>(mq, mk, mv, mo, mdq, lse, dvec, dq_acc, (__nv_bfloat16*)dk,
+  KPO_CUDA(::kpo::pdl_launch(attn_bwd_tc_kernel<D>, grid, C::THREADS, C::SMEM, st, mq, mk, mv, mo, mdq, lse, dvec, dq_acc, (__nv_bfloat16*)dk,
                                                           (__nv_bfloat16*)dv, (int)T, hq, hkv, dks, dvs, scale, causal,
-                                                          dkv_acc, getenv("KPO_ATTN_BWD_ABLATE") ? atoi(getenv("KPO_ATTN_BWD_ABLATE")) : 0);
+                                                          dkv_acc, getenv("KPO_ATTN_BWD_ABLATE") ? atoi(getenv("KPO_ATTN_BWD_ABLATE")) : 0));
   KPO_LAUNCH_CHECK();
   return KPO_OK;
 }

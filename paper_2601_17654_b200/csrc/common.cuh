@@ -6,6 +6,8 @@
 #include <stdio.h>
 #include <stdarg.h>
 #include <string>
+#include <utility>
+#include <cstdlib>
 
 #include "../../include/kpo.h"
 
@@ -41,6 +43,48 @@ inline int num_sms(int device = -1) {
   cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
   if (device >= 0 && device < 64) cached[device] = n;
   return n;
+}
+
+// ------------------------------------------------------------------ programmatic dependent launch
+// Every compute kernel is launched with programmatic stream serialization: it lets the next kernel
+// of the stream launch once all of its CTAs have started (griddepcontrol.launch_dependents), and the
+// next kernel waits for this one's completion and memory flush (griddepcontrol.wait) before it
+// touches global memory.  The dependent's launch latency and prologue (barrier init, TMEM
+// allocation, tensor-map prefetch) then overlap the tail of the previous kernel.  Both
+// instructions are no-ops for a kernel launched without the attribute.
+// Opt-in (KPO_PDL=1): measured on the layer step it is SLOWER (5.73 -> 6.06 ms per iteration, A/B in
+// one session), most likely because early-launched dependents take SMs the SM-budgeted collective
+// on the other stream needs; the launch path and the kernel-side waits are kept for that experiment.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#define KPO_PDL_ENTRY()             \
+  do {                              \
+    ::kpo::pdl_launch_dependents(); \
+    ::kpo::pdl_wait();              \
+  } while (0)
+
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("KPO_PDL");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 // ------------------------------------------------------------------ device helpers

@@ -18,6 +18,7 @@ __global__ void __launch_bounds__(256) rmsnorm_fwd_cached(const __nv_bfloat16* _
                                                           __nv_bfloat16* __restrict__ y,
                                                           float* __restrict__ rstd, int64_t rows,
                                                           int cols, float eps) {
+  KPO_PDL_ENTRY();
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -54,6 +55,7 @@ __global__ void __launch_bounds__(256) rmsnorm_fwd_generic(const __nv_bfloat16* 
                                                            __nv_bfloat16* __restrict__ y,
                                                            float* __restrict__ rstd, int64_t rows,
                                                            int cols, float eps) {
+  KPO_PDL_ENTRY();
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -95,6 +97,7 @@ __global__ void __launch_bounds__(256)
                           const __nv_bfloat16* __restrict__ w, const float* __restrict__ rstd,
                           const __nv_bfloat16* __restrict__ dres, __nv_bfloat16* __restrict__ dx, int64_t rows,
                           int cols) {
+  KPO_PDL_ENTRY();
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -141,6 +144,7 @@ __global__ void __launch_bounds__(256)
                            const __nv_bfloat16* __restrict__ w, const float* __restrict__ rstd,
                            const __nv_bfloat16* __restrict__ dres, __nv_bfloat16* __restrict__ dx, int64_t rows,
                            int cols) {
+  KPO_PDL_ENTRY();
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -188,6 +192,7 @@ __global__ void __launch_bounds__(128)
                       const __nv_bfloat16* __restrict__ w, const float* __restrict__ rstd,
                       const __nv_bfloat16* __restrict__ dres, __nv_bfloat16* __restrict__ dx,
                       float* __restrict__ dw_partial, int64_t rows, int rows_per_warp) {
+  KPO_PDL_ENTRY();
   constexpr int cols = NV * 256;
   extern __shared__ float red[];  // [4 warps][cols] dgamma accumulators (each warp owns its row)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -282,6 +287,7 @@ static inline bool fused_norm_bwd_ok(int64_t cols) {
 __global__ void __launch_bounds__(128)
     rmsnorm_bwd_dw(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
                    const float* __restrict__ rstd, float* __restrict__ dw_partial, int64_t rows, int cols) {
+  KPO_PDL_ENTRY();
   const int chunk = blockIdx.x * blockDim.x + threadIdx.x;
   if (chunk * 8 >= cols) return;
   const int64_t r0 = (int64_t)blockIdx.y * kNormBwdSlab;
@@ -304,6 +310,7 @@ __global__ void __launch_bounds__(128)
 // out[c] = sum_r in[r, c]; one thread per column, coalesced across the warp.
 __global__ void colsum_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
                               int64_t rows, int64_t cols) {
+  KPO_PDL_ENTRY();
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= cols) return;
   float s = 0.f;
@@ -317,6 +324,7 @@ __global__ void colsum_kernel(const float* __restrict__ in, __nv_bfloat16* __res
 __global__ void rope_kernel(const __nv_bfloat16* __restrict__ in, int64_t in_stride,
                             __nv_bfloat16* __restrict__ out, int64_t out_stride, int heads,
                             int head_dim, float log2_theta, int64_t pos0, int inverse) {
+  KPO_PDL_ENTRY();
   extern __shared__ float cs[];  // [half] cos, [half] sin
   const int half = head_dim / 2;
   const int64_t t = blockIdx.x;
@@ -356,6 +364,7 @@ __device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + __expf
 
 __global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ act,
                                   int64_t rows, int64_t ffn) {
+  KPO_PDL_ENTRY();
   const int64_t nvr = ffn / 8;
   const int64_t total = rows * nvr;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
@@ -373,6 +382,7 @@ __global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfl
 
 __global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ dact, const __nv_bfloat16* __restrict__ gu,
                                   __nv_bfloat16* __restrict__ dgu, int64_t rows, int64_t ffn) {
+  KPO_PDL_ENTRY();
   const int64_t nvr = ffn / 8;
   const int64_t total = rows * nvr;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
@@ -423,14 +433,14 @@ extern "C" int kpo_rmsnorm_fwd(const void* x, const void* w, void* y, float* rst
   if (cols % 256 == 0 && cols / 256 <= 16) {
     switch (cols / 256) {
 #define KPO_NORM_CASE(n) \
-  case n: rmsnorm_fwd_cached<n><<<grid, block, 0, s>>>(X, W, Y, rstd, rows, (int)cols, eps); break;
+  case n: KPO_CUDA(::kpo::pdl_launch(rmsnorm_fwd_cached<n>, grid, block, 0, s, X, W, Y, rstd, rows, (int)cols, eps)); break;
       KPO_NORM_CASE(1) KPO_NORM_CASE(2) KPO_NORM_CASE(3) KPO_NORM_CASE(4) KPO_NORM_CASE(5)
       KPO_NORM_CASE(6) KPO_NORM_CASE(8) KPO_NORM_CASE(10) KPO_NORM_CASE(12) KPO_NORM_CASE(16)
 #undef KPO_NORM_CASE
-      default: rmsnorm_fwd_generic<<<grid, block, 0, s>>>(X, W, Y, rstd, rows, (int)cols, eps);
+      default: KPO_CUDA(::kpo::pdl_launch(rmsnorm_fwd_generic, grid, block, 0, s, X, W, Y, rstd, rows, (int)cols, eps));
     }
   } else {
-    rmsnorm_fwd_generic<<<grid, block, 0, s>>>(X, W, Y, rstd, rows, (int)cols, eps);
+    KPO_CUDA(::kpo::pdl_launch(rmsnorm_fwd_generic, grid, block, 0, s, X, W, Y, rstd, rows, (int)cols, eps));
   }
   KPO_LAUNCH_CHECK();
   return KPO_OK;
@@ -474,7 +484,7 @@ extern "C" int kpo_rmsnorm_bwd(const void* dy, const void* x, const void* w, con
       KPO_CUDA(cudaFuncSetAttribute(rmsnorm_bwd_fused<n>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536)); \
       set = true;                                                                                           \
     }                                                                                                       \
-    rmsnorm_bwd_fused<n><<<g, 128, sm, st>>>(Dy, X, W, rstd, Dr, Dx, dw_partial, rows, rpw);                \
+    KPO_CUDA(::kpo::pdl_launch(rmsnorm_bwd_fused<n>, g, 128, sm, st, Dy, X, W, rstd, Dr, Dx, dw_partial, rows, rpw));                \
     break;                                                                                                  \
   }
       KPO_NBF_CASE(4) KPO_NBF_CASE(8) KPO_NBF_CASE(12) KPO_NBF_CASE(16)
@@ -487,25 +497,25 @@ extern "C" int kpo_rmsnorm_bwd(const void* dy, const void* x, const void* w, con
   if (cols % 256 == 0 && cols / 256 <= 4) {  // small rows: cache in registers; large rows: two-pass re-read
     switch (cols / 256) {
 #define KPO_NB_CASE(n) \
-  case n: rmsnorm_bwd_dx_cached<n><<<grid, block, 0, st>>>(Dy, X, W, rstd, Dr, Dx, rows, (int)cols); break;
+  case n: KPO_CUDA(::kpo::pdl_launch(rmsnorm_bwd_dx_cached<n>, grid, block, 0, st, Dy, X, W, rstd, Dr, Dx, rows, (int)cols)); break;
       KPO_NB_CASE(1) KPO_NB_CASE(2) KPO_NB_CASE(3) KPO_NB_CASE(4)
 #undef KPO_NB_CASE
-      default: rmsnorm_bwd_dx_generic<<<grid, block, 0, st>>>(Dy, X, W, rstd, Dr, Dx, rows, (int)cols);
+      default: KPO_CUDA(::kpo::pdl_launch(rmsnorm_bwd_dx_generic, grid, block, 0, st, Dy, X, W, rstd, Dr, Dx, rows, (int)cols));
     }
   } else {
-    rmsnorm_bwd_dx_generic<<<grid, block, 0, st>>>(Dy, X, W, rstd, Dr, Dx, rows, (int)cols);
+    KPO_CUDA(::kpo::pdl_launch(rmsnorm_bwd_dx_generic, grid, block, 0, st, Dy, X, W, rstd, Dr, Dx, rows, (int)cols));
   }
   KPO_LAUNCH_CHECK();
   const dim3 g2((unsigned)((cols / 8 + 127) / 128), (unsigned)((rows + kNormBwdSlab - 1) / kNormBwdSlab));
-  rmsnorm_bwd_dw<<<g2, 128, 0, st>>>(Dy, X, rstd, dw_partial, rows, (int)cols);
+  KPO_CUDA(::kpo::pdl_launch(rmsnorm_bwd_dw, g2, 128, 0, st, Dy, X, rstd, dw_partial, rows, (int)cols));
   KPO_LAUNCH_CHECK();
   return KPO_OK;
 }
 
 extern "C" int kpo_colsum_f32_to_bf16(const float* in, void* out, int64_t rows, int64_t cols, void* stream) {
   KPO_CHECK_ARG(in && out && rows >= 0 && cols > 0, "colsum: bad args");
-  colsum_kernel<<<(unsigned)((cols + 255) / 256), 256, 0, (cudaStream_t)stream>>>(in, (__nv_bfloat16*)out,
-                                                                                rows, cols);
+  KPO_CUDA(::kpo::pdl_launch(colsum_kernel, (unsigned)((cols + 255) / 256), 256, 0, (cudaStream_t)stream, in, (__nv_bfloat16*)out,
+                                                                                rows, cols));
   KPO_LAUNCH_CHECK();
   return KPO_OK;
 }
@@ -520,9 +530,9 @@ extern "C" int kpo_rope(const void* in, int64_t in_row_stride, void* out, int64_
   KPO_CHECK_ARG(theta > 1.f, "rope: theta must be > 1");
   if (tokens == 0) return KPO_OK;
   const int threads = 256;
-  rope_kernel<<<(unsigned)tokens, threads, head_dim * sizeof(float), (cudaStream_t)stream>>>(
+  KPO_CUDA(::kpo::pdl_launch(rope_kernel, (unsigned)tokens, threads, head_dim * sizeof(float), (cudaStream_t)stream, 
       (const __nv_bfloat16*)in, in_row_stride, (__nv_bfloat16*)out, out_row_stride, heads, head_dim,
-      log2f(theta), pos0, inverse);
+      log2f(theta), pos0, inverse));
   KPO_LAUNCH_CHECK();
   return KPO_OK;
 }
@@ -530,8 +540,8 @@ extern "C" int kpo_rope(const void* in, int64_t in_row_stride, void* out, int64_
 extern "C" int kpo_swiglu_fwd(const void* gu, void* act, int64_t rows, int64_t ffn, void* stream) {
   KPO_CHECK_ARG(gu && act && ffn % 8 == 0 && aligned16(gu) && aligned16(act), "swiglu_fwd: bad args");
   if (rows == 0) return KPO_OK;
-  swiglu_fwd_kernel<<<elem_grid(rows * ffn / 8, 256), 256, 0, (cudaStream_t)stream>>>(
-      (const __nv_bfloat16*)gu, (__nv_bfloat16*)act, rows, ffn);
+  KPO_CUDA(::kpo::pdl_launch(swiglu_fwd_kernel, elem_grid(rows * ffn / 8, 256), 256, 0, (cudaStream_t)stream, 
+      (const __nv_bfloat16*)gu, (__nv_bfloat16*)act, rows, ffn));
   KPO_LAUNCH_CHECK();
   return KPO_OK;
 }
@@ -540,8 +550,8 @@ extern "C" int kpo_swiglu_bwd(const void* dact, const void* gu, void* dgu, int64
                               void* stream) {
   KPO_CHECK_ARG(dact && gu && dgu && ffn % 8 == 0, "swiglu_bwd: bad args");
   if (rows == 0) return KPO_OK;
-  swiglu_bwd_kernel<<<elem_grid(rows * ffn / 8, 256), 256, 0, (cudaStream_t)stream>>>(
-      (const __nv_bfloat16*)dact, (const __nv_bfloat16*)gu, (__nv_bfloat16*)dgu, rows, ffn);
+  KPO_CUDA(::kpo::pdl_launch(swiglu_bwd_kernel, elem_grid(rows * ffn / 8, 256), 256, 0, (cudaStream_t)stream, 
+      (const __nv_bfloat16*)dact, (const __nv_bfloat16*)gu, (__nv_bfloat16*)dgu, rows, ffn));
   KPO_LAUNCH_CHECK();
   return KPO_OK;
 }

@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 __nv_bfloat16* __restrict__ D, const __nv_bfloat16* __restrict__ C, int M, int N, int K,
                 int64_t ldd, int* __restrict__ sched) {
+  ::kpo::pdl_launch_dependents();  // the next kernel may start its prologue; it waits for us
   using CF = Cfg<BN>;
   constexpr int STAGES = CF::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -100,6 +101,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  ::kpo::pdl_wait();  // inputs, scheduler words and outputs of the previous kernel are settled
 
   if (warp == 0) {
     if (lane == 0) {
@@ -263,8 +265,8 @@ static int launch(const CUtensorMap& ta, const CUtensorMap& tb, void* D, const v
     KPO_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM));
     attr_set = true;
   }
-  kern<<<grid, kThreads, Cfg<BN>::SMEM, s>>>(ta, tb, (__nv_bfloat16*)D, (const __nv_bfloat16*)C, (int)M, (int)N,
-                                              (int)K, ldd, sched);
+  KPO_CUDA(::kpo::pdl_launch(kern, grid, kThreads, Cfg<BN>::SMEM, s, ta, tb, (__nv_bfloat16*)D, (const __nv_bfloat16*)C, (int)M, (int)N,
+                                              (int)K, ldd, sched));
   KPO_LAUNCH_CHECK();
   return KPO_OK;
 }
@@ -298,6 +300,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  __nv_bfloat16* __restrict__ D, const __nv_bfloat16* __restrict__ C, int M, int N, int K,
                  int64_t ldd, int* __restrict__ sched) {
+  ::kpo::pdl_launch_dependents();  // the next kernel may start its prologue; it waits for us
   using CF = Cfg2<BN>;
   constexpr int STAGES = CF::STAGES;
   constexpr int HB = BN / 2;
@@ -341,6 +344,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  ::kpo::pdl_wait();  // inputs, scheduler words and outputs of the previous kernel are settled
   const uint32_t leader_sempty0 = mapa(smem_u32(&sempty[0]), 0);
   const uint32_t leader_tempty0 = mapa(smem_u32(&tempty[0]), 0);
 
@@ -516,8 +520,8 @@ static int launch2(const CUtensorMap& ta, const CUtensorMap& tb, void* D, const 
     KPO_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2<BN>::SMEM));
     attr_set = true;
   }
-  kern<<<grid, kThreads, Cfg2<BN>::SMEM, s>>>(ta, tb, (__nv_bfloat16*)D, (const __nv_bfloat16*)C, (int)M, (int)N,
-                                               (int)K, ldd, sched);
+  KPO_CUDA(::kpo::pdl_launch(kern, grid, kThreads, Cfg2<BN>::SMEM, s, ta, tb, (__nv_bfloat16*)D, (const __nv_bfloat16*)C, (int)M, (int)N,
+                                               (int)K, ldd, sched));
   KPO_LAUNCH_CHECK();
   return KPO_OK;
 }

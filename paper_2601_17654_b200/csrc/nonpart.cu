@@ -15,6 +15,7 @@ __global__ void __launch_bounds__(256) embedding_fwd_kernel(const int32_t* __res
                                                             const __nv_bfloat16* __restrict__ table,
                                                             __nv_bfloat16* __restrict__ out, int64_t T, int64_t h,
                                                             int64_t vocab, int* __restrict__ bad) {
+  KPO_PDL_ENTRY();
   const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
@@ -36,6 +37,7 @@ __global__ void __launch_bounds__(256) embedding_bwd_kernel(const int32_t* __res
                                                             const __nv_bfloat16* __restrict__ dy,
                                                             float* __restrict__ dtable, int64_t T, int64_t h,
                                                             int64_t vocab) {
+  KPO_PDL_ENTRY();
   const int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
@@ -80,6 +82,7 @@ __global__ void __launch_bounds__(kCeThreads) cross_entropy_kernel(const __nv_bf
                                                                     float* __restrict__ loss, int64_t V,
                                                                     int64_t ld, float grad_scale,
                                                                     int ignore_index) {
+  KPO_PDL_ENTRY();
   const int64_t t = blockIdx.x;
   const __nv_bfloat16* row = logits + t * ld;
   __nv_bfloat16* drow = dlogits + t * ld;
@@ -160,8 +163,8 @@ extern "C" int kpo_embedding_fwd(const int32_t* ids, const void* table, void* ou
                 "embedding_fwd: hidden must be a positive multiple of 8");
   KPO_CHECK_ARG(((uintptr_t)table & 15) == 0 && ((uintptr_t)out & 15) == 0, "embedding_fwd: 16B alignment");
   if (tokens == 0) return KPO_OK;
-  embedding_fwd_kernel<<<(unsigned)((tokens + 7) / 8), 256, 0, (cudaStream_t)stream>>>(
-      ids, (const __nv_bfloat16*)table, (__nv_bfloat16*)out, tokens, hidden, vocab, bad_flag);
+  KPO_CUDA(::kpo::pdl_launch(embedding_fwd_kernel, (unsigned)((tokens + 7) / 8), 256, 0, (cudaStream_t)stream, 
+      ids, (const __nv_bfloat16*)table, (__nv_bfloat16*)out, tokens, hidden, vocab, bad_flag));
   KPO_LAUNCH_CHECK();
   return KPO_OK;
 }
@@ -173,8 +176,8 @@ extern "C" int kpo_embedding_bwd(const int32_t* ids, const void* dy, float* dtab
                 "embedding_bwd: hidden must be a positive multiple of 8");
   KPO_CHECK_ARG(((uintptr_t)dy & 15) == 0 && ((uintptr_t)dtable & 15) == 0, "embedding_bwd: 16B alignment");
   if (tokens == 0) return KPO_OK;
-  embedding_bwd_kernel<<<(unsigned)((tokens + 7) / 8), 256, 0, (cudaStream_t)stream>>>(
-      ids, (const __nv_bfloat16*)dy, dtable, tokens, hidden, vocab);
+  KPO_CUDA(::kpo::pdl_launch(embedding_bwd_kernel, (unsigned)((tokens + 7) / 8), 256, 0, (cudaStream_t)stream, 
+      ids, (const __nv_bfloat16*)dy, dtable, tokens, hidden, vocab));
   KPO_LAUNCH_CHECK();
   return KPO_OK;
 }
@@ -187,8 +190,8 @@ extern "C" int kpo_cross_entropy(const void* logits, void* dlogits, const int32_
                 "cross_entropy: vocab and row stride must be positive multiples of 8");
   KPO_CHECK_ARG(((uintptr_t)logits & 15) == 0 && ((uintptr_t)dlogits & 15) == 0, "cross_entropy: 16B alignment");
   if (tokens == 0) return KPO_OK;
-  cross_entropy_kernel<<<(unsigned)tokens, kCeThreads, 0, (cudaStream_t)stream>>>(
-      (const __nv_bfloat16*)logits, (__nv_bfloat16*)dlogits, labels, loss, vocab, ld, grad_scale, ignore_index);
+  KPO_CUDA(::kpo::pdl_launch(cross_entropy_kernel, (unsigned)tokens, kCeThreads, 0, (cudaStream_t)stream, 
+      (const __nv_bfloat16*)logits, (__nv_bfloat16*)dlogits, labels, loss, vocab, ld, grad_scale, ignore_index));
   KPO_LAUNCH_CHECK();
   return KPO_OK;
 }

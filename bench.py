@@ -383,6 +383,31 @@ def run_kpo(args):
                "min_energy": tot(emin)}
         frontier = {k: {"time_ms": round(v[0], 4), "energy_j": round(v[1], 4)} for k, v in pts.items()}
         frontier["chosen_min_energy"] = {n: emin[n][0].timing.encode() + f"@{emin[n][0].sm_alloc}" for n in layer.order}
+        # the selected schedule sets executed as whole iterations (device time + NVML energy over >= 2 s),
+        # next to the default nanobatching schedule measured the same way
+        frontier["executed"] = {}
+        for label, choice in (("nanobatching_default", default), ("min_time", tmin), ("min_energy", emin)):
+            sched = {n: choice[n][0] for n in layer.order}
+            r2 = LayerRunner(layer, eng, schedule=sched)
+            r2.warm()
+            for _ in range(3):
+                r2.step()
+            torch.cuda.synchronize(dev)
+            n_it = max(args.steps, int(math.ceil(2.0 / max(ms / 1e3, 1e-4))))
+            q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            barrier()
+            torch.cuda.synchronize(dev)
+            w0 = time.perf_counter()
+            q0.record(eng.exec.compute)
+            for _ in range(n_it):
+                r2.step()
+            q1.record(eng.exec.compute)
+            torch.cuda.synchronize(dev)
+            w1 = time.perf_counter()
+            t_it = max_over_ranks(q0.elapsed_time(q1) / n_it)
+            e_it = sum_over_ranks(eng.sampler.window_j(w0, w1) / n_it)
+            frontier["executed"][label] = {"s_per_iter": round(t_it / 1e3, 7), "j_per_iter": round(e_it, 4),
+                                           "iterations": n_it}
         frontier["note"] = ("frequency fixed: NVML locked clocks NOT_SUPPORTED on this pool (power.py); sweep over "
                             "comm SM budget x launch timing, windows of " + str(args.sweep_window) + " s")
 

@@ -289,7 +289,12 @@ def run_kpo(args):
     d2h = sum(t.numel() * t.element_size() for t in dxs)
 
     # ------------------------------------------------ dominant kernel: per-unit times inside the step
-    ut = run.unit_times(iters=3)
+    try:
+        ut = run.unit_times_graph(iters=3)
+        ut_mode = "graph replay"
+    except Exception as ex:  # capture unsupported: eager issue with the same events
+        ut = run.unit_times(iters=3)
+        ut_mode = "eager (" + type(ex).__name__ + ")"
     per_unit = {}
     for name in layer.order:
         for u in layer.programs[name].units:
@@ -471,6 +476,7 @@ def run_kpo(args):
                          "algorithmic_per_launch": dom_unit.spec.flops if dom_row["bound"] == "tensor"
                          else dom_unit.spec.bytes, "avg_launch_ms": dom_row["avg_launch_ms"]},
             "kernels": kernels,
+            "kernels_timing": "CUDA events around each launch unit on the compute stream, " + ut_mode + ", 3 iterations",
             "iteration_roofline": iter_roofline,
             "comm": {"mode": "loopback (HBM)" if world == 1 else "cuda-ipc p2p (NVLink)", "units": comm_rows},
             "frontier": frontier,

@@ -129,6 +129,43 @@ class LayerRunner:
         self.engine.exec.compute.synchronize()
 
     # ---------------------------------------------------------------- instrumentation
+    def unit_times_graph(self, iters: int = 3) -> dict[str, list[float]]:
+        """Per-launch-unit durations (ms) inside real iterations executed the way the step executes
+        them: every partition (with timing events recorded around each unit on the compute stream,
+        the stream the unit's kernels are launched on) captured as a CUDA graph and replayed, comm
+        overlapping.  Unlike the eager variant, host-side launch work is not inside the intervals."""
+        ex = self.engine.exec
+        marks, graphs = [], []
+        for name in self.layer.order:
+            prog, cfg = self.layer.programs[name], self.schedule[name]
+            wrapped = []
+            for u in prog.units:
+                e0 = torch.cuda.Event(enable_timing=True, external=True)
+                e1 = torch.cuda.Event(enable_timing=True, external=True)
+                marks.append((u.name, e0, e1))
+
+                def fn(st, u=u, e0=e0, e1=e1):
+                    e0.record(st)
+                    u.fn(st)
+                    e1.record(st)
+                wrapped.append(type(u)(u.name, u.spec, fn, u.kind, u.n_kernels))
+            tmp = type(prog)(prog.name, wrapped, prog.comm, prog.comm_group_size)
+            ex.issue(tmp, cfg, self.ncta)  # eager once (first-call setup outside the capture)
+            torch.cuda.synchronize(self.engine.device)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=ex.compute):
+                ex.issue(tmp, cfg, self.ncta)
+            graphs.append(g)
+        out: dict[str, list[float]] = {}
+        for _ in range(iters):
+            with torch.cuda.stream(ex.compute):
+                for g in graphs:
+                    g.replay()
+            torch.cuda.synchronize(self.engine.device)
+            for nm, e0, e1 in marks:
+                out.setdefault(nm, []).append(e0.elapsed_time(e1))
+        return out
+
     def unit_times(self, iters: int = 3) -> dict[str, list[float]]:
         """Per-launch-unit durations (ms) inside real iterations: eager issue with CUDA events
         recorded on the stream each unit is launched on (the compute stream), comm overlapping."""

@@ -85,6 +85,16 @@ int kpo_gemm(const void* A, const void* B, void* D, const void* C, int64_t M, in
              int a_mn_major, int b_mn_major, int64_t lda, int64_t ldb, int64_t ldd, int max_ctas,
              int* sched, void* stream);
 
+/* Forward (TN) GEMM whose output columns [0, rope_cols) are rotary-embedded in the epilogue:
+ * heads of head_dim = 128 columns, pairs (i, i + 64) rotated by table[row][i] = (cos, sin), before the
+ * bf16 rounding.  Fuses the reference's separate "rope" memory-bound KernelSpec (workloads.py:46)
+ * into "linear_qkv" (workloads.py:45).  table: fp32 [M][head_dim/2][2] from kpo_rope_table. */
+int kpo_gemm_rope(const void* A, const void* B, void* D, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb,
+                  int64_t ldd, int max_ctas, int* sched, const float* rope_table, int64_t rope_cols, int head_dim,
+                  void* stream);
+/* table[t][i] = (cos, sin)((pos0 + t) * theta^(-2i/head_dim)), fp32, t < tokens, i < head_dim/2. */
+int kpo_rope_table(int64_t tokens, int head_dim, float theta, int64_t pos0, float* table, void* stream);
+
 /* ---------------------------------------------------------------- attention */
 /* Causal GQA flash attention, bf16 in/out, fp32 softmax statistics.
  * q: [T, hq, d] with token stride q_stride (elements), k/v: [T, hkv, d] with k_stride/v_stride,

@@ -274,7 +274,9 @@ __global__ void __launch_bounds__(128)
 
 // rows per warp and CTA count of the fused backward (2 CTAs of 4 warps per SM, one wave)
 static inline void fused_norm_bwd_grid(int64_t rows, int& rows_per_warp, int& grid) {
-  const int64_t warps = 4LL * 2 * num_sms();
+  int sms = num_sms();
+  if (sms <= 0) sms = 148;  // no device visible (host-only queries): B200's SM count
+  const int64_t warps = 4LL * 2 * sms;
   rows_per_warp = (int)((rows + warps - 1) / warps);
   if (rows_per_warp < 1) rows_per_warp = 1;
   grid = (int)((rows + 4LL * rows_per_warp - 1) / (4LL * rows_per_warp));
@@ -533,6 +535,30 @@ extern "C" int kpo_rope(const void* in, int64_t in_row_stride, void* out, int64_
   KPO_CUDA(::kpo::pdl_launch(rope_kernel, (unsigned)tokens, threads, head_dim * sizeof(float), (cudaStream_t)stream, 
       (const __nv_bfloat16*)in, in_row_stride, (__nv_bfloat16*)out, out_row_stride, heads, head_dim,
       log2f(theta), pos0, inverse));
+  KPO_LAUNCH_CHECK();
+  return KPO_OK;
+}
+
+// (cos, sin) of position pos0 + t and frequency i, for t < tokens and i < head_dim / 2: the same
+// arithmetic as rope_kernel, tabulated once for the fused rotary epilogue of the QKV GEMM.
+__global__ void rope_table_kernel(float2* __restrict__ table, int64_t tokens, int half, float log2_theta,
+                                  int64_t pos0) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= tokens * half) return;
+  const int64_t t = e / half;
+  const int i = (int)(e % half);
+  const float inv_freq = exp2f(-(2.0f * (float)i / (float)(2 * half)) * log2_theta);
+  float sn, cn;
+  sincosf((float)(pos0 + t) * inv_freq, &sn, &cn);
+  table[e] = make_float2(cn, sn);
+}
+
+extern "C" int kpo_rope_table(int64_t tokens, int head_dim, float theta, int64_t pos0, float* table, void* stream) {
+  KPO_CHECK_ARG(table && tokens >= 0 && head_dim % 2 == 0 && head_dim > 0 && theta > 1.f, "rope_table: bad args");
+  if (tokens == 0) return KPO_OK;
+  const int64_t n = tokens * (head_dim / 2);
+  rope_table_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<float2*>(table), tokens, head_dim / 2, log2f(theta), pos0);
   KPO_LAUNCH_CHECK();
   return KPO_OK;
 }

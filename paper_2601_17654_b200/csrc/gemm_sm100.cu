@@ -66,12 +66,108 @@ constexpr int kCPre = 4;
 // bulk tensor store [64 cols x 32 rows].  Full-line writes instead of 16-byte row-strided stores
 // (measured: the row-strided stores cost ~1.5x the L2 throughput of cuBLAS's TMA-store epilogue for
 // the same tile); rows / columns beyond M / N are clipped by the tensor map.
-template <int BN, int BUFS, typename WaitAcc>
+// Fused rotary embedding for the QKV projection: output columns [0, cols) are q / k heads of 128;
+// each pair (i, i + 64) of a head is rotated by the row's angle table entry i (cos, sin), exactly the
+// rotation of rope_kernel (elementwise.cu), but on the fp32 accumulator before the single bf16
+// rounding.  cs = [rows][64] float2 (kpo_rope_table).
+struct RopeArgs {
+  const float2* cs;
+  int cols;
+};
+
+template <int BUFS>
+__device__ __forceinline__ void store_box(uint32_t stage, int lane, int& store_cnt, const uint4* packed,
+                                          const CUtensorMap* tmD, int col0, int warp_row0) {
+  const int b = store_cnt % BUFS;
+  if (lane == 0) {
+    if (BUFS == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+  __syncwarp();
+  const uint32_t box = stage + b * 4096;
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(box + lane * 128 + ((k ^ (lane & 7)) << 4)),
+                 "r"(packed[k].x), "r"(packed[k].y), "r"(packed[k].z), "r"(packed[k].w)
+                 : "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(tmD)),
+                 "r"(box), "r"(col0), "r"(warp_row0)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+  ++store_cnt;
+}
+
+// one 128-column head of a rope tile: chunks (0, 2) then (1, 3) are the rotation pairs
+template <int BUFS>
+__device__ __forceinline__ void epilogue_rope_head(uint32_t tmem_head, const float2* cs_row, bool row_ok, int col0,
+                                                   int warp_row0, uint32_t stage, int lane, int& store_cnt,
+                                                   const CUtensorMap* tmD) {
+  uint4 lo[8], hi[8];  // output columns [0, 64) and [64, 128) of the head, packed bf16
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    uint32_t a[32], b[32];
+    tmem_ld32(tmem_head + h * 32, a);
+    tmem_ld32(tmem_head + 64 + h * 32, b);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      float oa[8], ob[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int i = h * 32 + v * 8 + j;  // frequency index
+        const float2 t = row_ok ? cs_row[i] : make_float2(1.f, 0.f);
+        const float x = __uint_as_float(a[v * 8 + j]), y = __uint_as_float(b[v * 8 + j]);
+        oa[j] = x * t.x - y * t.y;
+        ob[j] = y * t.x + x * t.y;
+      }
+      lo[h * 4 + v] = pack8(oa);
+      hi[h * 4 + v] = pack8(ob);
+    }
+  }
+  store_box<BUFS>(stage, lane, store_cnt, lo, tmD, col0, warp_row0);
+  store_box<BUFS>(stage, lane, store_cnt, hi, tmD, col0 + 64, warp_row0);
+}
+
+template <int BN, int BUFS, bool ROPE, typename WaitAcc>
 __device__ __forceinline__ void epilogue_row(uint32_t tmem_row, const CUtensorMap* tmD, const __nv_bfloat16* C,
                                              int row, bool row_ok, int col_base, int N, int64_t ldd, int warp_row0,
-                                             uint32_t stage, int lane, int& store_cnt, WaitAcc wait_acc) {
+                                             uint32_t stage, int lane, int& store_cnt, RopeArgs rope,
+                                             WaitAcc wait_acc) {
   constexpr int NC = BN / 32;
   static_assert(NC % 2 == 0, "64-column store boxes");
+  if (ROPE && BN % 128 == 0 && rope.cs != nullptr && col_base < rope.cols) {  // tile-uniform: q / k heads
+    wait_acc();
+    const float2* cs_row = rope.cs + (int64_t)(row_ok ? row : 0) * 64;
+#pragma unroll 1
+    for (int hh = 0; hh < BN / 128; ++hh) {
+      const int col0 = col_base + hh * 128;
+      if (col0 >= N) break;
+      if (col0 < rope.cols)
+        epilogue_rope_head<BUFS>(tmem_row + hh * 128, cs_row, row_ok, col0, warp_row0, stage, lane, store_cnt, tmD);
+      else {  // a v head in the same tile: plain conversion
+        uint4 lo[8], hi[8];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          uint32_t r[32];
+          tmem_ld32(tmem_row + hh * 128 + h * 32, r);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            float f[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) f[j] = __uint_as_float(r[v * 8 + j]);
+            (h < 2 ? lo : hi)[(h & 1) * 4 + v] = pack8(f);
+          }
+        }
+        store_box<BUFS>(stage, lane, store_cnt, lo, tmD, col0, warp_row0);
+        store_box<BUFS>(stage, lane, store_cnt, hi, tmD, col0 + 64, warp_row0);
+      }
+    }
+    return;
+  }
   const __nv_bfloat16* crow = (C != nullptr && row_ok) ? C + (int64_t)row * ldd : nullptr;
   uint4 cpf[kCPre][4];
   auto cload = [&](int c, uint4* dst) {
@@ -111,29 +207,7 @@ __device__ __forceinline__ void epilogue_row(uint32_t tmem_row, const CUtensorMa
       if (crow && c + kCPre < NC) cload(c + kCPre, cpf[c % kCPre]);
     }
     if (col0 >= N) continue;  // warp-uniform: the whole box is past the last column
-    const int b = store_cnt % BUFS;
-    if (lane == 0) {
-      // the store that last used this buffer has finished reading it
-      if (BUFS == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-      else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-    }
-    __syncwarp();
-    const uint32_t box = stage + b * 4096;
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(box + lane * 128 + ((k ^ (lane & 7)) << 4)),
-                   "r"(packed[k].x), "r"(packed[k].y), "r"(packed[k].z), "r"(packed[k].w)
-                   : "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncwarp();
-    if (lane == 0) {
-      asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                       reinterpret_cast<uint64_t>(tmD)),
-                   "r"(box), "r"(col0), "r"(warp_row0)
-                   : "memory");
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    }
-    ++store_cnt;
+    store_box<BUFS>(stage, lane, store_cnt, packed, tmD, col0, warp_row0);
   }
   (void)row_ok;
 }
@@ -143,7 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmD,
                 __nv_bfloat16* __restrict__ D, const __nv_bfloat16* C /* may alias D */, int M, int N, int K,
-                int64_t ldd, int* __restrict__ sched) {
+                int64_t ldd, int* __restrict__ sched, RopeArgs rope) {
   ::kpo::pdl_launch_dependents();  // the next kernel may start its prologue; it waits for us
   using CF = Cfg<BN>;
   constexpr int STAGES = CF::STAGES;
@@ -300,9 +374,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       tile_coords(tile, num_m, num_n, mb, nb);
       const int acc = acc_it & 1;
       const int row = mb * BM + q * 32 + lane;
-      epilogue_row<BN, CF::EPI_BUFS>(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN, &tmD, C, row, row < M,
+      epilogue_row<BN, CF::EPI_BUFS, !A_MN && !B_MN>(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN, &tmD, C, row, row < M,
                                      nb * BN, N, ldd, mb * BM + q * 32,
-                                     smem_u32(smem + CF::EPI_OFF) + q * CF::EPI_BUFS * 4096, lane, store_cnt,
+                                     smem_u32(smem + CF::EPI_OFF) + q * CF::EPI_BUFS * 4096, lane, store_cnt, rope,
                        [&] {
                          mbar_wait(smem_u32(&tfull[acc]), (acc_it >> 1) & 1);
                          tc_fence_after();
@@ -325,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ------------------------------------------------------------------ host side
 template <int BN, bool A_MN, bool B_MN>
 static int launch(const CUtensorMap& ta, const CUtensorMap& tb, void* D, const void* C, int64_t M, int64_t N,
-                  int64_t K, int64_t ldd, int grid, int* sched, cudaStream_t s) {
+                  int64_t K, int64_t ldd, int grid, int* sched, cudaStream_t s, RopeArgs rope) {
   auto kern = gemm_kernel<BN, A_MN, B_MN>;
   CUtensorMap td;
   if (int e = make_map_2d(&td, D, N, M, ldd, 64, 32)) return e;
@@ -335,7 +409,7 @@ static int launch(const CUtensorMap& ta, const CUtensorMap& tb, void* D, const v
     attr_set = true;
   }
   KPO_CUDA(::kpo::pdl_launch(kern, grid, kThreads, Cfg<BN>::SMEM, s, ta, tb, td, (__nv_bfloat16*)D, (const __nv_bfloat16*)C, (int)M, (int)N,
-                                              (int)K, ldd, sched));
+                                              (int)K, ldd, sched, rope));
   KPO_LAUNCH_CHECK();
   return KPO_OK;
 }
@@ -371,7 +445,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmD,
                  __nv_bfloat16* __restrict__ D, const __nv_bfloat16* C /* may alias D */, int M, int N, int K,
-                 int64_t ldd, int* __restrict__ sched) {
+                 int64_t ldd, int* __restrict__ sched, RopeArgs rope) {
   ::kpo::pdl_launch_dependents();  // the next kernel may start its prologue; it waits for us
   using CF = Cfg2<BN>;
   constexpr int STAGES = CF::STAGES;
@@ -541,9 +615,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tile_coords(tile, num_m, num_n, mb, nb);
       const int acc = acc_it & 1;
       const int row = mb * 256 + (int)rank * 128 + q * 32 + lane;
-      epilogue_row<BN, CF::EPI_BUFS>(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN, &tmD, C, row, row < M,
+      epilogue_row<BN, CF::EPI_BUFS, !A_MN && !B_MN>(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN, &tmD, C, row, row < M,
                                      nb * BN, N, ldd, mb * 256 + (int)rank * 128 + q * 32,
-                                     smem_u32(smem + CF::EPI_OFF) + q * CF::EPI_BUFS * 4096, lane, store_cnt,
+                                     smem_u32(smem + CF::EPI_OFF) + q * CF::EPI_BUFS * 4096, lane, store_cnt, rope,
                        [&] {
                          mbar_wait(smem_u32(&tfull[acc]), (acc_it >> 1) & 1);
                          tc_fence_after();
@@ -564,7 +638,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
 template <int BN, bool A_MN, bool B_MN>
 static int launch2(const CUtensorMap& ta, const CUtensorMap& tb, void* D, const void* C, int64_t M, int64_t N,
-                   int64_t K, int64_t ldd, int grid, int* sched, cudaStream_t s) {
+                   int64_t K, int64_t ldd, int grid, int* sched, cudaStream_t s, RopeArgs rope) {
   auto kern = gemm2_kernel<BN, A_MN, B_MN>;
   CUtensorMap td;
   if (int e = make_map_2d(&td, D, N, M, ldd, 64, 32)) return e;
@@ -574,7 +648,7 @@ static int launch2(const CUtensorMap& ta, const CUtensorMap& tb, void* D, const 
     attr_set = true;
   }
   KPO_CUDA(::kpo::pdl_launch(kern, grid, kThreads, Cfg2<BN>::SMEM, s, ta, tb, td, (__nv_bfloat16*)D, (const __nv_bfloat16*)C, (int)M, (int)N,
-                                               (int)K, ldd, sched));
+                                               (int)K, ldd, sched, rope));
   KPO_LAUNCH_CHECK();
   return KPO_OK;
 }
@@ -641,9 +715,9 @@ int make_map_2d_f32(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t ou
 using namespace kpo;
 using namespace kpo::sm100;
 
-extern "C" int kpo_gemm(const void* A, const void* B, void* D, const void* C, int64_t M, int64_t N, int64_t K,
-                        int a_mn_major, int b_mn_major, int64_t lda, int64_t ldb, int64_t ldd, int max_ctas,
-                        int* sched, void* stream) {
+static int gemm_impl(const void* A, const void* B, void* D, const void* C, int64_t M, int64_t N, int64_t K,
+                     int a_mn_major, int b_mn_major, int64_t lda, int64_t ldb, int64_t ldd, int max_ctas, int* sched,
+                     void* stream, kpo::gemm::RopeArgs rope) {
   using namespace kpo::gemm;
   KPO_CHECK_ARG(A && B && D && sched, "gemm: null pointer");
   KPO_CHECK_ARG(M > 0 && N > 0 && K > 0, "gemm: M, N, K must be positive");
@@ -677,6 +751,7 @@ extern "C" int kpo_gemm(const void* A, const void* B, void* D, const void* C, in
   double best_eff = -1.0;
   for (const Choice& c : choices) {
     if (c.pair && (no_pair || M < 256)) continue;
+    if (rope.cs && c.bn % 128 != 0) continue;  // rope tiles hold whole 128-column heads
     const double e = eff(c);
     if (e > best_eff * 1.01) {
       best = c;
@@ -708,10 +783,10 @@ extern "C" int kpo_gemm(const void* A, const void* B, void* D, const void* C, in
     if (st2) return st2;
     cudaStream_t s2 = (cudaStream_t)stream;
 #define KPO_GEMM2_DISPATCH(BNv)                                                                                    \
-  if (!a_mn_major && !b_mn_major) return launch2<BNv, false, false>(ta2, tb2, D, C, M, N, K, ldd, grid2, sched, s2); \
-  if (!a_mn_major && b_mn_major) return launch2<BNv, false, true>(ta2, tb2, D, C, M, N, K, ldd, grid2, sched, s2);   \
-  if (a_mn_major && !b_mn_major) return launch2<BNv, true, false>(ta2, tb2, D, C, M, N, K, ldd, grid2, sched, s2);   \
-  return launch2<BNv, true, true>(ta2, tb2, D, C, M, N, K, ldd, grid2, sched, s2);
+  if (!a_mn_major && !b_mn_major) return launch2<BNv, false, false>(ta2, tb2, D, C, M, N, K, ldd, grid2, sched, s2, rope); \
+  if (!a_mn_major && b_mn_major) return launch2<BNv, false, true>(ta2, tb2, D, C, M, N, K, ldd, grid2, sched, s2, rope);   \
+  if (a_mn_major && !b_mn_major) return launch2<BNv, true, false>(ta2, tb2, D, C, M, N, K, ldd, grid2, sched, s2, rope);   \
+  return launch2<BNv, true, true>(ta2, tb2, D, C, M, N, K, ldd, grid2, sched, s2, rope);
     if (bn2 == 256) {
       KPO_GEMM2_DISPATCH(256)
     } else {
@@ -729,10 +804,10 @@ extern "C" int kpo_gemm(const void* A, const void* B, void* D, const void* C, in
   if (st) return st;
   cudaStream_t s = (cudaStream_t)stream;
 #define KPO_GEMM_DISPATCH(BNv)                                                                      \
-  if (!a_mn_major && !b_mn_major) return launch<BNv, false, false>(ta, tb, D, C, M, N, K, ldd, grid, sched, s); \
-  if (!a_mn_major && b_mn_major) return launch<BNv, false, true>(ta, tb, D, C, M, N, K, ldd, grid, sched, s);   \
-  if (a_mn_major && !b_mn_major) return launch<BNv, true, false>(ta, tb, D, C, M, N, K, ldd, grid, sched, s);   \
-  return launch<BNv, true, true>(ta, tb, D, C, M, N, K, ldd, grid, sched, s);
+  if (!a_mn_major && !b_mn_major) return launch<BNv, false, false>(ta, tb, D, C, M, N, K, ldd, grid, sched, s, rope); \
+  if (!a_mn_major && b_mn_major) return launch<BNv, false, true>(ta, tb, D, C, M, N, K, ldd, grid, sched, s, rope);   \
+  if (a_mn_major && !b_mn_major) return launch<BNv, true, false>(ta, tb, D, C, M, N, K, ldd, grid, sched, s, rope);   \
+  return launch<BNv, true, true>(ta, tb, D, C, M, N, K, ldd, grid, sched, s, rope);
   if (bn == 256) {
     KPO_GEMM_DISPATCH(256)
   } else if (bn == 192) {
@@ -741,4 +816,22 @@ extern "C" int kpo_gemm(const void* A, const void* B, void* D, const void* C, in
     KPO_GEMM_DISPATCH(128)
   }
 #undef KPO_GEMM_DISPATCH
+}
+
+extern "C" int kpo_gemm(const void* A, const void* B, void* D, const void* C, int64_t M, int64_t N, int64_t K,
+                        int a_mn_major, int b_mn_major, int64_t lda, int64_t ldb, int64_t ldd, int max_ctas,
+                        int* sched, void* stream) {
+  return gemm_impl(A, B, D, C, M, N, K, a_mn_major, b_mn_major, lda, ldb, ldd, max_ctas, sched, stream,
+                   kpo::gemm::RopeArgs{nullptr, 0});
+}
+
+extern "C" int kpo_gemm_rope(const void* A, const void* B, void* D, int64_t M, int64_t N, int64_t K, int64_t lda,
+                             int64_t ldb, int64_t ldd, int max_ctas, int* sched, const float* rope_table,
+                             int64_t rope_cols, int head_dim, void* stream) {
+  KPO_CHECK_ARG(rope_table, "gemm_rope: null rope table");
+  KPO_CHECK_ARG(head_dim == 128, "gemm_rope: the fused rotary epilogue handles head_dim 128");
+  KPO_CHECK_ARG(rope_cols > 0 && rope_cols % head_dim == 0 && rope_cols <= N,
+                "gemm_rope: rope_cols must be a positive multiple of head_dim within N");
+  return gemm_impl(A, B, D, nullptr, M, N, K, 0, 0, lda, ldb, ldd, max_ctas, sched, stream,
+                   kpo::gemm::RopeArgs{reinterpret_cast<const float2*>(rope_table), (int)rope_cols});
 }

@@ -215,6 +215,10 @@ class PartitionedLayer:
         rank0 = self.rank == 0
         W, dw = self.w, self.dw
         US = specs.unit_specs(wl)
+        fused = specs.fused_rope(wl)
+        qk_src = "qkv" if fused else "qkr"
+        if fused:
+            self.rope_cs = ops.rope_table(T, d, theta, self.device)
         self.units: dict[tuple[str, int], LaunchUnit] = {}
         kinds = {"attention_core": "attention", "attention_bwd": "attention"}
 
@@ -234,12 +238,15 @@ class PartitionedLayer:
             fns = {
                 # ---------------- forward
                 "norm1": lambda st, a=a: ops.rmsnorm_fwd(a["x"], W["g1"], a["xn1"], a["rstd1"], eps, stream=st),
-                "linear_qkv": lambda st, a=a, s=s: ops.linear(a["xn1"], W["wqkv"], a["qkv"], sched=s["linear_qkv"],
-                                                              stream=st),
+                "linear_qkv": (lambda st, a=a, s=s: ops.linear_rope(a["xn1"], W["wqkv"], a["qkv"], self.rope_cs, qd,
+                                                                    d, sched=s["linear_qkv"], stream=st))
+                if fused else (lambda st, a=a, s=s: ops.linear(a["xn1"], W["wqkv"], a["qkv"], sched=s["linear_qkv"],
+                                                              stream=st)),
                 "rope": lambda st, a=a: ops.rope(a["qkv"], a["qkr"], hq + hkv, d, theta, stream=st),
-                "attention_core": lambda st, a=a: ops.attn_fwd(a["qkr"][:, :hq * d], a["qkr"][:, hq * d:],
-                                                               a["qkv"][:, qd:], a["ao"], a["lse"], T, hq, hkv, d,
-                                                               scale, stream=st),
+                # with the fused rotary epilogue q / k are rotated in place in qkv
+                "attention_core": lambda st, a=a, qk=qk_src: ops.attn_fwd(a[qk][:, :hq * d], a[qk][:, hq * d:qd],
+                                                                          a["qkv"][:, qd:], a["ao"], a["lse"], T, hq,
+                                                                          hkv, d, scale, stream=st),
                 "linear_proj": lambda st, a=a, s=s, hp=hp, r=res_attn: ops.linear(
                     a["ao"], W["wo"], hp, residual=r, sched=s["linear_proj"], stream=st),
                 "norm2": lambda st, a=a: ops.rmsnorm_fwd(a["h"], W["g2"], a["xn2"], a["rstd2"], eps, stream=st),
@@ -268,8 +275,8 @@ class PartitionedLayer:
                                                                  stream=st),
                 "o_wgrad": lambda st, a=a, s=s, acc=acc: ops.linear_wgrad(
                     a["dh"], a["ao"], dw["wo"], accumulate=dw["wo"] if acc else None, sched=s["o_wgrad"], stream=st),
-                "attention_bwd": lambda st, a=a: ops.attn_bwd(
-                    a["qkr"][:, :hq * d], a["qkr"][:, hq * d:], a["qkv"][:, qd:], a["ao"], a["dao"], a["lse"],
+                "attention_bwd": lambda st, a=a, qk=qk_src: ops.attn_bwd(
+                    a[qk][:, :hq * d], a[qk][:, hq * d:qd], a["qkv"][:, qd:], a["ao"], a["dao"], a["lse"],
                     a["dqkr"][:, :hq * d], a["dqkr"][:, hq * d:], a["dqkv"][:, qd:], T, hq, hkv, d, scale,
                     self.attn_ws, stream=st),
                 "rope_bwd": lambda st, a=a: ops.rope(a["dqkr"], a["dqkv"], hq + hkv, d, theta, inverse=True,
@@ -321,7 +328,7 @@ class PartitionedLayer:
                 comm = self._ar_unit(arg, self.nb[arg[1]][out_of[arg[0]]])
             else:
                 comm = self._fsdp_unit(arg)
-            units = [self.units[(k, b)] for k in dict(specs.BLOCKS)[blk]]
+            units = [self.units[(k, b)] for k in dict(specs.blocks(self.wl))[blk]]
             self.programs[name] = PartitionProgram(name, units, comm, wl.world)
             self.order.append(name)
 

@@ -124,6 +124,25 @@ def linear(x: torch.Tensor, w: torch.Tensor, out: torch.Tensor, residual: torch.
     gemm_raw(x, w, out, M, N, K, False, False, C=residual, **kw)
 
 
+def rope_table(tokens: int, head_dim: int, theta: float, device, pos0: int = 0, stream=None) -> torch.Tensor:
+    """fp32 [tokens, head_dim/2, 2] (cos, sin) table for linear_rope."""
+    t = torch.empty(tokens, head_dim // 2, 2, dtype=torch.float32, device=device)
+    _lib.call("kpo_rope_table", tokens, head_dim, ctypes.c_float(theta), pos0, _ptr(t), _stream(stream))
+    return t
+
+
+def linear_rope(x: torch.Tensor, w: torch.Tensor, out: torch.Tensor, table: torch.Tensor, rope_cols: int,
+                head_dim: int = 128, max_ctas: int = 0, sched: int | None = None, stream=None) -> None:
+    """out = x @ w^T with the rotary embedding applied to output columns [0, rope_cols) in the epilogue."""
+    _need_cuda(x, w, out, table)
+    M, K = x.shape
+    N = w.shape[0]
+    if sched is None:
+        sched = default_sched(x.device)
+    _lib.call("kpo_gemm_rope", _ptr(x), _ptr(w), _ptr(out), M, N, K, x.stride(0), w.stride(0), out.stride(0),
+              max_ctas, sched, _ptr(table), rope_cols, head_dim, _stream(stream))
+
+
 def linear_dgrad(dy: torch.Tensor, w: torch.Tensor, dx: torch.Tensor, accumulate: torch.Tensor | None = None,
                  **kw) -> None:
     """dx[M,K] = dy[M,N] @ w[N,K]  (B is MN-major: w rows are the reduction dim)."""

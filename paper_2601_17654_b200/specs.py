@@ -10,6 +10,8 @@ which is what the reference's `comm_bytes / comm_rate` cost model consumes (simg
 
 from __future__ import annotations
 
+import os
+
 from .domain import KernelSpec, PartitionSpec
 from .model import Workload
 
@@ -18,6 +20,17 @@ FWD_MLP = ["norm2", "linear_up", "swiglu", "linear_down"]
 BWD_MLP = ["norm1_bwd", "down_dgrad", "down_wgrad", "swiglu_bwd", "gu_dgrad", "gu_wgrad"]
 BWD_ATTN = ["norm2_bwd", "o_dgrad", "o_wgrad", "attention_bwd", "rope_bwd", "qkv_dgrad", "qkv_wgrad"]
 BLOCKS = [("fwd_attn", FWD_ATTN), ("fwd_mlp", FWD_MLP), ("bwd_mlp", BWD_MLP), ("bwd_attn", BWD_ATTN)]
+
+
+def fused_rope(wl: Workload) -> bool:
+    """head_dim 128: the rotary embedding runs in the QKV GEMM's epilogue (kpo_gemm_rope), so the
+    forward attention partition has no separate "rope" launch unit."""
+    return wl.d == 128 and os.environ.get("KPO_FUSED_ROPE", "1") != "0"
+
+
+def blocks(wl: Workload) -> list[tuple[str, list[str]]]:
+    fa = [k for k in FWD_ATTN if k != "rope"] if fused_rope(wl) else FWD_ATTN
+    return [("fwd_attn", fa), ("fwd_mlp", FWD_MLP), ("bwd_mlp", BWD_MLP), ("bwd_attn", BWD_ATTN)]
 
 # FSDP comm units per partition: ('ag', t) all-gathers the next layer's weight t, ('rs', t)
 # reduce-scatters the previous layer's gradient of t (fused into one comm unit, compose.py:32-45).
@@ -114,5 +127,5 @@ def partition_specs(wl: Workload) -> list[PartitionSpec]:
         name = f"{blk}{b}"
         kind, arg = plan[name]
         cspec = ar_spec(wl, arg)[0] if kind == "ar" else fsdp_spec(wl, arg)[0]
-        out.append(PartitionSpec(tuple(us[k] for k in dict(BLOCKS)[blk]), cspec, wl.world, name))
+        out.append(PartitionSpec(tuple(us[k] for k in dict(blocks(wl))[blk]), cspec, wl.world, name))
     return out

@@ -181,3 +181,29 @@ def test_attention_fwd_lazy_rescale_divergent_rows(cuda, T, hq, hkv):
     torch.cuda.synchronize()
     ref = _attn_ref(q.float(), k.float(), v.float(), hq, hkv, d)
     assert rel_err(o.view(T, hq, d).transpose(0, 1), ref) < 1e-2
+
+
+@pytest.mark.parametrize("M,N,rope_cols", [(4096, 5120, 4096), (1000, 768, 512), (300, 384, 384)])
+def test_gemm_rope_epilogue(cuda, M, N, rope_cols):
+    """Fused rotary epilogue of the QKV projection vs fp32 GEMM + rotate-half of the q / k heads."""
+    from paper_2601_17654_b200 import ops
+    K, d, theta = 512, 128, 500000.0
+    g = torch.Generator(device="cuda").manual_seed(M + N)
+    x = torch.randn(M, K, device=cuda, generator=g).bfloat16()
+    w = torch.randn(N, K, device=cuda, generator=g).bfloat16()
+    out = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+    table = ops.rope_table(M, d, theta, cuda)
+    ops.linear_rope(x, w, out, table, rope_cols, d)
+    torch.cuda.synchronize()
+    ref = x.float() @ w.float().t()
+    half = d // 2
+    inv = theta ** (-(torch.arange(half, dtype=torch.float64, device=cuda) * 2 / d))
+    ang = torch.arange(M, dtype=torch.float64, device=cuda)[:, None] * inv[None]
+    c, s_ = ang.cos().float(), ang.sin().float()
+    qk = ref[:, :rope_cols].view(M, rope_cols // d, d)
+    a, b = qk[..., :half], qk[..., half:]
+    rot = torch.cat([a * c[:, None] - b * s_[:, None], b * c[:, None] + a * s_[:, None]], -1).view(M, rope_cols)
+    ref = torch.cat([rot, ref[:, rope_cols:]], 1)
+    assert rel_err(out, ref) < 8e-3
+    # table entries: fp32 angle arithmetic like the separate rope kernel (angle rounding ~ pos * 2^-24)
+    assert torch.allclose(table[:, :, 0], c, atol=1e-3) and torch.allclose(table[:, :, 1], s_, atol=1e-3)

@@ -137,6 +137,14 @@ int kpo_embedding_bwd(const int32_t* ids, const void* dy, float* dtable, int64_t
 int kpo_cross_entropy(const void* logits, void* dlogits, const int32_t* labels, float* loss, int64_t tokens,
                       int64_t vocab, int64_t ld, float grad_scale, int ignore_index, void* stream);
 
+/* kpo_attn_bwd for q / k that were rotated by kpo_gemm_rope: dq and dk come out inverse-rotated
+ * (gradients w.r.t. the un-rotated projections), fusing the reference's "rope" backward.  head_dim 128. */
+int kpo_attn_bwd_rope(const void* q, const void* k, const void* v, const void* o, const void* dout,
+                      const float* lse, void* dq, void* dk, void* dv, int64_t T, int hq, int hkv, int d,
+                      int64_t q_stride, int64_t k_stride, int64_t v_stride, int64_t o_stride,
+                      int64_t dq_stride, int64_t dk_stride, int64_t dv_stride, float scale, int causal,
+                      void* workspace, const float* rope_table, void* stream);
+
 /* ---------------------------------------------------------------- SM-budgeted collectives */
 /* A communicator owns one symmetric buffer per rank (IPC-exported) plus per-CTA flag words.
  * world > 1, loopback == 0: one process per GPU; exchange kpo_comm_ipc_handle() blobs (out of band,

@@ -58,6 +58,9 @@ SIGNATURES = {
     "kpo_embedding_bwd": (_i32, [_c_void_p, _c_void_p, _c_void_p, _i64, _i64, _i64, _c_void_p]),
     "kpo_cross_entropy": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _i64, _i64, _i64, _f32, _i32,
                                  _c_void_p]),
+    "kpo_attn_bwd_rope": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p,
+                                 _c_void_p, _c_void_p, _i64, _i32, _i32, _i32, _i64, _i64, _i64, _i64, _i64, _i64,
+                                 _i64, _f32, _i32, _c_void_p, _c_void_p, _c_void_p]),
     "kpo_comm_create": (_i32, [_i32, _i32, _i32, _size, _i32, ctypes.POINTER(_c_void_p)]),
     "kpo_comm_ipc_handle": (_i32, [_c_void_p, _c_void_p]),
     "kpo_comm_open_peers": (_i32, [_c_void_p, _c_void_p]),

@@ -15,7 +15,7 @@ int attn_fwd_tcgen05(const void* q, const void* k, const void* v, void* o, float
 int attn_bwd_tcgen05_main(const void* q, const void* k, const void* v, const void* dout, const float* lse,
                           const float* dvec, float* dq_acc, void* dk, void* dv, int64_t T, int hq, int hkv, int d,
                           int64_t qs, int64_t ks, int64_t vs, int64_t os, int64_t dks, int64_t dvs, float scale,
-                          int causal, float* dkv_acc, cudaStream_t st);
+                          int causal, float* dkv_acc, cudaStream_t st, const float* rope_table);
 }
 
 namespace kpo {
@@ -293,6 +293,37 @@ __global__ void attn_bwd_post_kernel(const float* __restrict__ dq_acc, __nv_bflo
   *reinterpret_cast<uint4*>(dq + (int64_t)t * dqs + (int64_t)h * D + c) = pack8(f);
 }
 
+// fp32 accumulator -> bf16 with the inverse rotary embedding of token t (pairs (i, i + D/2));
+// one thread per 8 pairs.  Used for dQ (and split-mode dK) when the forward rotated q / k in the
+// QKV GEMM epilogue.
+template <int D>
+__global__ void attn_bwd_post_rope_kernel(const float* __restrict__ acc, __nv_bfloat16* __restrict__ out, int T,
+                                          int heads, int64_t os, const float2* __restrict__ cs) {
+  KPO_PDL_ENTRY();
+  constexpr int H = D / 2;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = (int64_t)T * heads * (H / 8);
+  if (i >= total) return;
+  const int64_t th = i / (H / 8);
+  const int i0 = (int)(i % (H / 8)) * 8;
+  const int t = (int)(th / heads), h = (int)(th % heads);
+  const float* src = acc + th * D;
+  const float4 a0 = *reinterpret_cast<const float4*>(src + i0), a1 = *reinterpret_cast<const float4*>(src + i0 + 4);
+  const float4 b0 = *reinterpret_cast<const float4*>(src + H + i0), b1 = *reinterpret_cast<const float4*>(src + H + i0 + 4);
+  const float xa[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+  const float xb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+  float oa[8], ob[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float2 r = cs[(int64_t)t * H + i0 + j];
+    oa[j] = xa[j] * r.x + xb[j] * r.y;
+    ob[j] = xb[j] * r.x - xa[j] * r.y;
+  }
+  __nv_bfloat16* dst = out + (int64_t)t * os + (int64_t)h * D;
+  *reinterpret_cast<uint4*>(dst + i0) = pack8(oa);
+  *reinterpret_cast<uint4*>(dst + H + i0) = pack8(ob);
+}
+
 template <int D>
 struct BwdCfg {
   static constexpr int BN = 64, BM = 64, WARPS = 4, NT = WARPS * 32;
@@ -523,7 +554,8 @@ template <int D>
 static int bwd_launch(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse,
                       void* dq, void* dk, void* dv, int64_t T, int hq, int hkv, int64_t qs, int64_t ks, int64_t vs,
                       int64_t os, int64_t dqs, int64_t dks, int64_t dvs, float scale, int causal, void* ws,
-                      cudaStream_t s, bool use_tc) {
+                      cudaStream_t s, bool use_tc, const float* rope_table = nullptr) {
+  const float2* rope_cs = reinterpret_cast<const float2*>(rope_table);
   using CF = BwdCfg<D>;
   float* dq_acc = (float*)ws;
   float* dvec = dq_acc + T * hq * D;
@@ -541,11 +573,15 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* o
     float* dkv_acc = split ? dvec + (int64_t)hq * T : nullptr;
     if (split) KPO_CUDA(cudaMemsetAsync(dkv_acc, 0, sizeof(float) * 2 * T * hkv * D, s));
     int st = attn_bwd_tcgen05_main(q, k, v, dout, lse, dvec, dq_acc, dk, dv, T, hq, hkv, D, qs, ks, vs, os, dks, dvs,
-                                   scale, causal, dkv_acc, s);
+                                   scale, causal, dkv_acc, s, rope_table);
     if (st) return st;
     if (split) {
       const int64_t n = T * hkv * D / 8;
-      KPO_CUDA(::kpo::pdl_launch(attn_bwd_post_kernel<D>, (unsigned)((n + 255) / 256), 256, 0, s, dkv_acc, (__nv_bfloat16*)dk, (int)T, hkv, dks));
+      if (rope_cs)
+        KPO_CUDA(::kpo::pdl_launch(attn_bwd_post_rope_kernel<D>, (unsigned)((n / 2 + 255) / 256), 256, 0, s, dkv_acc,
+                                   (__nv_bfloat16*)dk, (int)T, hkv, dks, rope_cs));
+      else
+        KPO_CUDA(::kpo::pdl_launch(attn_bwd_post_kernel<D>, (unsigned)((n + 255) / 256), 256, 0, s, dkv_acc, (__nv_bfloat16*)dk, (int)T, hkv, dks));
       KPO_LAUNCH_CHECK();
       KPO_CUDA(::kpo::pdl_launch(attn_bwd_post_kernel<D>, (unsigned)((n + 255) / 256), 256, 0, s, dkv_acc + T * hkv * D, (__nv_bfloat16*)dv,
                                                                            (int)T, hkv, dvs));
@@ -565,7 +601,11 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* o
   }
   {
     const int64_t n = T * hq * D / 8;
-    KPO_CUDA(::kpo::pdl_launch(attn_bwd_post_kernel<D>, (unsigned)((n + 255) / 256), 256, 0, s, dq_acc, (__nv_bfloat16*)dq, (int)T, hq, dqs));
+    if (rope_cs)
+      KPO_CUDA(::kpo::pdl_launch(attn_bwd_post_rope_kernel<D>, (unsigned)((n / 2 + 255) / 256), 256, 0, s, dq_acc,
+                                 (__nv_bfloat16*)dq, (int)T, hq, dqs, rope_cs));
+    else
+      KPO_CUDA(::kpo::pdl_launch(attn_bwd_post_kernel<D>, (unsigned)((n + 255) / 256), 256, 0, s, dq_acc, (__nv_bfloat16*)dq, (int)T, hq, dqs));
     KPO_LAUNCH_CHECK();
   }
   return KPO_OK;
@@ -623,4 +663,19 @@ extern "C" int kpo_attn_bwd(const void* q, const void* k, const void* v, const v
                                  o_stride, dq_stride, dk_stride, dv_stride, scale, causal, workspace, s, true);
   return attn::bwd_launch<64>(q, k, v, o, dout, lse, dq, dk, dv, T, hq, hkv, q_stride, k_stride, v_stride, o_stride,
                               dq_stride, dk_stride, dv_stride, scale, causal, workspace, s, false);
+}
+
+extern "C" int kpo_attn_bwd_rope(const void* q, const void* k, const void* v, const void* o, const void* dout,
+                                 const float* lse, void* dq, void* dk, void* dv, int64_t T, int hq, int hkv, int d,
+                                 int64_t q_stride, int64_t k_stride, int64_t v_stride, int64_t o_stride,
+                                 int64_t dq_stride, int64_t dk_stride, int64_t dv_stride, float scale, int causal,
+                                 void* workspace, const float* rope_table, void* stream) {
+  KPO_CHECK_ARG(q && k && v && o && dout && lse && dq && dk && dv && workspace && rope_table,
+                "attn_bwd_rope: null pointer");
+  KPO_CHECK_ARG(attn_args_ok(T, hq, hkv, d) && d == 128 && T % 8 == 0,
+                "attn_bwd_rope: the fused inverse rotary path needs head_dim 128 and T %% 8 == 0");
+  KPO_CHECK_ARG(((uintptr_t)workspace & 15) == 0, "attn_bwd_rope: workspace must be 16B aligned");
+  return attn::bwd_launch<128>(q, k, v, o, dout, lse, dq, dk, dv, T, hq, hkv, q_stride, k_stride, v_stride, o_stride,
+                               dq_stride, dk_stride, dv_stride, scale, causal, workspace, (cudaStream_t)stream, true,
+                               rope_table);
 }

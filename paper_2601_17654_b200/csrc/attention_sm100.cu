@@ -375,7 +375,9 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
                        const float* __restrict__ lse, const float* __restrict__ dvec, float* __restrict__ dq_acc,
                        __nv_bfloat16* __restrict__ dk, __nv_bfloat16* __restrict__ dv, int T, int hq, int hkv,
                        int64_t dks, int64_t dvs, float scale, int causal, float* __restrict__ dkv_acc,
-                       int ablate) {
+                       int ablate, const float2* __restrict__ rope_cs) {
+  // rope_cs != nullptr: dK leaves inverse-rotated (the gradient w.r.t. the un-rotated k), the fused
+  // backward of the QKV GEMM's rotary epilogue; dQ is rotated by the dq conversion kernel
   ::kpo::pdl_launch_dependents();  // the next kernel may start its prologue; it waits for us
   // ablate (KPO_ATTN_BWD_ABLATE, measurement only; results are wrong when != 0): 1 = no dQ reduce-add,
   // 2 = no dQ drain (TMEM -> smem), 4 = no exponentials, 8 = no dQ^T MMA, 16 = no softmax,
@@ -627,6 +629,32 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
       const uint32_t col = which ? C::COL_DV : C::COL_DK;
       const float mul = which ? 1.f : scale;
       __nv_bfloat16* row = which ? dv + (int64_t)key * dvs + (int64_t)kvh * D : dk + (int64_t)key * dks + (int64_t)kvh * D;
+      if (which == 0 && rope_cs != nullptr && !split) {
+        // inverse rotary: pairs (i, i + D/2) of the key's row, (cos, sin) of the key position
+        const float2* cs = rope_cs + (int64_t)(key < T ? key : 0) * (D / 2);
+#pragma unroll 1
+        for (int c = 0; c < D / 64; ++c) {
+          uint32_t va[32], vb[32];
+          tmem_ld32_nowait(lane_addr + col + c * 32, va);
+          tmem_ld32_nowait(lane_addr + col + D / 2 + c * 32, vb);
+          tmem_wait_ld();
+          if (ok) {
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              float oa[8], ob[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float2 t = cs[c * 32 + q4 * 8 + j];
+                const float x = __uint_as_float(va[q4 * 8 + j]) * mul, y = __uint_as_float(vb[q4 * 8 + j]) * mul;
+                oa[j] = x * t.x + y * t.y;
+                ob[j] = y * t.x - x * t.y;
+              }
+              *reinterpret_cast<uint4*>(row + c * 32 + q4 * 8) = pack8(oa);
+              *reinterpret_cast<uint4*>(row + D / 2 + c * 32 + q4 * 8) = pack8(ob);
+            }
+          }
+        }
+      } else {
 #pragma unroll 1
       for (int c = 0; c < D / 32; ++c) {
         uint32_t v[32];
@@ -650,6 +678,7 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
             *reinterpret_cast<uint4*>(row + c * 32 + q4 * 8) = u;
           }
         }
+      }
       }
       if (!ok && !split && steps == 0 && key < T) {  // no causal work: gradients are zero
         for (int c = 0; c < D; c += 8) *reinterpret_cast<uint4*>(row + c) = make_uint4(0, 0, 0, 0);
@@ -706,7 +735,8 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
 template <int D>
 int bwd_launch(const void* q, const void* k, const void* v, const void* dout, const float* lse, const float* dvec,
                float* dq_acc, void* dk, void* dv, int64_t T, int hq, int hkv, int64_t qs, int64_t ks, int64_t vs,
-               int64_t os, int64_t dks, int64_t dvs, float scale, int causal, float* dkv_acc, cudaStream_t st) {
+               int64_t os, int64_t dks, int64_t dvs, float scale, int causal, float* dkv_acc, cudaStream_t st,
+               const float* rope_table) {
   using C = Bwd<D>;
   CUtensorMap mq, mk, mv, mo, mdq;
   int e;
@@ -723,7 +753,8 @@ int bwd_launch(const void* q, const void* k, const void* v, const void* dout, co
   dim3 grid((unsigned)(dkv_acc ? hq : hkv), (unsigned)((T + C::BN - 1) / C::BN));
   KPO_CUDA(::kpo::pdl_launch(attn_bwd_tc_kernel<D>, grid, C::THREADS, C::SMEM, st, mq, mk, mv, mo, mdq, lse, dvec, dq_acc, (__nv_bfloat16*)dk,
                                                           (__nv_bfloat16*)dv, (int)T, hq, hkv, dks, dvs, scale, causal,
-                                                          dkv_acc, getenv("KPO_ATTN_BWD_ABLATE") ? atoi(getenv("KPO_ATTN_BWD_ABLATE")) : 0));
+                                                          dkv_acc, getenv("KPO_ATTN_BWD_ABLATE") ? atoi(getenv("KPO_ATTN_BWD_ABLATE")) : 0,
+                                                          reinterpret_cast<const float2*>(rope_table)));
   KPO_LAUNCH_CHECK();
   return KPO_OK;
 }
@@ -739,13 +770,13 @@ int attn_fwd_tcgen05(const void* q, const void* k, const void* v, void* o, float
 int attn_bwd_tcgen05_main(const void* q, const void* k, const void* v, const void* dout, const float* lse,
                           const float* dvec, float* dq_acc, void* dk, void* dv, int64_t T, int hq, int hkv, int d,
                           int64_t qs, int64_t ks, int64_t vs, int64_t os, int64_t dks, int64_t dvs, float scale,
-                          int causal, float* dkv_acc, cudaStream_t st) {
+                          int causal, float* dkv_acc, cudaStream_t st, const float* rope_table) {
   if (d != 128) {
     set_error("attn_bwd tcgen05 path needs head_dim 128");
     return KPO_ERR_UNSUPPORTED;
   }
   return attn_tc::bwd_launch<128>(q, k, v, dout, lse, dvec, dq_acc, dk, dv, T, hq, hkv, qs, ks, vs, os, dks, dvs,
-                                  scale, causal, dkv_acc, st);
+                                  scale, causal, dkv_acc, st, rope_table);
 }
 
 }  // namespace kpo

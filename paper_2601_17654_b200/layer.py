@@ -275,10 +275,13 @@ class PartitionedLayer:
                                                                  stream=st),
                 "o_wgrad": lambda st, a=a, s=s, acc=acc: ops.linear_wgrad(
                     a["dh"], a["ao"], dw["wo"], accumulate=dw["wo"] if acc else None, sched=s["o_wgrad"], stream=st),
-                "attention_bwd": lambda st, a=a, qk=qk_src: ops.attn_bwd(
-                    a[qk][:, :hq * d], a[qk][:, hq * d:qd], a["qkv"][:, qd:], a["ao"], a["dao"], a["lse"],
+                "attention_bwd": (lambda st, a=a: ops.attn_bwd(
+                    a["qkv"][:, :hq * d], a["qkv"][:, hq * d:qd], a["qkv"][:, qd:], a["ao"], a["dao"], a["lse"],
+                    a["dqkv"][:, :hq * d], a["dqkv"][:, hq * d:qd], a["dqkv"][:, qd:], T, hq, hkv, d, scale,
+                    self.attn_ws, stream=st, rope_table=self.rope_cs)) if fused else (lambda st, a=a: ops.attn_bwd(
+                    a["qkr"][:, :hq * d], a["qkr"][:, hq * d:], a["qkv"][:, qd:], a["ao"], a["dao"], a["lse"],
                     a["dqkr"][:, :hq * d], a["dqkr"][:, hq * d:], a["dqkv"][:, qd:], T, hq, hkv, d, scale,
-                    self.attn_ws, stream=st),
+                    self.attn_ws, stream=st)),
                 "rope_bwd": lambda st, a=a: ops.rope(a["dqkr"], a["dqkv"], hq + hkv, d, theta, inverse=True,
                                                      stream=st),
                 "qkv_dgrad": lambda st, a=a, s=s, o=dxn1p: ops.linear_dgrad(a["dqkv"], W["wqkv"], o,
@@ -348,23 +351,24 @@ class PartitionedLayer:
         once per nanobatch, each collective right after the unit that produces its input."""
         st = stream or torch.cuda.current_stream()
         tp = self.wl.parallel == "tp"
+        blk = dict(specs.blocks(self.wl))  # unit lists (no separate rope units when RoPE is fused)
         for b in range(self.wl.nanobatches):
             a = self.nb[b]
-            for k in ["norm1", "linear_qkv", "rope", "attention_core", "linear_proj"]:
+            for k in blk["fwd_attn"]:
                 self.units[(k, b)].fn(st)
             if tp:
                 self.comm.all_reduce(self.partial[b % 2][("hp", b)], self.stage, a["h"], ncta, stream=st)
-            for k in ["norm2", "linear_up", "swiglu", "linear_down"]:
+            for k in blk["fwd_mlp"]:
                 self.units[(k, b)].fn(st)
             if tp:
                 self.comm.all_reduce(self.partial[b % 2][("yp", b)], self.stage, a["y"], ncta, stream=st)
         for b in range(self.wl.nanobatches):
             a = self.nb[b]
-            for k in ["down_dgrad", "down_wgrad", "swiglu_bwd", "gu_dgrad", "gu_wgrad"]:
+            for k in [u for u in blk["bwd_mlp"] if u != "norm1_bwd"]:
                 self.units[(k, b)].fn(st)
             if tp:
                 self.comm.all_reduce(self.partial[b % 2][("dxn2p", b)], self.stage, a["dxn2"], ncta, stream=st)
-            for k in ["norm2_bwd", "o_dgrad", "o_wgrad", "attention_bwd", "rope_bwd", "qkv_dgrad", "qkv_wgrad"]:
+            for k in blk["bwd_attn"]:
                 self.units[(k, b)].fn(st)
             if tp:
                 self.comm.all_reduce(self.partial[b % 2][("dxn1p", b)], self.stage, a["dxn1"], ncta, stream=st)

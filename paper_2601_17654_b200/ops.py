@@ -181,13 +181,20 @@ def attn_bwd_workspace(T: int, hq: int, hkv: int, d: int, device) -> torch.Tenso
     return torch.empty(n, dtype=torch.uint8, device=device)
 
 
-def attn_bwd(q, k, v, o, dout, lse, dq, dk, dv, T, hq, hkv, d, scale, workspace, causal=True, stream=None):
-    _need_cuda(q, k, v, o, dout, lse, dq, dk, dv, workspace)
+def attn_bwd(q, k, v, o, dout, lse, dq, dk, dv, T, hq, hkv, d, scale, workspace, causal=True, stream=None,
+             rope_table=None):
+    """rope_table (from rope_table()): q / k were rotated by linear_rope, so dq / dk are returned
+    inverse-rotated (the fused backward of the rotary embedding)."""
+    _need_cuda(q, k, v, o, dout, lse, dq, dk, dv, workspace, rope_table)
     if dout.stride(0) != o.stride(0):
         raise ValueError("attn_bwd: dout must share o's token stride")
-    _lib.call("kpo_attn_bwd", _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(dout), _ptr(lse), _ptr(dq), _ptr(dk),
-              _ptr(dv), T, hq, hkv, d, q.stride(0), k.stride(0), v.stride(0), o.stride(0), dq.stride(0),
-              dk.stride(0), dv.stride(0), ctypes.c_float(scale), int(causal), _ptr(workspace), _stream(stream))
+    args = (_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(dout), _ptr(lse), _ptr(dq), _ptr(dk), _ptr(dv), T, hq, hkv, d,
+            q.stride(0), k.stride(0), v.stride(0), o.stride(0), dq.stride(0), dk.stride(0), dv.stride(0),
+            ctypes.c_float(scale), int(causal), _ptr(workspace))
+    if rope_table is None:
+        _lib.call("kpo_attn_bwd", *args, _stream(stream))
+    else:
+        _lib.call("kpo_attn_bwd_rope", *args, _ptr(rope_table), _stream(stream))
 
 
 # ------------------------------------------------------------------ non-partition work (nonpart.cu)

@@ -29,8 +29,11 @@ def fused_rope(wl: Workload) -> bool:
 
 
 def blocks(wl: Workload) -> list[tuple[str, list[str]]]:
-    fa = [k for k in FWD_ATTN if k != "rope"] if fused_rope(wl) else FWD_ATTN
-    return [("fwd_attn", fa), ("fwd_mlp", FWD_MLP), ("bwd_mlp", BWD_MLP), ("bwd_attn", BWD_ATTN)]
+    if not fused_rope(wl):
+        return list(BLOCKS)
+    fa = [k for k in FWD_ATTN if k != "rope"]
+    ba = [k for k in BWD_ATTN if k != "rope_bwd"]  # dq / dk leave attention backward inverse-rotated
+    return [("fwd_attn", fa), ("fwd_mlp", FWD_MLP), ("bwd_mlp", BWD_MLP), ("bwd_attn", ba)]
 
 # FSDP comm units per partition: ('ag', t) all-gathers the next layer's weight t, ('rs', t)
 # reduce-scatters the previous layer's gradient of t (fused into one comm unit, compose.py:32-45).

@@ -207,3 +207,33 @@ def test_gemm_rope_epilogue(cuda, M, N, rope_cols):
     assert rel_err(out, ref) < 8e-3
     # table entries: fp32 angle arithmetic like the separate rope kernel (angle rounding ~ pos * 2^-24)
     assert torch.allclose(table[:, :, 0], c, atol=1e-3) and torch.allclose(table[:, :, 1], s_, atol=1e-3)
+
+
+@pytest.mark.parametrize("T,hq,hkv", [(1024, 8, 2), (512, 4, 1)])
+def test_attention_bwd_rope_fused(cuda, T, hq, hkv):
+    """attn_bwd with the fused inverse rotary (q / k rotated by the QKV epilogue) equals attn_bwd followed
+    by the separate inverse rope kernel on dq / dk (both split-group and grouped dK paths)."""
+    from paper_2601_17654_b200 import ops
+    d, theta = 128, 500000.0
+    g = torch.Generator(device="cuda").manual_seed(T + hq)
+    qkv = torch.randn(T, (hq + 2 * hkv) * d, device=cuda, generator=g).bfloat16()
+    qd = (hq + hkv) * d
+    q, k, v = qkv[:, :hq * d], qkv[:, hq * d:qd], qkv[:, qd:]
+    o = torch.empty(T, hq * d, device=cuda, dtype=torch.bfloat16)
+    lse = torch.empty(hq, T, device=cuda)
+    scale = 1 / math.sqrt(d)
+    ops.attn_fwd(q, k, v, o, lse, T, hq, hkv, d, scale)
+    dout = torch.randn_like(o)
+    ws = ops.attn_bwd_workspace(T, hq, hkv, d, cuda)
+    table = ops.rope_table(T, d, theta, cuda)
+    d1 = torch.empty_like(qkv)
+    ops.attn_bwd(q, k, v, o, dout, lse, d1[:, :hq * d], d1[:, hq * d:qd], d1[:, qd:], T, hq, hkv, d, scale, ws,
+                 rope_table=table)
+    d0 = torch.empty_like(qkv)
+    ops.attn_bwd(q, k, v, o, dout, lse, d0[:, :hq * d], d0[:, hq * d:qd], d0[:, qd:], T, hq, hkv, d, scale, ws)
+    ref = torch.empty_like(qkv)
+    ref[:, qd:] = d0[:, qd:]
+    ops.rope(d0, ref, hq + hkv, d, theta, inverse=True)
+    torch.cuda.synchronize()
+    assert rel_err(d1[:, :qd], ref[:, :qd]) < 1e-2
+    assert rel_err(d1[:, qd:], ref[:, qd:]) < 1e-2

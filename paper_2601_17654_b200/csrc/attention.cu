@@ -255,25 +255,30 @@ template <int D>
 __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
                                     float* __restrict__ dvec, float* __restrict__ dq_acc, int T, int hq,
                                     int64_t os) {
+  // D[h][t] = sum_d O[t,h,d] dO[t,h,d] and zero the fp32 dQ accumulator: one thread per 8 elements,
+  // D/8 consecutive lanes per (t, h) row, reduced with shuffles inside the lane group
   KPO_PDL_ENTRY();
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (gw >= (int64_t)T * hq) return;
-  const int t = (int)(gw / hq), h = (int)(gw % hq);
-  const __nv_bfloat16* orow = o + (int64_t)t * os + (int64_t)h * D;
-  const __nv_bfloat16* drow = dout + (int64_t)t * os + (int64_t)h * D;
+  constexpr int G = D / 8;  // lanes per row (16 for D = 128, 8 for D = 64)
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t row = gt / G;
+  const int c = (int)(gt % G) * 8;
+  const bool ok = row < (int64_t)T * hq;
+  const int t = ok ? (int)(row / hq) : 0, h = ok ? (int)(row % hq) : 0;
   float acc = 0.f;
-  for (int c = lane * 8; c < D; c += 256) {
+  if (ok) {
     float a[8], b[8];
-    unpack8(*reinterpret_cast<const uint4*>(orow + c), a);
-    unpack8(*reinterpret_cast<const uint4*>(drow + c), b);
+    unpack8(*reinterpret_cast<const uint4*>(o + (int64_t)t * os + (int64_t)h * D + c), a);
+    unpack8(*reinterpret_cast<const uint4*>(dout + (int64_t)t * os + (int64_t)h * D + c), b);
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc += a[j] * b[j];
   }
-  acc = warp_sum(acc);
-  if (lane == 0) dvec[(int64_t)h * T + t] = acc;
-  float4* dq = reinterpret_cast<float4*>(dq_acc + ((int64_t)t * hq + h) * D);
-  for (int c = lane; c < D / 4; c += 32) dq[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (!ok) return;
+  if (c == 0) dvec[(int64_t)h * T + t] = acc;
+  float4* dq = reinterpret_cast<float4*>(dq_acc + ((int64_t)t * hq + h) * D + c);
+  dq[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+  dq[1] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 template <int D>
@@ -560,8 +565,8 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* o
   float* dq_acc = (float*)ws;
   float* dvec = dq_acc + T * hq * D;
   {
-    const int64_t warps = T * hq;
-    KPO_CUDA(::kpo::pdl_launch(attn_bwd_pre_kernel<D>, (unsigned)((warps * 32 + 255) / 256), 256, 0, s, 
+    const int64_t threads = T * hq * (D / 8);
+    KPO_CUDA(::kpo::pdl_launch(attn_bwd_pre_kernel<D>, (unsigned)((threads + 255) / 256), 256, 0, s, 
         (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, dvec, dq_acc, (int)T, hq, os));
     KPO_LAUNCH_CHECK();
   }

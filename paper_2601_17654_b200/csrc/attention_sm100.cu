@@ -299,6 +299,286 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
 }
 
+// -------------------------------------------------------------------------------------------------
+// Forward, two Q tiles per CTA (256 query rows).  Each softmax warpgroup owns one 128-row Q tile and
+// one O accumulator; the two groups are fed by different S MMAs at different times, so on every SM
+// sub-partition one warp's exponentials (MUFU) overlap the other warp's TMEM loads / row max / P
+// stores, and every K / V tile feeds four MMAs (2 S + 2 PV) instead of two.
+//   warps 0-3  softmax Q tile 0 (TMEM lanes = rows), warps 4-7 softmax Q tile 1   (setmaxnreg 232)
+//   warp 8     TMA producer (Q0, Q1 once; K / V 2-stage rings)                    (setmaxnreg 40)
+//   warp 9     TMEM allocator + MMA issuer; warps 10-11 idle
+//   TMEM: S0 0..127, S1 128..255 (P_g written over the first 64 columns of S_g), O0 256..383, O1 384..511
+//   MMA order: S0_0, S1_0, then per KV tile j: PV0_j, S0_{j+1}, PV1_j, S1_{j+1}
+// A commit after S_g(j) completes only when every earlier MMA of the issuer has (in particular
+// PV_g(j-1)), so a softmax group can rescale O_g as soon as it has seen S_g(j).
+template <int D>
+struct Fwd2 {
+  static constexpr int BM = 128, BN = 128, KS = 2, VS = 2;
+  static constexpr int Q_BYTES = BM * D * 2;
+  static constexpr int KV_BYTES = BN * D * 2;
+  static constexpr int OFF_Q = 0;  // Q0, Q1
+  static constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
+  static constexpr int OFF_V = OFF_K + KS * KV_BYTES;
+  static constexpr int OFF_BAR = OFF_V + VS * KV_BYTES;
+  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+  static constexpr int COL_S0 = 0, COL_S1 = 128, COL_O0 = 256, COL_O1 = 384;
+  static constexpr int THREADS = 384;
+};
+
+template <int D>
+__global__ void __launch_bounds__(384, 1)
+    attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                        const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ o,
+                        float* __restrict__ lse, int T, int hq, int hkv, int64_t os, float scale_log2, int causal,
+                        int pingpong) {
+  ::kpo::pdl_launch_dependents();
+  using C = Fwd2<D>;
+  constexpr int BM = C::BM, BN = C::BN, KSUB = D / 64;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* q_full = bar + 0;
+  uint64_t* k_full = bar + 1;    // [2]
+  uint64_t* k_empty = bar + 3;   // [2]
+  uint64_t* v_full = bar + 5;    // [2]
+  uint64_t* v_empty = bar + 7;   // [2]
+  uint64_t* s_full = bar + 9;    // [2] per Q tile
+  uint64_t* p_full = bar + 11;   // [2] per Q tile (4 warps)
+  uint64_t* pv_done = bar + 13;  // [2] per Q tile
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 15);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mblk = gridDim.y - 1 - blockIdx.y;  // heavy (late) causal rows first
+  const int h = blockIdx.x;
+  const int kvh = h / (hq / hkv);
+  const int m0 = mblk * 2 * BM;
+  const int tiles_all = (T + BN - 1) / BN;
+  int n_g[2];
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
+    n_g[g] = tiles_all;
+    if (causal) n_g[g] = min(tiles_all, (m0 + g * BM + BM + BN - 1) / BN);
+    if (m0 + g * BM >= T) n_g[g] = 0;  // Q tile 1 past the end
+  }
+  const int n_all = max(n_g[0], n_g[1]);
+
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(q_full), 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&k_full[i]), 1);
+      mbar_init(smem_u32(&k_empty[i]), 1);
+      mbar_init(smem_u32(&v_full[i]), 1);
+      mbar_init(smem_u32(&v_empty[i]), 1);
+      mbar_init(smem_u32(&s_full[i]), 1);
+      mbar_init(smem_u32(&p_full[i]), 4);
+      mbar_init(smem_u32(&pv_done[i]), 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 9) tmem_alloc(smem_u32(tmem_slot), 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (*tmem_slot != 0) __trap();
+  ::kpo::pdl_wait();
+  constexpr uint32_t tmem = 0;
+  const uint32_t sQ = smem_u32(smem + C::OFF_Q), sK = smem_u32(smem + C::OFF_K), sV = smem_u32(smem + C::OFF_V);
+
+  if (warp >= 8) {
+    // the CTA holds 384 x 168 registers: 256 x 232 + 128 x 40 = 64512 fits exactly
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+    if (warp == 8 && lane == 0) {
+      // ------------------------------------------------------------ TMA producer
+      mbar_arrive_expect_tx(smem_u32(q_full), 2 * C::Q_BYTES);
+#pragma unroll
+      for (int g = 0; g < 2; ++g)
+#pragma unroll
+        for (int kb = 0; kb < KSUB; ++kb)
+          tma_load_2d(sQ + g * C::Q_BYTES + kb * BM * 128, &tmQ, smem_u32(q_full), h * D + kb * 64, m0 + g * BM);
+      for (int j = 0; j < n_all; ++j) {
+        const int s = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        mbar_wait(smem_u32(&k_empty[s]), ph ^ 1);
+        uint32_t fb = smem_u32(&k_full[s]);
+        mbar_arrive_expect_tx(fb, C::KV_BYTES);
+#pragma unroll
+        for (int kb = 0; kb < KSUB; ++kb)
+          tma_load_2d(sK + s * C::KV_BYTES + kb * BN * 128, &tmK, fb, kvh * D + kb * 64, j * BN);
+        mbar_wait(smem_u32(&v_empty[s]), ph ^ 1);
+        fb = smem_u32(&v_full[s]);
+        mbar_arrive_expect_tx(fb, C::KV_BYTES);
+#pragma unroll
+        for (int kb = 0; kb < KSUB; ++kb)
+          tma_load_2d(sV + s * C::KV_BYTES + kb * BN * 128, &tmV, fb, kvh * D + kb * 64, j * BN);
+      }
+    } else if (warp == 9) {  // the whole warp runs the issue loop; elect.sync issues
+      // ------------------------------------------------------------ MMA issuer
+      constexpr uint32_t ID_S = idesc_bf16(BM, BN, false, false);
+      constexpr uint32_t ID_O = idesc_bf16(BM, D, false, true);
+      mbar_wait(smem_u32(q_full), 0);
+      auto issue_s = [&](int g, int j) {  // S_g(j) = Q_g K_j^T into S_g
+        const int s = j & 1;
+        const uint32_t q_k = desc_lo(sQ + g * C::Q_BYTES, 16), k_k = desc_lo(sK + s * C::KV_BYTES, 16);
+        const uint32_t d_s = tmem + (g ? C::COL_S1 : C::COL_S0);
+#pragma unroll
+        for (int kb = 0; kb < KSUB; ++kb)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            tc_mma_lo_w(d_s, q_k + kb * (BM * 8) + k * 2, k_k + kb * (BN * 8) + k * 2, ID_S, (kb | k) ? 1u : 0u);
+        tc_commit_w(smem_u32(&s_full[g]));
+      };
+      auto issue_pv = [&](int g, int j) {  // O_g += P_g(j) V_j
+        const int s = j & 1;
+        mbar_wait(smem_u32(&p_full[g]), j & 1);
+        tc_fence_after();
+        const uint32_t v_mn = desc_lo(sV + s * C::KV_BYTES, BN * 128);
+        const uint32_t p_t = tmem + (g ? C::COL_S1 : C::COL_S0);
+        const uint32_t o_t = tmem + (g ? C::COL_O1 : C::COL_O0);
+#pragma unroll
+        for (int kk = 0; kk < BN / 16; ++kk)
+          tc_mma_ts_lo_w(o_t, p_t + kk * 8, v_mn + kk * 128, ID_O, (j > 0 || kk > 0) ? 1u : 0u);
+        tc_commit_w(smem_u32(&pv_done[g]));
+      };
+      // prologue: S0_0, S1_0 (K_0)
+      mbar_wait(smem_u32(&k_full[0]), 0);
+      tc_fence_after();
+      if (n_g[0] > 0) issue_s(0, 0);
+      if (n_g[1] > 0) issue_s(1, 0);
+      tc_commit_w(smem_u32(&k_empty[0]));
+      for (int j = 0; j < n_all; ++j) {
+        const int s = j & 1;
+        const bool more = j + 1 < n_all;
+        mbar_wait(smem_u32(&v_full[s]), (j >> 1) & 1);
+        if (more) mbar_wait(smem_u32(&k_full[s ^ 1]), ((j + 1) >> 1) & 1);
+        tc_fence_after();
+        if (j < n_g[0]) issue_pv(0, j);
+        if (j + 1 < n_g[0]) issue_s(0, j + 1);
+        if (j < n_g[1]) issue_pv(1, j);
+        if (j + 1 < n_g[1]) issue_s(1, j + 1);
+        tc_commit_w(smem_u32(&v_empty[s]));
+        if (more) tc_commit_w(smem_u32(&k_empty[s ^ 1]));
+      }
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
+    // ------------------------------------------------------------ softmax group g (one row per thread)
+    const int g = warp >> 2;
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const int q = m0 + g * BM + r;
+    const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
+    const uint32_t s_addr = lane_addr + (g ? C::COL_S1 : C::COL_S0);
+    const uint32_t o_addr = lane_addr + (g ? C::COL_O1 : C::COL_O0);
+    const int ng = n_g[g];
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int j = 0; j < ng; ++j) {
+      mbar_wait(smem_u32(&s_full[g]), j & 1);
+      tc_fence_after();
+      float sv[BN];
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) tmem_ld32_nowait(s_addr + c * 32, reinterpret_cast<uint32_t*>(sv + c * 32));
+      tmem_wait_ld();
+      const int k0 = j * BN;
+      const bool mask = (causal && k0 + BN - 1 > m0 + g * BM) || (k0 + BN > T);  // group-uniform
+      if (mask) {
+#pragma unroll
+        for (int i = 0; i < BN; ++i) {
+          const int key = k0 + i;
+          sv[i] = (key >= T || (causal && key > q)) ? -INFINITY : sv[i];
+        }
+      }
+      float pm[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) pm[e] = sv[e];
+#pragma unroll
+      for (int i = 8; i < BN; ++i) pm[i & 7] = fmaxf(pm[i & 7], sv[i]);
+      const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
+                             fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7]))) * scale_log2;
+      float corr = 1.f;
+      bool rescale = false;
+      if (mx > m_run + 8.f) {
+        corr = (m_run == -INFINITY) ? 0.f : ex2(m_run - mx);
+        rescale = (j > 0);
+        m_run = mx;
+      }
+      // O_g is stable here: S_g(j) completing implies PV_g(j-1) completed (commit semantics)
+      if (__any_sync(0xffffffffu, rescale)) {
+#pragma unroll 1
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t ov[32];
+          tmem_ld32_nowait(o_addr + c * 32, ov);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * corr);
+          tmem_st32(o_addr + c * 32, ov);
+        }
+      }
+      const float neg_m = -m_run;
+      // ping-pong: the two groups take turns on the exponentials (MUFU), so one group's TMEM loads,
+      // row max and P stores overlap the other's exp phase instead of both contending for MUFU
+      if (pingpong) {
+        if (g == 0 && j > 0) named_bar(1, 256);
+        if (g == 1 && j < n_g[0]) named_bar(2, 256);
+      }
+      float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int hb = 0; hb < 2; ++hb) {  // 64 keys -> 32 columns of bf16 pairs over S_g
+        uint32_t pk[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          float p[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int i = hb * 64 + c * 2 + e;
+            p[e] = ex2(fmaf(sv[i], scale_log2, neg_m));
+            ps[i & 7] += p[e];
+          }
+          pk[c] = pack_bf16x2(p[0], p[1]);
+        }
+        tmem_st32(s_addr + hb * 32, pk);
+      }
+      if (pingpong) {  // hand the MUFU to the other group
+        if (g == 0) asm volatile("bar.arrive 2, 256;" ::: "memory");
+        if (g == 1 && j + 1 < n_g[0]) asm volatile("bar.arrive 1, 256;" ::: "memory");
+      }
+      const float lsum = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
+      l_run = l_run * corr + lsum;
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&p_full[g]));
+    }
+    if (ng > 0) {
+      // ------------------------------------------------------------ epilogue
+      mbar_wait(smem_u32(&pv_done[g]), (ng - 1) & 1);
+      tc_fence_after();
+      const float inv = 1.f / l_run;
+      const bool row_ok = q < T;
+      __nv_bfloat16* orow = o + (int64_t)q * os + (int64_t)h * D;
+#pragma unroll 1
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t ov[32];
+        tmem_ld32_nowait(o_addr + c * 32, ov);
+        tmem_wait_ld();
+        if (row_ok) {
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            float f[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(ov[v * 8 + e]) * inv;
+            *reinterpret_cast<uint4*>(orow + c * 32 + v * 8) = pack8(f);
+          }
+        }
+      }
+      if (row_ok) lse[(int64_t)h * T + q] = (m_run + __log2f(l_run)) / kLog2e;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 9) tmem_dealloc(tmem, 512);
+}
+
 template <int D>
 int fwd_launch(const void* q, const void* k, const void* v, void* o, float* lse, int64_t T, int hq, int hkv,
                int64_t qs, int64_t ks, int64_t vs, int64_t os, float scale, int causal, cudaStream_t st) {
@@ -317,6 +597,18 @@ int fwd_launch(const void* q, const void* k, const void* v, void* o, float* lse,
                                          causal));
     return KPO_OK;
   };
+  static const int variant = getenv("KPO_ATTN_FWD") ? atoi(getenv("KPO_ATTN_FWD")) : 2;
+  if (variant == 2 && D == 128) {
+    using C2 = Fwd2<D>;
+    dim3 grid2((unsigned)hq, (unsigned)((T + 2 * C2::BM - 1) / (2 * C2::BM)));
+    auto kern2 = attn_fwd_tc2_kernel<D>;
+    KPO_CUDA(cudaFuncSetAttribute(kern2, cudaFuncAttributeMaxDynamicSharedMemorySize, C2::SMEM));
+    KPO_CUDA(::kpo::pdl_launch(kern2, grid2, C2::THREADS, C2::SMEM, st, mq, mk, mv, (__nv_bfloat16*)o, lse, (int)T,
+                               hq, hkv, os, scale * kLog2e, causal,
+                               getenv("KPO_ATTN_PINGPONG") ? atoi(getenv("KPO_ATTN_PINGPONG")) : 1));
+    KPO_LAUNCH_CHECK();
+    return KPO_OK;
+  }
   int rc;
   if (mode == 0) rc = go(attn_fwd_tc_kernel<D, 0x00>);
   else if (mode == 2) rc = go(attn_fwd_tc_kernel<D, 0x55>);

@@ -773,7 +773,7 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // the whole warp runs the issue loop (warp-uniform operands); elect.sync issues
       // ------------------------------------------------------------ MMA issuer
       constexpr uint32_t ID_S = idesc_bf16(BN, BM, false, false);   // S^T, dP^T
       constexpr uint32_t ID_G = idesc_bf16(BN, D, false, true);     // dV, dK
@@ -793,8 +793,8 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
 #pragma unroll
           for (int k = 0; k < BM / 16; ++k) {
             const uint32_t acc = (j > 0 || k > 0) ? 1u : 0u;
-            tc_mma_ts_lo(tmem + C::COL_DV, pt + k * 8, o_mn + k * 128, ID_GT, acc);
-            tc_mma_lo(tmem + C::COL_DK, ds_k + k * 2, q_mn + k * 128, ID_G, acc);
+            tc_mma_ts_lo_w(tmem + C::COL_DV, pt + k * 8, o_mn + k * 128, ID_GT, acc);
+            tc_mma_lo_w(tmem + C::COL_DK, ds_k + k * 2, q_mn + k * 128, ID_G, acc);
           }
         }
         mbar_wait(smem_u32(&dq_empty[0]), (j & 1) ^ 1);
@@ -802,11 +802,11 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
         if (!(ablate & 8)) {
 #pragma unroll
           for (int k = 0; k < BN / 16; ++k)
-            tc_mma_lo(tmem + C::COL_DQ, k_mn + k * 128, ds_mn + k * 128, ID_Q, k > 0 ? 1u : 0u);
+            tc_mma_lo_w(tmem + C::COL_DQ, k_mn + k * 128, ds_mn + k * 128, ID_Q, k > 0 ? 1u : 0u);
         }
-        tc_commit(smem_u32(&dq_full[0]));
-        tc_commit(smem_u32(&pds_empty[st]));
-        tc_commit(smem_u32(&qd_empty[qs]));
+        tc_commit_w(smem_u32(&dq_full[0]));
+        tc_commit_w(smem_u32(&pds_empty[st]));
+        tc_commit_w(smem_u32(&qd_empty[qs]));
       };
       auto scores = [&](int s) {
         const int st = s % C::QSTAGES;
@@ -819,12 +819,12 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const uint32_t acc = (kb | k) ? 1u : 0u;
-              tc_mma_lo(tmem + C::COL_S, k_k + kb * (BN * 8) + k * 2, q_k + kb * (BM * 8) + k * 2, ID_S, acc);
-              tc_mma_lo(tmem + C::COL_DP, v_k + kb * (BN * 8) + k * 2, o_k + kb * (BM * 8) + k * 2, ID_S, acc);
+              tc_mma_lo_w(tmem + C::COL_S, k_k + kb * (BN * 8) + k * 2, q_k + kb * (BM * 8) + k * 2, ID_S, acc);
+              tc_mma_lo_w(tmem + C::COL_DP, v_k + kb * (BN * 8) + k * 2, o_k + kb * (BM * 8) + k * 2, ID_S, acc);
             }
           }
         }
-        tc_commit(smem_u32(s_full));
+        tc_commit_w(smem_u32(s_full));
       };
       if (steps > 0) scores(0);
       for (int s = 0; s < steps; ++s) {
@@ -834,7 +834,7 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
         }
         grads(s);
       }
-      tc_commit(smem_u32(acc_done));
+      tc_commit_w(smem_u32(acc_done));
     }
   } else if (warp < 2 + C::SM_WARPS) {
     // ------------------------------------------------------------ softmax warps 2..9

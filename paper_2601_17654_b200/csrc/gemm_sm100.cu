@@ -316,8 +316,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ===================== MMA issuer (single thread)
+    {
+      // ===================== MMA issuer: the whole warp runs the loop (warp-uniform operands in
+      // uniform registers), elect.sync issues each tcgen05.mma / commit
       constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)A_MN << 15) |
                                  ((uint32_t)B_MN << 16) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
       // K-major SW128: SBO = 8 rows * 128B; MN-major SW128: LBO = MN-chunk stride, SBO = 8 K-rows.
@@ -331,7 +332,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int slot = it & 1;
         mbar_wait(smem_u32(&sfull[slot]), (it >> 1) & 1);
         const int tile = stile[slot];
-        mbar_arrive(smem_u32(&sempty[slot]));
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&sempty[slot]));
         ++it;
         if (tile >= num_tiles) break;
         const int acc = acc_it & 1;
@@ -347,14 +349,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t a_lo = desc_lo(sa, A_LBO), b_lo = desc_lo(sb, B_LBO);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            tc_mma_lo(d_tmem, a_lo + k * (A_KSTEP >> 4), b_lo + k * (B_KSTEP >> 4), IDESC, (kb | k) != 0);
-          tc_commit(smem_u32(&empty[stage]));
+            tc_mma_lo_w(d_tmem, a_lo + k * (A_KSTEP >> 4), b_lo + k * (B_KSTEP >> 4), IDESC, (kb | k) != 0);
+          tc_commit_w(smem_u32(&empty[stage]));
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit(smem_u32(&tfull[acc]));
+        tc_commit_w(smem_u32(&tfull[acc]));
         ++acc_it;
       }
     }
@@ -555,8 +557,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {
-      // ===================== MMA issuer (leader only, M = 256 across the pair)
+    if (leader) {
+      // ===================== MMA issuer (leader CTA's warp 1, M = 256 across the pair; elect.sync issues)
       constexpr uint32_t IDESC = idesc_bf16(256, BN, A_MN, B_MN);
       constexpr uint32_t A_LBO = A_MN ? BK * 128 : 16, A_SBO = 1024;
       constexpr uint32_t B_LBO = B_MN ? BK * 128 : 16, B_SBO = 1024;
@@ -568,7 +570,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int slot = it & 1;
         mbar_wait(smem_u32(&sfull[slot]), (it >> 1) & 1);
         const int tile = stile[slot];
-        mbar_arrive(smem_u32(&sempty[slot]));
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&sempty[slot]));
         ++it;
         if (tile >= num_tiles) break;
         const int acc = acc_it & 1;
@@ -584,14 +587,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const uint32_t a_lo = desc_lo(sa, A_LBO), b_lo = desc_lo(sb, B_LBO);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            tc_mma_pair_lo(d_tmem, a_lo + k * (A_KSTEP >> 4), b_lo + k * (B_KSTEP >> 4), IDESC, (kb | k) != 0);
-          tc_commit_pair(smem_u32(&empty[stage]));
+            tc_mma_pair_lo_w(d_tmem, a_lo + k * (A_KSTEP >> 4), b_lo + k * (B_KSTEP >> 4), IDESC, (kb | k) != 0);
+          tc_commit_pair_w(smem_u32(&empty[stage]));
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit_pair(smem_u32(&tfull[acc]));
+        tc_commit_pair_w(smem_u32(&tfull[acc]));
         ++acc_it;
       }
     }

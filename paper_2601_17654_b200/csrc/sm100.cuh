@@ -225,6 +225,18 @@ __device__ __forceinline__ void tc_commit_w(uint32_t bar) {
       : "memory");
 }
 
+__device__ __forceinline__ void tc_mma_pair_lo_w(uint32_t tmem_d, uint32_t a_lo, uint32_t b_lo, uint32_t idesc,
+                                                 uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 da, db;\n\t"
+      "mov.b64 da, {%1, %5};\n\t"
+      "mov.b64 db, {%2, %5};\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], da, db, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(a_lo), "r"(b_lo), "r"(idesc), "r"(acc), "n"(kDescHiSw128));
+}
+
 __device__ __forceinline__ void tc_mma_pair_lo(uint32_t tmem_d, uint32_t a_lo, uint32_t b_lo, uint32_t idesc,
                                                uint32_t acc) {
   asm volatile(
@@ -301,6 +313,15 @@ __device__ __forceinline__ void tc_mma_pair(uint32_t tmem_d, uint64_t da, uint64
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+// warp-converged variant of tc_commit_pair (elect.sync picks the issuing lane)
+__device__ __forceinline__ void tc_commit_pair_w(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
 }
 // commit: arrive on the barrier at the same offset in both CTAs of the pair
 __device__ __forceinline__ void tc_commit_pair(uint32_t bar) {

@@ -1003,17 +1003,22 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&dq_empty[0]));
-      // own fp32 staging tile: wait until the previous TMA reduce has read it
-      if (dtid == 0) bulk_wait_read0();
-      named_bar(2, 128);
+      // the staging tile drains in two 32-query halves: half hf is rewritten once its previous reduce
+      // has read it, while the other half's reduce may still be in flight
       float* stg = reinterpret_cast<float*>(smem + C::OFF_DQ);
 #pragma unroll
-      for (int qi = 0; qi < BM; ++qi) stg[qi * D + dcol] = v[qi] * scale;
-      fence_async_smem();
-      named_bar(2, 128);
-      if (dtid == 0 && !(ablate & 1)) {
-        tma_reduce_add_2d(&tmDQ, smem_u32(stg), h * D, m0);
-        bulk_commit();
+      for (int hf = 0; hf < 2; ++hf) {
+        if (dtid == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        named_bar(2, 128);
+        float* sh = stg + hf * (BM / 2) * D;
+#pragma unroll
+        for (int qi = 0; qi < BM / 2; ++qi) sh[qi * D + dcol] = v[hf * (BM / 2) + qi] * scale;
+        fence_async_smem();
+        named_bar(2, 128);
+        if (dtid == 0) {
+          if (!(ablate & 1)) tma_reduce_add_2d(&tmDQ, smem_u32(sh), h * D, m0 + hf * (BM / 2));
+          bulk_commit();
+        }
       }
     }
     if (dtid == 0) bulk_wait0();
@@ -1032,7 +1037,8 @@ int bwd_launch(const void* q, const void* k, const void* v, const void* dout, co
   using C = Bwd<D>;
   CUtensorMap mq, mk, mv, mo, mdq;
   int e;
-  if ((e = make_map_2d_f32(&mdq, dq_acc, (uint64_t)hq * D, T, (uint64_t)hq * D, D, C::BM))) return e;
+  // dQ reduce boxes of half a step (32 queries): the two halves of the staging tile drain separately
+  if ((e = make_map_2d_f32(&mdq, dq_acc, (uint64_t)hq * D, T, (uint64_t)hq * D, D, C::BM / 2))) return e;
   if ((e = make_map_2d(&mq, q, (uint64_t)hq * D, T, qs, 64, C::BM))) return e;
   if ((e = make_map_2d(&mk, k, (uint64_t)hkv * D, T, ks, 64, C::BN))) return e;
   if ((e = make_map_2d(&mv, v, (uint64_t)hkv * D, T, vs, 64, C::BN))) return e;

@@ -654,8 +654,11 @@ struct Bwd {
   // TMEM: S^T 0..63, dP^T 64..127, dQ^T 128..191, P^T (bf16 pairs, 2 buffers x 32 cols) 192..255,
   //       dV 256..383, dK 384..511
   static constexpr int COL_S = 0, COL_DP = 64, COL_DQ = 128, COL_PT = 192, COL_DV = 256, COL_DK = 384;
-  static constexpr int THREADS = 448;  // TMA, MMA, 8 softmax warps (2 per lane quarter), 4 dQ-drain warps
-  static constexpr int SM_WARPS = 8;
+  // TMA, MMA, SM_WARPS softmax warps (SM_WARPS / 4 per lane quarter, each BM * 4 / SM_WARPS query
+  // columns), 4 dQ-drain warps.  16 softmax warps halve the per-warp latency of the softmax, which sits
+  // between the S / dP MMAs and the gradient MMAs of a step (ablation: removing it saved 18%).
+  static constexpr int SM_WARPS = 16;
+  static constexpr int THREADS = (2 + SM_WARPS + 4) * 32;
 };
 
 
@@ -837,14 +840,15 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
       tc_commit_w(smem_u32(acc_done));
     }
   } else if (warp < 2 + C::SM_WARPS) {
-    // ------------------------------------------------------------ softmax warps 2..9
-    // row = key (TMEM lane quarter = warp % 4); the two warps of a quarter split the 64 query columns
+    // ------------------------------------------------------------ softmax warps 2 .. 2 + SM_WARPS - 1
+    // row = key (TMEM lane quarter = warp % 4); the SM_WARPS / 4 warps of a quarter split the 64 query
+    // columns
     const int quarter = warp & 3;
-    const int half = (warp - 2) >> 2;
+    const int half = (warp - 2) >> 2;  // column group of this warp (0 .. SM_WARPS/4 - 1)
     const int r = quarter * 32 + lane;
     const int key = n0 + r;
     const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
-    constexpr int HC = BM / 2;  // query columns per warp
+    constexpr int HC = BM * 4 / C::SM_WARPS;  // query columns per warp
     const float* stat_half = stat + half * HC;
     for (int s = 0, mi = 0; s < steps; ++s, mi = (mi + 1 == mq) ? 0 : mi + 1) {
       const int m0 = (m_start + mi) * BM;
@@ -852,8 +856,13 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
       mbar_wait(smem_u32(s_full), s & 1);
       tc_fence_after();
       float sv[HC], dp[HC];
-      tmem_ld32_nowait(lane_addr + C::COL_S + half * HC, reinterpret_cast<uint32_t*>(sv));
-      tmem_ld32_nowait(lane_addr + C::COL_DP + half * HC, reinterpret_cast<uint32_t*>(dp));
+      if constexpr (HC == 32) {
+        tmem_ld32_nowait(lane_addr + C::COL_S + half * HC, reinterpret_cast<uint32_t*>(sv));
+        tmem_ld32_nowait(lane_addr + C::COL_DP + half * HC, reinterpret_cast<uint32_t*>(dp));
+      } else {
+        tmem_ld16_nowait(lane_addr + C::COL_S + half * HC, reinterpret_cast<uint32_t*>(sv));
+        tmem_ld16_nowait(lane_addr + C::COL_DP + half * HC, reinterpret_cast<uint32_t*>(dp));
+      }
       // this warp's 32 query statistics (lse, D), bulk-copied by the TMA warp with the Q/dO stage
       const uint32_t sst = smem_u32(stat_half + (s % C::QSTAGES) * 2 * BM);
       tmem_wait_ld();
@@ -903,7 +912,8 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
                      : "memory");
       }
       // P^T row (this warp's 32 queries = 16 packed columns) -> TMEM, the A operand of the dV MMA
-      tmem_st16(lane_addr + C::COL_PT + buf * 32 + half * (HC / 2), pp);
+      if constexpr (HC == 32) tmem_st16(lane_addr + C::COL_PT + buf * 32 + half * (HC / 2), pp);
+      else tmem_st8(lane_addr + C::COL_PT + buf * 32 + half * (HC / 2), pp);
       tmem_wait_st();
       tc_fence_before();
       fence_async_smem();
@@ -979,7 +989,7 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
     }
   done_softmax:;
   } else {
-    // ------------------------------------------------------------ dQ drain warps 10..13 (lane = head dim)
+    // ------------------------------------------------------------ dQ drain warps (the last 4; lane = head dim)
     const int quarter = warp & 3;
     const int dcol = quarter * 32 + lane;
     const int dtid = threadIdx.x - (2 + C::SM_WARPS) * 32;  // 0..127
@@ -989,30 +999,31 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
       step_coords(s, h, m0);
       mbar_wait(smem_u32(&dq_full[0]), s & 1);
       tc_fence_after();
-      float v[BM];
       if (ablate & 2) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&dq_empty[0]));
         continue;
       }
-#pragma unroll
-      for (int c = 0; c < BM / 32; ++c)
-        tmem_ld32_nowait(lane_addr + C::COL_DQ + c * 32, reinterpret_cast<uint32_t*>(v + c * 32));
-      tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&dq_empty[0]));
       // the staging tile drains in two 32-query halves: half hf is rewritten once its previous reduce
-      // has read it, while the other half's reduce may still be in flight
+      // has read it, while the other half's reduce may still be in flight; dQ^T's TMEM columns are
+      // released once the second half has been loaded (32 live registers, not 64)
       float* stg = reinterpret_cast<float*>(smem + C::OFF_DQ);
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
+        float v[BM / 2];
+        tmem_ld32_nowait(lane_addr + C::COL_DQ + hf * 32, reinterpret_cast<uint32_t*>(v));
+        tmem_wait_ld();
+        if (hf == 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&dq_empty[0]));
+        }
         if (dtid == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         named_bar(2, 128);
         float* sh = stg + hf * (BM / 2) * D;
 #pragma unroll
-        for (int qi = 0; qi < BM / 2; ++qi) sh[qi * D + dcol] = v[hf * (BM / 2) + qi] * scale;
+        for (int qi = 0; qi < BM / 2; ++qi) sh[qi * D + dcol] = v[qi] * scale;
         fence_async_smem();
         named_bar(2, 128);
         if (dtid == 0) {

@@ -12,7 +12,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkpo.so")
+# KPO_LIB_PATH: A/B measurement tools load an alternative build of the same library (tools/*_ab.*)
+LIB_PATH = os.environ.get("KPO_LIB_PATH") or os.path.join(_HERE, "libkpo.so")
 
 KPO_OK = 0
 KPO_ERR_INVALID = -1

@@ -12,8 +12,10 @@ namespace kpo {
 
 // ===================================================================== RMSNorm forward
 // One warp per row.  Rows of up to 32*8*NV elements are cached in registers (NV uint4 per lane).
+// Register cap: 3 CTAs (24 row-warps) per SM for rows up to 3072 columns — unbounded, ptxas hoists the
+// gamma loads and reaches 150 registers, i.e. 8 warps per SM and 3.5 waves of latency-bound rows.
 template <int NV>
-__global__ void __launch_bounds__(256) rmsnorm_fwd_cached(const __nv_bfloat16* __restrict__ x,
+__global__ void __launch_bounds__(256, NV <= 12 ? 3 : 1) rmsnorm_fwd_cached(const __nv_bfloat16* __restrict__ x,
                                                           const __nv_bfloat16* __restrict__ w,
                                                           __nv_bfloat16* __restrict__ y,
                                                           float* __restrict__ rstd, int64_t rows,
@@ -47,6 +49,48 @@ __global__ void __launch_bounds__(256) rmsnorm_fwd_cached(const __nv_bfloat16* _
     for (int j = 0; j < 8; ++j) f[j] = f[j] * r * g[j];
     yr[lane + 32 * i] = pack8(f);
   }
+}
+
+// One 128-thread CTA per row for rows of 1024*NV columns (NV uint4 per thread): ~30 registers, 16
+// rows resident per SM, and a finished row's SM slot is refilled at CTA granularity.
+template <int NV>
+__global__ void __launch_bounds__(128) rmsnorm_fwd_row(const __nv_bfloat16* __restrict__ x,
+                                                       const __nv_bfloat16* __restrict__ w,
+                                                       __nv_bfloat16* __restrict__ y, float* __restrict__ rstd,
+                                                       int64_t rows, int cols, float eps) {
+  KPO_PDL_ENTRY();
+  __shared__ float red[4];
+  const int64_t row = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + row * cols);
+  uint4 v[NV];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    v[i] = ld_nc_v4(xr + tid + 128 * i);
+    float f[8];
+    unpack8(v[i], f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) ss += f[j] * f[j];
+  }
+  ss = warp_sum(ss);
+  if (lane == 0) red[wid] = ss;
+  __syncthreads();
+  ss = (red[0] + red[1]) + (red[2] + red[3]);
+  const float r = rsqrtf(ss / (float)cols + eps);
+  if (tid == 0 && rstd) rstd[row] = r;
+  const uint4* wr = reinterpret_cast<const uint4*>(w);
+  uint4* yr = reinterpret_cast<uint4*>(y + row * cols);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    float f[8], g[8];
+    unpack8(v[i], f);
+    unpack8(wr[tid + 128 * i], g);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[j] = f[j] * r * g[j];
+    yr[tid + 128 * i] = pack8(f);
+  }
+  (void)rows;
 }
 
 // Generic fallback: two passes over the row (second pass served by L1/L2).
@@ -181,109 +225,125 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// Fused single-pass backward for rows of 256*NV columns (hidden 1024..4096): each warp keeps its row
-// of x and dy in registers (2*NV uint4 per lane), computes dx, and accumulates dgamma for its columns
-// over the rows it owns; the CTA's 4 warps reduce their dgamma through shared memory into one fp32
-// partial row per CTA.  x and dy are read from HBM once (the split dx + dgamma kernels read them
-// twice).  Every warp owns exactly `rows_per_warp` consecutive rows.
+// Fused single-pass backward for rows of 1024*NV columns (hidden 1024..4096).  A 256-thread CTA owns
+// a contiguous block of rows; its two 128-thread groups take alternate rows, one row per group at a
+// time, with the next row's x / dy / dres loads issued before the current row is reduced (two rows
+// per group in flight).  Each thread owns the same 8*NV columns of every row, so its share of dgamma
+// accumulates in registers; the groups combine through shared memory into ONE fp32 partial row per
+// CTA.  x, dy and dres are read from HBM once.
 template <int NV>
-__global__ void __launch_bounds__(128)
-    rmsnorm_bwd_fused(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
-                      const __nv_bfloat16* __restrict__ w, const float* __restrict__ rstd,
-                      const __nv_bfloat16* __restrict__ dres, __nv_bfloat16* __restrict__ dx,
-                      float* __restrict__ dw_partial, int64_t rows, int rows_per_warp) {
+__global__ void __launch_bounds__(256)
+    rmsnorm_bwd_rows(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+                     const __nv_bfloat16* __restrict__ w, const float* __restrict__ rstd,
+                     const __nv_bfloat16* __restrict__ dres, __nv_bfloat16* __restrict__ dx,
+                     float* __restrict__ dw_partial, int64_t rows, int rows_per_cta) {
   KPO_PDL_ENTRY();
-  constexpr int cols = NV * 256;
-  extern __shared__ float red[];  // [4 warps][cols] dgamma accumulators (each warp owns its row)
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t r0 = ((int64_t)blockIdx.x * 4 + wid) * rows_per_warp;
-  float* acc = red + wid * cols;
+  constexpr int cols = NV * 1024;
+  __shared__ float red[2][2][4];            // [group][row parity][warp] partial dot products
+  __shared__ __align__(16) float comb[cols];  // group 1's dgamma share, added by group 0
+  const int tid = threadIdx.x & 127, grp = threadIdx.x >> 7, lane = threadIdx.x & 31, wid = tid >> 5;
+  const int64_t r_begin = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t r_end = min(rows, r_begin + rows_per_cta);
+  float acc[NV][8];
+  float g[NV][8];
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
-    float4* a4 = reinterpret_cast<float4*>(acc + (lane + 32 * i) * 8);
-    a4[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-    a4[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    unpack8(reinterpret_cast<const uint4*>(w)[tid + 128 * i], g[i]);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
   }
-  const uint4* wr = reinterpret_cast<const uint4*>(w);
-  for (int k = 0; k < rows_per_warp; ++k) {
-    const int64_t row = r0 + k;
-    if (row >= rows) break;
+  uint4 cx[NV], cd[NV], cr[NV], nx[NV], nd[NV], nr[NV];
+  auto load = [&](int64_t row, uint4* ox, uint4* od, uint4* orr) {
     const uint4* xr = reinterpret_cast<const uint4*>(x + row * cols);
     const uint4* dyr = reinterpret_cast<const uint4*>(dy + row * cols);
-    uint4 xv[NV], dv[NV];  // the row stays packed in registers (bf16)
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
-      xv[i] = ld_nc_v4(xr + lane + 32 * i);
-      dv[i] = ld_nc_v4(dyr + lane + 32 * i);
+      ox[i] = ld_nc_v4(xr + tid + 128 * i);
+      od[i] = ld_nc_v4(dyr + tid + 128 * i);
     }
+    if (dres) {
+      const uint4* rr = reinterpret_cast<const uint4*>(dres + row * cols);
+#pragma unroll
+      for (int i = 0; i < NV; ++i) orr[i] = ld_nc_v4(rr + tid + 128 * i);
+    }
+  };
+  int64_t row = r_begin + grp;
+  if (row < r_end) load(row, cx, cd, cr);
+  for (int k = 0; row < r_end; ++k, row += 2) {
+    const bool more = row + 2 < r_end;
+    if (more) load(row + 2, nx, nd, nr);
     const float r = rstd[row];
     float dot = 0.f;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
-      float a[8], b[8], g[8];
-      unpack8(xv[i], a);
-      unpack8(dv[i], b);
-      unpack8(wr[lane + 32 * i], g);
-      float4* a4 = reinterpret_cast<float4*>(acc + (lane + 32 * i) * 8);
-      float4 p = a4[0], q = a4[1];
-      p.x += b[0] * a[0] * r; p.y += b[1] * a[1] * r; p.z += b[2] * a[2] * r; p.w += b[3] * a[3] * r;
-      q.x += b[4] * a[4] * r; q.y += b[5] * a[5] * r; q.z += b[6] * a[6] * r; q.w += b[7] * a[7] * r;
-      a4[0] = p;
-      a4[1] = q;
+      float a[8], b[8];
+      unpack8(cx[i], a);
+      unpack8(cd[i], b);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) dot += g[j] * b[j] * a[j];
+      for (int j = 0; j < 8; ++j) {
+        acc[i][j] += b[j] * a[j] * r;
+        dot += g[i][j] * b[j] * a[j];
+      }
     }
     dot = warp_sum(dot);
+    if (lane == 0) red[grp][k & 1][wid] = dot;
+    asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
+    dot = (red[grp][k & 1][0] + red[grp][k & 1][1]) + (red[grp][k & 1][2] + red[grp][k & 1][3]);
     const float c = dot * r * r * r / (float)cols;
     uint4* dxr = reinterpret_cast<uint4*>(dx + row * cols);
-    const uint4* dresr = dres ? reinterpret_cast<const uint4*>(dres + row * cols) : nullptr;
-    // opaque redefinition: the second pass unpacks the packed row again instead of keeping the
-    // unpacked floats of the first pass alive (which would not fit in registers for NV >= 12)
-#pragma unroll
-    for (int i = 0; i < NV; ++i)
-      asm volatile("" : "+r"(xv[i].x), "+r"(xv[i].y), "+r"(xv[i].z), "+r"(xv[i].w), "+r"(dv[i].x), "+r"(dv[i].y),
-                   "+r"(dv[i].z), "+r"(dv[i].w));
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
-      float a[8], b[8], g[8], o[8];
-      unpack8(xv[i], a);
-      unpack8(dv[i], b);
-      unpack8(wr[lane + 32 * i], g);
-      float res[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      if (dresr) unpack8(ld_nc_v4(dresr + lane + 32 * i), res);
+      float a[8], b[8], o[8], res[8];
+      unpack8(cx[i], a);
+      unpack8(cd[i], b);
+      if (dres) unpack8(cr[i], res);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) o[j] = r * g[j] * b[j] - a[j] * c + res[j];
-      dxr[lane + 32 * i] = pack8(o);
+      for (int j = 0; j < 8; ++j) o[j] = r * g[i][j] * b[j] - a[j] * c + (dres ? res[j] : 0.f);
+      dxr[tid + 128 * i] = pack8(o);
+    }
+    if (more) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        cx[i] = nx[i];
+        cd[i] = nd[i];
+        cr[i] = nr[i];
+      }
+    }
+  }
+  if (grp == 1) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      float4* c4 = reinterpret_cast<float4*>(comb + (tid + 128 * i) * 8);
+      c4[0] = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+      c4[1] = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
     }
   }
   __syncthreads();
-  float4* out = reinterpret_cast<float4*>(dw_partial + (int64_t)blockIdx.x * cols);
-  for (int c4 = threadIdx.x; c4 < cols / 4; c4 += blockDim.x) {
-    float4 s4 = reinterpret_cast<const float4*>(red)[c4];
+  if (grp == 0) {
+    float4* out = reinterpret_cast<float4*>(dw_partial + (int64_t)blockIdx.x * cols);
 #pragma unroll
-    for (int ww = 1; ww < 4; ++ww) {
-      const float4 t = reinterpret_cast<const float4*>(red + ww * cols)[c4];
-      s4.x += t.x;
-      s4.y += t.y;
-      s4.z += t.z;
-      s4.w += t.w;
+    for (int i = 0; i < NV; ++i) {
+      const int c8 = tid + 128 * i;
+      const float4* c4 = reinterpret_cast<const float4*>(comb + c8 * 8);
+      const float4 p = c4[0], q = c4[1];
+      out[c8 * 2] = make_float4(acc[i][0] + p.x, acc[i][1] + p.y, acc[i][2] + p.z, acc[i][3] + p.w);
+      out[c8 * 2 + 1] = make_float4(acc[i][4] + q.x, acc[i][5] + q.y, acc[i][6] + q.z, acc[i][7] + q.w);
     }
-    out[c4] = s4;
   }
 }
 
-// rows per warp and CTA count of the fused backward (2 CTAs of 4 warps per SM, one wave)
-static inline void fused_norm_bwd_grid(int64_t rows, int& rows_per_warp, int& grid) {
+// rows per CTA (even: the two row groups stay in step) and CTA count of the fused backward: one CTA
+// per SM, one wave
+static inline void fused_norm_bwd_grid(int64_t rows, int& rows_per_cta, int& grid) {
   int sms = num_sms();
   if (sms <= 0) sms = 148;  // no device visible (host-only queries): B200's SM count
-  const int64_t warps = 4LL * 2 * sms;
-  rows_per_warp = (int)((rows + warps - 1) / warps);
-  if (rows_per_warp < 1) rows_per_warp = 1;
-  grid = (int)((rows + 4LL * rows_per_warp - 1) / (4LL * rows_per_warp));
+  int64_t rpc = (rows + sms - 1) / sms;
+  rpc += rpc & 1;
+  if (rpc < 2) rpc = 2;
+  rows_per_cta = (int)rpc;
+  grid = (int)((rows + rpc - 1) / rpc);
 }
-static inline bool fused_norm_bwd_ok(int64_t cols) {
-  return cols % 256 == 0 && (cols / 256 == 4 || cols / 256 == 8 || cols / 256 == 12);  // 16: spills
-}
+static inline bool fused_norm_bwd_ok(int64_t cols) { return cols % 1024 == 0 && cols / 1024 <= 4; }
 
 // one thread per 8-column chunk, a 64-row slab per blockIdx.y; coalesced 16-byte loads along rows
 __global__ void __launch_bounds__(128)
@@ -432,7 +492,15 @@ extern "C" int kpo_rmsnorm_fwd(const void* x, const void* w, void* y, float* rst
   auto X = (const __nv_bfloat16*)x;
   auto W = (const __nv_bfloat16*)w;
   auto Y = (__nv_bfloat16*)y;
-  if (cols % 256 == 0 && cols / 256 <= 16) {
+  if (cols % 1024 == 0 && cols / 1024 <= 8 && cols / 1024 != 7) {
+    switch (cols / 1024) {
+#define KPO_NORM_ROW_CASE(n) \
+  case n: KPO_CUDA(::kpo::pdl_launch(rmsnorm_fwd_row<n>, dim3((unsigned)rows), dim3(128), 0, s, X, W, Y, rstd, rows, (int)cols, eps)); break;
+      KPO_NORM_ROW_CASE(1) KPO_NORM_ROW_CASE(2) KPO_NORM_ROW_CASE(3) KPO_NORM_ROW_CASE(4) KPO_NORM_ROW_CASE(5)
+      KPO_NORM_ROW_CASE(6) KPO_NORM_ROW_CASE(8)
+#undef KPO_NORM_ROW_CASE
+    }
+  } else if (cols % 256 == 0 && cols / 256 <= 16) {
     switch (cols / 256) {
 #define KPO_NORM_CASE(n) \
   case n: KPO_CUDA(::kpo::pdl_launch(rmsnorm_fwd_cached<n>, grid, block, 0, s, X, W, Y, rstd, rows, (int)cols, eps)); break;
@@ -475,21 +543,12 @@ extern "C" int kpo_rmsnorm_bwd(const void* dy, const void* x, const void* w, con
   auto Dr = (const __nv_bfloat16*)dres;
   auto Dx = (__nv_bfloat16*)dx;
   if (fused_norm_bwd_ok(cols)) {
-    int rpw, g;
-    fused_norm_bwd_grid(rows, rpw, g);
-    const size_t sm = 4 * (size_t)cols * sizeof(float);
-    switch (cols / 256) {
-#define KPO_NBF_CASE(n)                                                                                       \
-  case n: {                                                                                                 \
-    static bool set = false;                                                                                \
-    if (!set) {                                                                                             \
-      KPO_CUDA(cudaFuncSetAttribute(rmsnorm_bwd_fused<n>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536)); \
-      set = true;                                                                                           \
-    }                                                                                                       \
-    KPO_CUDA(::kpo::pdl_launch(rmsnorm_bwd_fused<n>, g, 128, sm, st, Dy, X, W, rstd, Dr, Dx, dw_partial, rows, rpw));                \
-    break;                                                                                                  \
-  }
-      KPO_NBF_CASE(4) KPO_NBF_CASE(8) KPO_NBF_CASE(12) KPO_NBF_CASE(16)
+    int rpc, g;
+    fused_norm_bwd_grid(rows, rpc, g);
+    switch (cols / 1024) {
+#define KPO_NBF_CASE(n) \
+  case n: KPO_CUDA(::kpo::pdl_launch(rmsnorm_bwd_rows<n>, g, 256, 0, st, Dy, X, W, rstd, Dr, Dx, dw_partial, rows, rpc)); break;
+      KPO_NBF_CASE(1) KPO_NBF_CASE(2) KPO_NBF_CASE(3) KPO_NBF_CASE(4)
 #undef KPO_NBF_CASE
     }
     KPO_LAUNCH_CHECK();

@@ -1,0 +1,55 @@
+"""Per-launch-unit in-step durations under the default (comm overlapped from kernel 0) and the
+sequential schedule, to separate comm interference from kernel speed.  Measurement only.
+python tools/unit_sched_ab.py [--config 2]"""
+import argparse, json, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2601_17654_b200.comm import Communicator
+from paper_2601_17654_b200.device import b200_model
+from paper_2601_17654_b200.engine import Engine
+from paper_2601_17654_b200.layer import PartitionedLayer
+from paper_2601_17654_b200.model import baseline_workload
+from paper_2601_17654_b200.runner import LayerRunner, sequential_schedule
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=2)
+a = ap.parse_args()
+wl = baseline_workload(a.config, world=8, tokens=4096)
+n = wl.weight_numels()
+sym = (sum(int(v * 2 / 8) + 4 * v for v in n.values()) if wl.parallel == "fsdp" else 9 * wl.tokens * wl.h * 2) + (64 << 20)
+comm = Communicator.loopback_group(8, sym)
+layer = PartitionedLayer(wl, comm)
+eng = Engine.for_layer(layer, b200_model())
+out = {}
+for tag, sched in (("default", None), ("sequential", sequential_schedule(layer, eng.gpu))):
+    r = LayerRunner(layer, eng, schedule=sched)
+    r.warm()
+    t = r.unit_times_graph(iters=5)
+    out[tag] = {k: round(sorted(v)[len(v) // 2], 4) for k, v in t.items()}
+print(json.dumps(out))
+
+# whole-step time (same process) for comparison with the sum of unit times
+r = LayerRunner(layer, eng)
+r.warm()
+for _ in range(5):
+    r.step()
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record(eng.exec.compute)
+for _ in range(20):
+    r.step()
+e1.record(eng.exec.compute)
+torch.cuda.synchronize()
+step_ms = e0.elapsed_time(e1) / 20
+ok = r.capture_step()
+for _ in range(5):
+    r.step()
+torch.cuda.synchronize()
+e0.record(eng.exec.compute)
+for _ in range(20):
+    r.step()
+e1.record(eng.exec.compute)
+torch.cuda.synchronize()
+print(json.dumps({"step_ms": step_ms, "step_graph_ms": e0.elapsed_time(e1) / 20, "captured": ok,
+                  "unit_sum_default_ms": sum(out["default"].values()),
+                  "n_units": len(out["default"])}))

@@ -71,6 +71,11 @@ int kpo_rope(const void* in, int64_t in_row_stride, void* out, int64_t out_row_s
  * act = silu(gate) * up : [rows, ffn]. */
 int kpo_swiglu_fwd(const void* gu, void* act, int64_t rows, int64_t ffn, void* stream);
 int kpo_swiglu_bwd(const void* dact, const void* gu, void* dgu, int64_t rows, int64_t ffn, void* stream);
+/* The same on the blocked gate|up layout of kpo_gemm_swiglu: columns [2*b*block, 2*b*block + block) of
+ * gu are gate block b, the next `block` columns the matching up block (block = 0: halves, as above). */
+int kpo_swiglu_fwd_blocked(const void* gu, void* act, int64_t rows, int64_t ffn, int block, void* stream);
+int kpo_swiglu_bwd_blocked(const void* dact, const void* gu, void* dgu, int64_t rows, int64_t ffn, int block,
+                           void* stream);
 
 /* ---------------------------------------------------------------- tensor-core GEMM (tcgen05) */
 /* D[M,N] = A[M,K] * B[K,N]  (+ C[M,N] if C != NULL), bf16 in/out, fp32 accumulation in TMEM.
@@ -92,6 +97,13 @@ int kpo_gemm(const void* A, const void* B, void* D, const void* C, int64_t M, in
 int kpo_gemm_rope(const void* A, const void* B, void* D, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb,
                   int64_t ldd, int max_ctas, int* sched, const float* rope_table, int64_t rope_cols, int head_dim,
                   void* stream);
+/* gate|up projection with the SwiGLU fused into the epilogue: gu[M, N] = A[M, K] @ B[N, K]^T (bf16) and
+ * act[M, N/2] = silu(gate) * up, where B's rows are 128-row gate / up blocks (gate block b = rows
+ * [256b, 256b + 128), its up block the next 128; kpo_swiglu_*_blocked with block = 128 read gu in the
+ * same order).  Fuses the reference's "swiglu" memory-bound KernelSpec into "linear_up"
+ * (workloads.py:61-62).  CTA-pair 256x256 tiles: M >= 256, N % 256 == 0. */
+int kpo_gemm_swiglu(const void* A, const void* B, void* gu, void* act, int64_t M, int64_t N, int64_t K, int64_t lda,
+                    int64_t ldb, int64_t ldgu, int64_t ldact, int max_ctas, int* sched, void* stream);
 /* table[t][i] = (cos, sin)((pos0 + t) * theta^(-2i/head_dim)), fp32, t < tokens, i < head_dim/2. */
 int kpo_rope_table(int64_t tokens, int head_dim, float theta, int64_t pos0, float* table, void* stream);
 

@@ -42,10 +42,14 @@ SIGNATURES = {
     "kpo_rope": (_i32, [_c_void_p, _i64, _c_void_p, _i64, _i64, _i32, _i32, _f32, _i64, _i32, _c_void_p]),
     "kpo_swiglu_fwd": (_i32, [_c_void_p, _c_void_p, _i64, _i64, _c_void_p]),
     "kpo_swiglu_bwd": (_i32, [_c_void_p, _c_void_p, _c_void_p, _i64, _i64, _c_void_p]),
+    "kpo_swiglu_fwd_blocked": (_i32, [_c_void_p, _c_void_p, _i64, _i64, _i32, _c_void_p]),
+    "kpo_swiglu_bwd_blocked": (_i32, [_c_void_p, _c_void_p, _c_void_p, _i64, _i64, _i32, _c_void_p]),
     "kpo_gemm": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _i64, _i64, _i64, _i32, _i32, _i64, _i64,
                         _i64, _i32, _c_void_p, _c_void_p]),
     "kpo_gemm_rope": (_i32, [_c_void_p, _c_void_p, _c_void_p, _i64, _i64, _i64, _i64, _i64, _i64, _i32, _c_void_p,
                              _c_void_p, _i64, _i32, _c_void_p]),
+    "kpo_gemm_swiglu": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _i64, _i64, _i64, _i64, _i64, _i64, _i64,
+                               _i32, _c_void_p, _c_void_p]),
     "kpo_rope_table": (_i32, [_i64, _i32, _f32, _i64, _c_void_p, _c_void_p]),
     "kpo_attn_fwd": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _i64, _i32, _i32, _i32,
                             _i64, _i64, _i64, _i64, _f32, _i32, _c_void_p]),

@@ -424,18 +424,26 @@ __global__ void rope_kernel(const __nv_bfloat16* __restrict__ in, int64_t in_str
 // ===================================================================== SwiGLU
 __device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + __expf(-x)); }
 
+// gate / up column of act column j: halves layout (blk == 0): g at j, u at ffn + j; blocked layout
+// (blk > 0, the fused gate|up GEMM's weight order): blocks of blk gate columns followed by the
+// matching blk up columns.
+__device__ __forceinline__ int64_t gate_col(int64_t j, int64_t ffn, int blk) {
+  return blk ? (j / blk) * 2 * blk + j % blk : j;
+}
+
 __global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ act,
-                                  int64_t rows, int64_t ffn) {
+                                  int64_t rows, int64_t ffn, int blk) {
   KPO_PDL_ENTRY();
   const int64_t nvr = ffn / 8;
   const int64_t total = rows * nvr;
+  const int64_t uoff = blk ? blk : ffn;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = idx / nvr, c = idx % nvr;
-    const __nv_bfloat16* row = gu + r * 2 * ffn;
+    const __nv_bfloat16* gp = gu + r * 2 * ffn + gate_col(c * 8, ffn, blk);
     float g[8], u[8], o[8];
-    unpack8(ld_nc_v4(row + c * 8), g);
-    unpack8(ld_nc_v4(row + ffn + c * 8), u);
+    unpack8(ld_nc_v4(gp), g);
+    unpack8(ld_nc_v4(gp + uoff), u);
 #pragma unroll
     for (int j = 0; j < 8; ++j) o[j] = g[j] * sigmoidf_(g[j]) * u[j];
     *reinterpret_cast<uint4*>(act + r * ffn + c * 8) = pack8(o);
@@ -443,17 +451,18 @@ __global__ void swiglu_fwd_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfl
 }
 
 __global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ dact, const __nv_bfloat16* __restrict__ gu,
-                                  __nv_bfloat16* __restrict__ dgu, int64_t rows, int64_t ffn) {
+                                  __nv_bfloat16* __restrict__ dgu, int64_t rows, int64_t ffn, int blk) {
   KPO_PDL_ENTRY();
   const int64_t nvr = ffn / 8;
   const int64_t total = rows * nvr;
+  const int64_t uoff = blk ? blk : ffn;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = idx / nvr, c = idx % nvr;
-    const __nv_bfloat16* row = gu + r * 2 * ffn;
+    const int64_t gc = r * 2 * ffn + gate_col(c * 8, ffn, blk);
     float g[8], u[8], d[8], dg[8], du[8];
-    unpack8(ld_nc_v4(row + c * 8), g);
-    unpack8(ld_nc_v4(row + ffn + c * 8), u);
+    unpack8(ld_nc_v4(gu + gc), g);
+    unpack8(ld_nc_v4(gu + gc + uoff), u);
     unpack8(ld_nc_v4(dact + r * ffn + c * 8), d);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -462,9 +471,8 @@ __global__ void swiglu_bwd_kernel(const __nv_bfloat16* __restrict__ dact, const 
       du[j] = d[j] * silu;
       dg[j] = d[j] * u[j] * s * (1.f + g[j] * (1.f - s));
     }
-    __nv_bfloat16* orow = dgu + r * 2 * ffn;
-    *reinterpret_cast<uint4*>(orow + c * 8) = pack8(dg);
-    *reinterpret_cast<uint4*>(orow + ffn + c * 8) = pack8(du);
+    *reinterpret_cast<uint4*>(dgu + gc) = pack8(dg);
+    *reinterpret_cast<uint4*>(dgu + gc + uoff) = pack8(du);
   }
 }
 
@@ -622,21 +630,37 @@ extern "C" int kpo_rope_table(int64_t tokens, int head_dim, float theta, int64_t
   return KPO_OK;
 }
 
-extern "C" int kpo_swiglu_fwd(const void* gu, void* act, int64_t rows, int64_t ffn, void* stream) {
+extern "C" int kpo_swiglu_fwd_blocked(const void* gu, void* act, int64_t rows, int64_t ffn, int block,
+                                      void* stream) {
   KPO_CHECK_ARG(gu && act && ffn % 8 == 0 && aligned16(gu) && aligned16(act), "swiglu_fwd: bad args");
+  KPO_CHECK_ARG(block >= 0 && block % 8 == 0 && (block == 0 || ffn % block == 0),
+                "swiglu_fwd: block must be 0 (gate | up halves) or a multiple of 8 dividing ffn");
   if (rows == 0) return KPO_OK;
-  KPO_CUDA(::kpo::pdl_launch(swiglu_fwd_kernel, elem_grid(rows * ffn / 8, 256), 256, 0, (cudaStream_t)stream, 
-      (const __nv_bfloat16*)gu, (__nv_bfloat16*)act, rows, ffn));
+  KPO_CUDA(::kpo::pdl_launch(swiglu_fwd_kernel, elem_grid(rows * ffn / 8, 256), 256, 0, (cudaStream_t)stream,
+                             (const __nv_bfloat16*)gu, (__nv_bfloat16*)act, rows, ffn, block));
+  KPO_LAUNCH_CHECK();
+  return KPO_OK;
+}
+
+extern "C" int kpo_swiglu_fwd(const void* gu, void* act, int64_t rows, int64_t ffn, void* stream) {
+  return kpo_swiglu_fwd_blocked(gu, act, rows, ffn, 0, stream);
+}
+
+extern "C" int kpo_swiglu_bwd_blocked(const void* dact, const void* gu, void* dgu, int64_t rows, int64_t ffn,
+                                      int block, void* stream) {
+  KPO_CHECK_ARG(dact && gu && dgu && ffn % 8 == 0 && aligned16(dact) && aligned16(gu) && aligned16(dgu),
+                "swiglu_bwd: bad args");
+  KPO_CHECK_ARG(block >= 0 && block % 8 == 0 && (block == 0 || ffn % block == 0),
+                "swiglu_bwd: block must be 0 (gate | up halves) or a multiple of 8 dividing ffn");
+  if (rows == 0) return KPO_OK;
+  KPO_CUDA(::kpo::pdl_launch(swiglu_bwd_kernel, elem_grid(rows * ffn / 8, 256), 256, 0, (cudaStream_t)stream,
+                             (const __nv_bfloat16*)dact, (const __nv_bfloat16*)gu, (__nv_bfloat16*)dgu, rows, ffn,
+                             block));
   KPO_LAUNCH_CHECK();
   return KPO_OK;
 }
 
 extern "C" int kpo_swiglu_bwd(const void* dact, const void* gu, void* dgu, int64_t rows, int64_t ffn,
                               void* stream) {
-  KPO_CHECK_ARG(dact && gu && dgu && ffn % 8 == 0, "swiglu_bwd: bad args");
-  if (rows == 0) return KPO_OK;
-  KPO_CUDA(::kpo::pdl_launch(swiglu_bwd_kernel, elem_grid(rows * ffn / 8, 256), 256, 0, (cudaStream_t)stream, 
-      (const __nv_bfloat16*)dact, (const __nv_bfloat16*)gu, (__nv_bfloat16*)dgu, rows, ffn));
-  KPO_LAUNCH_CHECK();
-  return KPO_OK;
+  return kpo_swiglu_bwd_blocked(dact, gu, dgu, rows, ffn, 0, stream);
 }

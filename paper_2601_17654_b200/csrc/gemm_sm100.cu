@@ -212,6 +212,44 @@ __device__ __forceinline__ void epilogue_row(uint32_t tmem_row, const CUtensorMa
   (void)row_ok;
 }
 
+// Fused SwiGLU for the gate|up projection (CTA-pair 256x256 tiles over weights stored in 128-row
+// gate / up blocks, layer.py `interleave_gate_up`): accumulator columns [0, 128) of a tile are gate
+// block nb and [128, 256) the matching up block, so act[:, nb*128 + i] = silu(g_i) * u_i is complete
+// inside one tile.  g / u are rounded to bf16 first, exactly the values the separate swiglu kernel
+// (elementwise.cu) would read back from gu, which is still written for the backward.
+template <int BUFS>
+__device__ __forceinline__ void epilogue_swiglu(uint32_t tmem_row, const CUtensorMap* tmGU, const CUtensorMap* tmAct,
+                                                int gu_col0, int act_col0, int warp_row0, uint32_t stage, int lane,
+                                                int& store_cnt) {
+#pragma unroll 1
+  for (int h2 = 0; h2 < 2; ++h2) {  // 64-column halves of the 128 act columns
+    uint4 pa[8], pg[8], pu[8];
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const int c = h2 * 2 + hh;
+      uint32_t g[32], u[32];
+      tmem_ld32(tmem_row + c * 32, g);
+      tmem_ld32(tmem_row + 128 + c * 32, u);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        float fg[8], fu[8], fa[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          fg[j] = __bfloat162float(__float2bfloat16_rn(__uint_as_float(g[v * 8 + j])));
+          fu[j] = __bfloat162float(__float2bfloat16_rn(__uint_as_float(u[v * 8 + j])));
+          fa[j] = fg[j] * (1.f / (1.f + __expf(-fg[j]))) * fu[j];  // = swiglu_fwd_kernel's expression
+        }
+        pg[hh * 4 + v] = pack8(fg);
+        pu[hh * 4 + v] = pack8(fu);
+        pa[hh * 4 + v] = pack8(fa);
+      }
+    }
+    store_box<BUFS>(stage, lane, store_cnt, pg, tmGU, gu_col0 + h2 * 64, warp_row0);
+    store_box<BUFS>(stage, lane, store_cnt, pu, tmGU, gu_col0 + 128 + h2 * 64, warp_row0);
+    store_box<BUFS>(stage, lane, store_cnt, pa, tmAct, act_col0 + h2 * 64, warp_row0);
+  }
+}
+
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -442,10 +480,10 @@ struct Cfg2 {
   static constexpr int SMEM = EPI_OFF + 4 * EPI_BUFS * 4096 + 1024;
 };
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, bool SWIGLU = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                 const __grid_constant__ CUtensorMap tmD,
+                 const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmAct,
                  __nv_bfloat16* __restrict__ D, const __nv_bfloat16* C /* may alias D */, int M, int N, int K,
                  int64_t ldd, int* __restrict__ sched, RopeArgs rope) {
   ::kpo::pdl_launch_dependents();  // the next kernel may start its prologue; it waits for us
@@ -618,13 +656,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tile_coords(tile, num_m, num_n, mb, nb);
       const int acc = acc_it & 1;
       const int row = mb * 256 + (int)rank * 128 + q * 32 + lane;
-      epilogue_row<BN, CF::EPI_BUFS, !A_MN && !B_MN>(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN, &tmD, C, row, row < M,
-                                     nb * BN, N, ldd, mb * 256 + (int)rank * 128 + q * 32,
-                                     smem_u32(smem + CF::EPI_OFF) + q * CF::EPI_BUFS * 4096, lane, store_cnt, rope,
-                       [&] {
-                         mbar_wait(smem_u32(&tfull[acc]), (acc_it >> 1) & 1);
-                         tc_fence_after();
-                       });
+      if constexpr (SWIGLU) {
+        static_assert(BN == 256 && !A_MN && !B_MN, "fused SwiGLU: TN 256x256 pair tiles");
+        mbar_wait(smem_u32(&tfull[acc]), (acc_it >> 1) & 1);
+        tc_fence_after();
+        epilogue_swiglu<CF::EPI_BUFS>(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN, &tmD, &tmAct, nb * BN,
+                                      nb * (BN / 2), mb * 256 + (int)rank * 128 + q * 32,
+                                      smem_u32(smem + CF::EPI_OFF) + q * CF::EPI_BUFS * 4096, lane, store_cnt);
+      } else {
+        epilogue_row<BN, CF::EPI_BUFS, !A_MN && !B_MN>(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN, &tmD, C, row,
+                                                       row < M, nb * BN, N, ldd, mb * 256 + (int)rank * 128 + q * 32,
+                                                       smem_u32(smem + CF::EPI_OFF) + q * CF::EPI_BUFS * 4096, lane,
+                                                       store_cnt, rope, [&] {
+                                                         mbar_wait(smem_u32(&tfull[acc]), (acc_it >> 1) & 1);
+                                                         tc_fence_after();
+                                                       });
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(leader_tempty0 + acc * 8);
@@ -639,18 +686,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_dealloc_pair(tmem_base, CF::TMEM_COLS);
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, bool SWIGLU = false>
 static int launch2(const CUtensorMap& ta, const CUtensorMap& tb, void* D, const void* C, int64_t M, int64_t N,
-                   int64_t K, int64_t ldd, int grid, int* sched, cudaStream_t s, RopeArgs rope) {
-  auto kern = gemm2_kernel<BN, A_MN, B_MN>;
-  CUtensorMap td;
+                   int64_t K, int64_t ldd, int grid, int* sched, cudaStream_t s, RopeArgs rope,
+                   void* act = nullptr, int64_t ldact = 0) {
+  auto kern = gemm2_kernel<BN, A_MN, B_MN, SWIGLU>;
+  CUtensorMap td, tact;
   if (int e = make_map_2d(&td, D, N, M, ldd, 64, 32)) return e;
+  if (SWIGLU) {
+    if (int e = make_map_2d(&tact, act, N / 2, M, ldact, 64, 32)) return e;
+  } else {
+    tact = td;
+  }
   static bool attr_set = false;
   if (!attr_set) {
     KPO_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2<BN>::SMEM));
     attr_set = true;
   }
-  KPO_CUDA(::kpo::pdl_launch(kern, grid, kThreads, Cfg2<BN>::SMEM, s, ta, tb, td, (__nv_bfloat16*)D, (const __nv_bfloat16*)C, (int)M, (int)N,
+  KPO_CUDA(::kpo::pdl_launch(kern, grid, kThreads, Cfg2<BN>::SMEM, s, ta, tb, td, tact, (__nv_bfloat16*)D, (const __nv_bfloat16*)C, (int)M, (int)N,
                                                (int)K, ldd, sched, rope));
   KPO_LAUNCH_CHECK();
   return KPO_OK;
@@ -837,4 +890,32 @@ extern "C" int kpo_gemm_rope(const void* A, const void* B, void* D, int64_t M, i
                 "gemm_rope: rope_cols must be a positive multiple of head_dim within N");
   return gemm_impl(A, B, D, nullptr, M, N, K, 0, 0, lda, ldb, ldd, max_ctas, sched, stream,
                    kpo::gemm::RopeArgs{reinterpret_cast<const float2*>(rope_table), (int)rope_cols});
+}
+
+extern "C" int kpo_gemm_swiglu(const void* A, const void* B, void* gu, void* act, int64_t M, int64_t N, int64_t K,
+                               int64_t lda, int64_t ldb, int64_t ldgu, int64_t ldact, int max_ctas, int* sched,
+                               void* stream) {
+  using namespace kpo::gemm;
+  KPO_CHECK_ARG(A && B && gu && act && sched, "gemm_swiglu: null pointer");
+  KPO_CHECK_ARG(M >= 256 && M < (1ll << 31) && K > 0 && K % 8 == 0 && K < (1ll << 31),
+                "gemm_swiglu: M must be >= 256 (CTA-pair tiles) and K a positive multiple of 8");
+  KPO_CHECK_ARG(N > 0 && N % 256 == 0 && N < (1ll << 31),
+                "gemm_swiglu: N (= 2 * ffn) must be a multiple of 256 (128-row gate / up blocks)");
+  KPO_CHECK_ARG(lda >= K && ldb >= K && ldgu >= N && ldact >= N / 2 && lda % 8 == 0 && ldb % 8 == 0 &&
+                    ldgu % 8 == 0 && ldact % 8 == 0,
+                "gemm_swiglu: bad leading dimensions");
+  KPO_CHECK_ARG(((uintptr_t)A & 15) == 0 && ((uintptr_t)B & 15) == 0 && ((uintptr_t)gu & 15) == 0 &&
+                    ((uintptr_t)act & 15) == 0,
+                "gemm_swiglu: pointers must be 16B aligned");
+  const int clusters = num_sms() / 2;
+  const int64_t tiles = ((M + 255) / 256) * (N / 256);
+  int cap = max_ctas > 0 ? max_ctas / 2 : clusters;
+  if (cap < 1) cap = 1;
+  if (cap > clusters) cap = clusters;
+  const int grid = 2 * (int)(tiles < cap ? tiles : cap);
+  CUtensorMap ta, tb;
+  if (int e = make_map_2d(&ta, A, K, M, lda, BK, 128)) return e;
+  if (int e = make_map_2d(&tb, B, K, N, ldb, BK, 128)) return e;
+  return launch2<256, false, false, true>(ta, tb, gu, nullptr, M, N, K, ldgu, grid, sched, (cudaStream_t)stream,
+                                          RopeArgs{nullptr, 0}, act, ldact);
 }

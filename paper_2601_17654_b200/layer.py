@@ -129,13 +129,20 @@ class PartitionedLayer:
     def _init_weights(self, seed: int) -> None:
         wl = self.wl
         full = self._full_weights(seed)
+        self._full_for_oracle = full  # reference layout (parity tests)
+        # fused SwiGLU: the engine stores gate|up weights (and so gu / dgu / the wgu gradient) in
+        # 128-row gate / up blocks (ops.interleave_gate_up); weight_grad() returns reference layout
+        self.swiglu_fused = specs.fused_swiglu(wl)
+        if self.swiglu_fused and wl.parallel != "tp":
+            full = dict(full, wgu=ops.interleave_gate_up(full["wgu"]))
         self.full_weights = full if wl.world == 1 or wl.parallel == "fsdp" else None
         self.tensors = ("wqkv", "wo", "wgu", "wd")
         if wl.parallel == "tp":
             self.w = self.tp_shard(full, self.rank)
+            if self.swiglu_fused:
+                self.w["wgu"] = ops.interleave_gate_up(self.w["wgu"])
         else:
             self.w = {k: v for k, v in full.items()}
-        self._full_for_oracle = full  # small configs only (kept for parity tests)
         T, h = wl.tokens, wl.h
         dev = self.device
         c = self.comm
@@ -250,9 +257,12 @@ class PartitionedLayer:
                 "linear_proj": lambda st, a=a, s=s, hp=hp, r=res_attn: ops.linear(
                     a["ao"], W["wo"], hp, residual=r, sched=s["linear_proj"], stream=st),
                 "norm2": lambda st, a=a: ops.rmsnorm_fwd(a["h"], W["g2"], a["xn2"], a["rstd2"], eps, stream=st),
-                "linear_up": lambda st, a=a, s=s: ops.linear(a["xn2"], W["wgu"], a["gu"], sched=s["linear_up"],
-                                                             stream=st),
-                "swiglu": lambda st, a=a: ops.swiglu_fwd(a["gu"], a["act"], stream=st),
+                "linear_up": (lambda st, a=a, s=s: ops.linear_swiglu(a["xn2"], W["wgu"], a["gu"], a["act"],
+                                                                     sched=s["linear_up"], stream=st))
+                if self.swiglu_fused else (lambda st, a=a, s=s: ops.linear(a["xn2"], W["wgu"], a["gu"],
+                                                                          sched=s["linear_up"], stream=st)),
+                "swiglu": lambda st, a=a, blk=ops.SWIGLU_BLOCK if self.swiglu_fused else 0: ops.swiglu_fwd(
+                    a["gu"], a["act"], stream=st, block=blk),
                 "linear_down": lambda st, a=a, s=s, yp=yp, r=res_mlp: ops.linear(
                     a["act"], W["wd"], yp, residual=r, sched=s["linear_down"], stream=st),
                 # ---------------- backward
@@ -263,7 +273,8 @@ class PartitionedLayer:
                 "down_wgrad": lambda st, a=a, s=s, acc=acc: ops.linear_wgrad(
                     a["dy"], a["act"], dw["wd"], accumulate=dw["wd"] if acc else None, sched=s["down_wgrad"],
                     stream=st),
-                "swiglu_bwd": lambda st, a=a: ops.swiglu_bwd(a["dact"], a["gu"], a["dgu"], stream=st),
+                "swiglu_bwd": lambda st, a=a, blk=ops.SWIGLU_BLOCK if self.swiglu_fused else 0: ops.swiglu_bwd(
+                    a["dact"], a["gu"], a["dgu"], stream=st, block=blk),
                 "gu_dgrad": lambda st, a=a, s=s, o=dxn2p: ops.linear_dgrad(a["dgu"], W["wgu"], o,
                                                                            sched=s["gu_dgrad"], stream=st),
                 "gu_wgrad": lambda st, a=a, s=s, acc=acc: ops.linear_wgrad(
@@ -376,4 +387,7 @@ class PartitionedLayer:
         self.finalize_norm_grads(st)
 
     def weight_grad(self, name: str) -> torch.Tensor:
+        """This rank's gradient of weight `name` in the reference layout ([gate; up] for wgu)."""
+        if name == "wgu" and self.swiglu_fused:
+            return ops.deinterleave_gate_up(self.dw[name])
         return self.dw[name]

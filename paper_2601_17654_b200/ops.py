@@ -69,16 +69,46 @@ def rope(inp: torch.Tensor, out: torch.Tensor, heads: int, head_dim: int, theta:
               ctypes.c_float(theta), pos0, int(inverse), _stream(stream))
 
 
-def swiglu_fwd(gu: torch.Tensor, act: torch.Tensor, stream=None) -> None:
+def swiglu_fwd(gu: torch.Tensor, act: torch.Tensor, stream=None, block: int = 0) -> None:
     _need_cuda(gu, act)
     rows, ffn = act.shape
-    _lib.call("kpo_swiglu_fwd", _ptr(gu), _ptr(act), rows, ffn, _stream(stream))
+    _lib.call("kpo_swiglu_fwd_blocked", _ptr(gu), _ptr(act), rows, ffn, block, _stream(stream))
 
 
-def swiglu_bwd(dact: torch.Tensor, gu: torch.Tensor, dgu: torch.Tensor, stream=None) -> None:
+def swiglu_bwd(dact: torch.Tensor, gu: torch.Tensor, dgu: torch.Tensor, stream=None, block: int = 0) -> None:
+    """block = 0: gu = [gate | up] halves; block > 0: the blocked layout of linear_swiglu."""
     _need_cuda(dact, gu, dgu)
     rows, ffn = dact.shape
-    _lib.call("kpo_swiglu_bwd", _ptr(dact), _ptr(gu), _ptr(dgu), rows, ffn, _stream(stream))
+    _lib.call("kpo_swiglu_bwd_blocked", _ptr(dact), _ptr(gu), _ptr(dgu), rows, ffn, block, _stream(stream))
+
+
+# gate / up block of the fused gate|up projection's weight order (kpo_gemm_swiglu)
+SWIGLU_BLOCK = 128
+
+
+def interleave_gate_up(w: torch.Tensor, block: int = SWIGLU_BLOCK) -> torch.Tensor:
+    """[gate (f rows); up (f rows)] -> 128-row blocks g0, u0, g1, u1, ... (rows of any trailing shape)."""
+    f = w.shape[0] // 2
+    tail = w.shape[1:]
+    return w.reshape(2, f // block, block, *tail).transpose(0, 1).reshape(2 * f, *tail).contiguous()
+
+
+def deinterleave_gate_up(w: torch.Tensor, block: int = SWIGLU_BLOCK) -> torch.Tensor:
+    f = w.shape[0] // 2
+    tail = w.shape[1:]
+    return w.reshape(f // block, 2, block, *tail).transpose(0, 1).reshape(2 * f, *tail).contiguous()
+
+
+def linear_swiglu(x: torch.Tensor, w_blocked: torch.Tensor, gu: torch.Tensor, act: torch.Tensor,
+                  max_ctas: int = 0, sched: int | None = None, stream=None) -> None:
+    """gu = x @ w_blocked^T and act = silu(gate) * up in one GEMM (w_blocked = interleave_gate_up(w))."""
+    _need_cuda(x, w_blocked, gu, act)
+    M, K = x.shape
+    N = w_blocked.shape[0]
+    if sched is None:
+        sched = default_sched(x.device)
+    _lib.call("kpo_gemm_swiglu", _ptr(x), _ptr(w_blocked), _ptr(gu), _ptr(act), M, N, K, x.stride(0),
+              w_blocked.stride(0), gu.stride(0), act.stride(0), max_ctas, sched, _stream(stream))
 
 
 # ------------------------------------------------------------------ GEMM

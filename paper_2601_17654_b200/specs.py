@@ -28,12 +28,21 @@ def fused_rope(wl: Workload) -> bool:
     return wl.d == 128 and os.environ.get("KPO_FUSED_ROPE", "1") != "0"
 
 
+def fused_swiglu(wl: Workload) -> bool:
+    """The SwiGLU runs in the gate|up GEMM's epilogue (kpo_gemm_swiglu: CTA-pair 256x256 tiles over
+    128-row gate / up weight blocks), so the forward MLP partition has no separate "swiglu" unit."""
+    return (wl.ffn % 128 == 0 and wl.tokens >= 256
+            and os.environ.get("KPO_FUSED_SWIGLU", "1") != "0")
+
+
 def blocks(wl: Workload) -> list[tuple[str, list[str]]]:
-    if not fused_rope(wl):
-        return list(BLOCKS)
-    fa = [k for k in FWD_ATTN if k != "rope"]
-    ba = [k for k in BWD_ATTN if k != "rope_bwd"]  # dq / dk leave attention backward inverse-rotated
-    return [("fwd_attn", fa), ("fwd_mlp", FWD_MLP), ("bwd_mlp", BWD_MLP), ("bwd_attn", ba)]
+    drop = set()
+    if fused_rope(wl):
+        drop |= {"rope", "rope_bwd"}  # dq / dk leave attention backward inverse-rotated
+    if fused_swiglu(wl):
+        drop.add("swiglu")
+    return [(blk, [k for k in units if k not in drop]) for blk, units in BLOCKS]
+
 
 # FSDP comm units per partition: ('ag', t) all-gathers the next layer's weight t, ('rs', t)
 # reduce-scatters the previous layer's gradient of t (fused into one comm unit, compose.py:32-45).

@@ -20,7 +20,8 @@ def test_partition_specs_shapes(idx):
     assert [p.name for p in parts] == ["fwd_attn0", "fwd_attn1", "fwd_mlp0", "fwd_mlp1", "bwd_mlp0", "bwd_mlp1",
                                        "bwd_attn0", "bwd_attn1"]
     n_fa = 4 if specs.fused_rope(wl) else 5  # head_dim 128: RoPE runs in the QKV GEMM epilogue
-    assert [len(p.comp_kernels) for p in parts] == [n_fa, n_fa, 4, 4, 6, 6, n_fa + 2, n_fa + 2]
+    n_fm = 3 if specs.fused_swiglu(wl) else 4  # SwiGLU in the gate|up GEMM epilogue
+    assert [len(p.comp_kernels) for p in parts] == [n_fa, n_fa, n_fm, n_fm, 6, 6, n_fa + 2, n_fa + 2]
     for p in parts:
         assert p.comm_kernel.is_comm and p.comm_group_size == wl.world
         kinds = {k.name: k.kind for k in p.comp_kernels}

@@ -209,6 +209,52 @@ def test_gemm_rope_epilogue(cuda, M, N, rope_cols):
     assert torch.allclose(table[:, :, 0], c, atol=1e-3) and torch.allclose(table[:, :, 1], s_, atol=1e-3)
 
 
+@pytest.mark.parametrize("M,ffn,K", [(256, 128, 256), (1000, 1024, 512), (4096, 1792, 4096)])
+def test_gemm_swiglu_epilogue(cuda, M, ffn, K):
+    """Fused SwiGLU epilogue of the gate|up projection: gu (blocked layout) equals the plain GEMM over the
+    blocked weights bit-exactly, and act equals the separate swiglu kernel on that gu bit-exactly
+    (both compute bf16 g * sigmoid(bf16 g) * bf16 u in fp32); act vs the fp32 reference within bf16
+    tolerance."""
+    from paper_2601_17654_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(M + ffn)
+    x = torch.randn(M, K, device=cuda, generator=g).bfloat16()
+    w = (torch.randn(2 * ffn, K, device=cuda, generator=g) * 0.05).bfloat16()
+    wb = ops.interleave_gate_up(w)
+    assert torch.equal(ops.deinterleave_gate_up(wb), w)
+    gu = torch.empty(M, 2 * ffn, device=cuda, dtype=torch.bfloat16)
+    act = torch.empty(M, ffn, device=cuda, dtype=torch.bfloat16)
+    ops.linear_swiglu(x, wb, gu, act)
+    gu_plain = torch.empty_like(gu)
+    ops.linear(x, wb, gu_plain)
+    act_sep = torch.empty_like(act)
+    ops.swiglu_fwd(gu_plain, act_sep, block=ops.SWIGLU_BLOCK)
+    torch.cuda.synchronize()
+    assert torch.equal(gu, gu_plain)
+    assert torch.equal(act, act_sep)
+    ref_gu = x.float() @ w.float().t()
+    ref = torch.nn.functional.silu(ref_gu[:, :ffn]) * ref_gu[:, ffn:]
+    assert rel_err(act, ref) < 1e-2
+    assert rel_err(ops.deinterleave_gate_up(gu.t()).t(), ref_gu) < 8e-3
+
+
+def test_swiglu_blocked_layout(cuda):
+    """The blocked gate|up layout (block 128) gives the same act / dgu as the halves layout, permuted."""
+    from paper_2601_17654_b200 import ops
+    rows, ffn = 300, 768
+    gu = torch.randn(rows, 2 * ffn, device=cuda).bfloat16()
+    gub = ops.interleave_gate_up(gu.t()).t().contiguous()
+    act, actb = (torch.empty(rows, ffn, device=cuda, dtype=torch.bfloat16) for _ in range(2))
+    ops.swiglu_fwd(gu, act)
+    ops.swiglu_fwd(gub, actb, block=128)
+    dact = torch.randn_like(act)
+    dgu, dgub = torch.empty_like(gu), torch.empty_like(gu)
+    ops.swiglu_bwd(dact, gu, dgu)
+    ops.swiglu_bwd(dact, gub, dgub, block=128)
+    torch.cuda.synchronize()
+    assert torch.equal(act, actb)
+    assert torch.equal(ops.deinterleave_gate_up(dgub.t()).t(), dgu)
+
+
 @pytest.mark.parametrize("T,hq,hkv", [(1024, 8, 2), (512, 4, 1)])
 def test_attention_bwd_rope_fused(cuda, T, hq, hkv):
     """attn_bwd with the fused inverse rotary (q / k rotated by the QKV epilogue) equals attn_bwd followed

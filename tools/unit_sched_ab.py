@@ -40,16 +40,30 @@ for _ in range(20):
     r.step()
 e1.record(eng.exec.compute)
 torch.cuda.synchronize()
-step_ms = e0.elapsed_time(e1) / 20
-ok = r.capture_step()
+print(json.dumps({"step_ms": e0.elapsed_time(e1) / 20,
+                  "unit_sum_default_ms": sum(out["default"].values()),
+                  "n_units": len(out["default"])}))
+
+# the same launch units, collectives replaced by no-ops, per-partition graphs: the compute-only step
+import dataclasses
+from paper_2601_17654_b200.runner import sequential_schedule as _seq
+progs = {}
+for name in layer.order:
+    p = layer.programs[name]
+    nocomm = dataclasses.replace(p.comm, fn=lambda st, ncta: None)
+    progs[name] = type(p)(p.name, p.units, nocomm, p.comm_group_size)
+saved = dict(layer.programs)
+layer.programs.update(progs)
+eng.exec.graphs.clear()
+r3 = LayerRunner(layer, eng, schedule=_seq(layer, eng.gpu))
+r3.warm()
 for _ in range(5):
-    r.step()
+    r3.step()
 torch.cuda.synchronize()
 e0.record(eng.exec.compute)
 for _ in range(20):
-    r.step()
+    r3.step()
 e1.record(eng.exec.compute)
 torch.cuda.synchronize()
-print(json.dumps({"step_ms": step_ms, "step_graph_ms": e0.elapsed_time(e1) / 20, "captured": ok,
-                  "unit_sum_default_ms": sum(out["default"].values()),
-                  "n_units": len(out["default"])}))
+print(json.dumps({"compute_only_ms": e0.elapsed_time(e1) / 20}))
+layer.programs.update(saved)

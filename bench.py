@@ -259,6 +259,14 @@ def run_kpo(args):
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     clocks = eng.sampler.clocks_summary(t0, t1)
 
+    # ------------------------------------------------ dominant kernel: per-unit times inside the step
+    # (right after the timed steps, in the same thermal / power state as the headline number)
+    try:
+        ut = run.unit_times_graph(iters=3)
+        ut_mode = "graph replay"
+    except Exception as ex:  # capture unsupported: eager issue with the same events
+        ut = run.unit_times(iters=3)
+        ut_mode = "eager (" + type(ex).__name__ + ")"
     # ------------------------------------------------ end to end through the host-buffer entry point
     pin = lambda t: torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
     xs = [pin(a["x"]).copy_(a["x"].cpu()) for a in layer.nb]
@@ -288,13 +296,6 @@ def run_kpo(args):
     h2d = sum(t.numel() * t.element_size() for t in xs + dys)
     d2h = sum(t.numel() * t.element_size() for t in dxs)
 
-    # ------------------------------------------------ dominant kernel: per-unit times inside the step
-    try:
-        ut = run.unit_times_graph(iters=3)
-        ut_mode = "graph replay"
-    except Exception as ex:  # capture unsupported: eager issue with the same events
-        ut = run.unit_times(iters=3)
-        ut_mode = "eager (" + type(ex).__name__ + ")"
     per_unit = {}
     for name in layer.order:
         for u in layer.programs[name].units:

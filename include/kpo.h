@@ -104,6 +104,15 @@ int kpo_gemm_rope(const void* A, const void* B, void* D, int64_t M, int64_t N, i
  * (workloads.py:61-62).  CTA-pair 256x256 tiles: M >= 256, N % 256 == 0. */
 int kpo_gemm_swiglu(const void* A, const void* B, void* gu, void* act, int64_t M, int64_t N, int64_t K, int64_t lda,
                     int64_t ldb, int64_t ldgu, int64_t ldact, int max_ctas, int* sched, void* stream);
+/* down-projection dgrad with the SwiGLU backward fused into the epilogue: dact = dy[M, K] @ w[K, N]
+ * (w = the down weight [hidden, ffn], MN-major B) is never written; per tile the epilogue TMA-loads the
+ * matching gate / up boxes of gu (128-blocked order of kpo_gemm_swiglu, [M, 2N]) and writes
+ * dgu [M, 2N] = (dact * u * sig(g) * (1 + g * (1 - sig(g))), dact * silu(g)) in the same order.
+ * Fuses the reference's "swiglu" backward into "linear_down"'s dgrad (workloads.py:61-62).
+ * CTA-pair 256x256 tiles: M >= 256, N % 256 == 0. */
+int kpo_gemm_swiglu_bwd(const void* dy, const void* w, const void* gu, void* dgu, int64_t M, int64_t N, int64_t K,
+                        int64_t lddy, int64_t ldw, int64_t ldgu, int64_t lddgu, int max_ctas, int* sched,
+                        void* stream);
 /* table[t][i] = (cos, sin)((pos0 + t) * theta^(-2i/head_dim)), fp32, t < tokens, i < head_dim/2. */
 int kpo_rope_table(int64_t tokens, int head_dim, float theta, int64_t pos0, float* table, void* stream);
 

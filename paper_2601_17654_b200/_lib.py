@@ -50,6 +50,8 @@ SIGNATURES = {
                              _c_void_p, _i64, _i32, _c_void_p]),
     "kpo_gemm_swiglu": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _i64, _i64, _i64, _i64, _i64, _i64, _i64,
                                _i32, _c_void_p, _c_void_p]),
+    "kpo_gemm_swiglu_bwd": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _i64, _i64, _i64, _i64, _i64, _i64,
+                                   _i64, _i32, _c_void_p, _c_void_p]),
     "kpo_rope_table": (_i32, [_i64, _i32, _f32, _i64, _c_void_p, _c_void_p]),
     "kpo_attn_fwd": (_i32, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _i64, _i32, _i32, _i32,
                             _i64, _i64, _i64, _i64, _f32, _i32, _c_void_p]),

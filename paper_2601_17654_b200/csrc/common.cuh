@@ -144,6 +144,11 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// logistic sigmoid for the SwiGLU kernels and the fused GEMM epilogues (one definition, so the fused
+// and separate paths are bit-identical): MUFU ex2 + MUFU rcp (__fdividef), no IEEE division.  For
+// x < -87 the denominator overflows and the result is 0, the correctly rounded limit.
+__device__ __forceinline__ float kpo_sigmoid(float x) { return __fdividef(1.f, 1.f + __expf(-x)); }
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -422,7 +422,7 @@ __global__ void rope_kernel(const __nv_bfloat16* __restrict__ in, int64_t in_str
 }
 
 // ===================================================================== SwiGLU
-__device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + __expf(-x)); }
+__device__ __forceinline__ float sigmoidf_(float x) { return kpo_sigmoid(x); }
 
 // gate / up column of act column j: halves layout (blk == 0): g at j, u at ffn + j; blocked layout
 // (blk > 0, the fused gate|up GEMM's weight order): blocks of blk gate columns followed by the

@@ -237,7 +237,7 @@ __device__ __forceinline__ void epilogue_swiglu(uint32_t tmem_row, const CUtenso
         for (int j = 0; j < 8; ++j) {
           fg[j] = __bfloat162float(__float2bfloat16_rn(__uint_as_float(g[v * 8 + j])));
           fu[j] = __bfloat162float(__float2bfloat16_rn(__uint_as_float(u[v * 8 + j])));
-          fa[j] = fg[j] * (1.f / (1.f + __expf(-fg[j]))) * fu[j];  // = swiglu_fwd_kernel's expression
+          fa[j] = fg[j] * kpo_sigmoid(fg[j]) * fu[j];  // = swiglu_fwd_kernel's expression
         }
         pg[hh * 4 + v] = pack8(fg);
         pu[hh * 4 + v] = pack8(fu);
@@ -248,6 +248,93 @@ __device__ __forceinline__ void epilogue_swiglu(uint32_t tmem_row, const CUtenso
     store_box<BUFS>(stage, lane, store_cnt, pu, tmGU, gu_col0 + 128 + h2 * 64, warp_row0);
     store_box<BUFS>(stage, lane, store_cnt, pa, tmAct, act_col0 + h2 * 64, warp_row0);
   }
+}
+
+// Fused SwiGLU backward for the down-projection dgrad (CTA-pair 256x256 tiles; gu / dgu in the 128-
+// blocked gate|up order): the tile's accumulator is dact[:, nb*256 .. +256), i.e. gate/up blocks
+// 2nb and 2nb+1, whose gate and up columns are the contiguous gu columns [512 nb, 512 nb + 512).
+// Per 64 dact columns a warp TMA-loads its 32 rows of the matching gate box and up box into its
+// staging buffers (the load for the first chunk is issued before the accumulator is ready), rounds
+// dact to bf16 (the value the separate kernel would read), computes dgate / dup with
+// swiglu_bwd_kernel's expressions in place, and TMA-stores both boxes to dgu.  dact itself is never
+// written.
+template <typename WaitAcc, typename Release>
+__device__ __forceinline__ void epilogue_swiglu_bwd(uint32_t tmem_row, const CUtensorMap* tmDGU,
+                                                    const CUtensorMap* tmGU, int act_col0, int warp_row0,
+                                                    uint32_t stage, uint32_t bar, uint32_t& nchunk, int lane,
+                                                    WaitAcc wait_acc, Release release_acc) {
+  // two box-pair slots of 8 KB: chunk c+1's loads are issued before chunk c is computed
+  auto gcol_of = [&](int c) { return (act_col0 / 128 + (c >> 1)) * 256 + (c & 1) * 64; };
+  auto issue = [&](int c, uint32_t n) {
+    const uint32_t buf = stage + (n & 1) * 8192;
+    if (lane == 0) {
+      // the slot's previous stores (chunk n-2) are the only bulk group still outstanding: once they have
+      // read the buffers, the loads may overwrite them
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      const uint32_t b = bar + (n & 1) * 8;
+      mbar_arrive_expect_tx(b, 8192);
+      tma_load_2d(buf, tmGU, b, gcol_of(c), warp_row0);
+      tma_load_2d(buf + 4096, tmGU, b, gcol_of(c) + 128, warp_row0);
+    }
+  };
+  issue(0, nchunk);
+  wait_acc();
+#pragma unroll 1
+  for (int c = 0; c < 4; ++c) {
+    const uint32_t n = nchunk + c;
+    uint32_t dv[64];
+    tmem_ld32_nowait(tmem_row + c * 64, dv);
+    tmem_ld32_nowait(tmem_row + c * 64 + 32, dv + 32);
+    tmem_wait_ld();
+    if (c == 3) release_acc();
+    if (c < 3) issue(c + 1, n + 1);
+    const uint32_t buf = stage + (n & 1) * 8192;
+    mbar_wait(bar + (n & 1) * 8, (n >> 1) & 1);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t off = lane * 128 + ((k ^ (lane & 7)) << 4);
+      uint4 gv, uv;
+      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(gv.x), "=r"(gv.y), "=r"(gv.z), "=r"(gv.w)
+                   : "r"(buf + off));
+      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(uv.x), "=r"(uv.y), "=r"(uv.z), "=r"(uv.w)
+                   : "r"(buf + 4096 + off));
+      float g[8], u[8], dg[8], du[8];
+      unpack8(gv, g);
+      unpack8(uv, u);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float dd = __bfloat162float(__float2bfloat16_rn(__uint_as_float(dv[k * 8 + j])));
+        const float sg = kpo_sigmoid(g[j]);
+        const float silu = g[j] * sg;
+        du[j] = dd * silu;
+        dg[j] = dd * u[j] * sg * (1.f + g[j] * (1.f - sg));
+      }
+      const uint4 pg = pack8(dg), pu = pack8(du);
+      asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(buf + off), "r"(pg.x), "r"(pg.y), "r"(pg.z),
+                   "r"(pg.w)
+                   : "memory");
+      asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(buf + 4096 + off), "r"(pu.x), "r"(pu.y),
+                   "r"(pu.z), "r"(pu.w)
+                   : "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      const int gcol = gcol_of(c);
+      asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                       reinterpret_cast<uint64_t>(tmDGU)),
+                   "r"(buf), "r"(gcol), "r"(warp_row0)
+                   : "memory");
+      asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                       reinterpret_cast<uint64_t>(tmDGU)),
+                   "r"(buf + 4096), "r"(gcol + 128), "r"(warp_row0)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  nchunk += 4;
 }
 
 template <int BN, bool A_MN, bool B_MN>
@@ -467,27 +554,31 @@ static int launch(const CUtensorMap& ta, const CUtensorMap& tb, void* D, const v
 //   * the leader fetches tile ids from the global scheduler word and broadcasts them to the peer
 //     through distributed shared memory; consumers in the peer arrive remotely on the leader's
 //     sempty[] / tempty[] barriers.
-template <int BN>
+template <int BN, int EPI = 0>
 struct Cfg2 {
   static constexpr int A_BYTES = 128 * BK * 2;
   static constexpr int B_BYTES = (BN / 2) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (BN == 256) ? 6 : 7;
+  // the fused SwiGLU backward's epilogue double-buffers its gate / up boxes: 4 buffers per warp, one
+  // operand stage fewer
+  static constexpr int STAGES = (BN == 256) ? (EPI == 2 ? 5 : 6) : 7;
   static constexpr int TMEM_COLS = (2 * BN <= 256) ? 256 : 512;
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
   static constexpr int EPI_OFF = BAR_OFF + 1024;
-  static constexpr int EPI_BUFS = (EPI_OFF + 4 * 2 * 4096 + 1024 <= 232448) ? 2 : 1;
+  static constexpr int EPI_BUFS = EPI == 2 ? 4 : ((EPI_OFF + 4 * 2 * 4096 + 1024 <= 232448) ? 2 : 1);
   static constexpr int SMEM = EPI_OFF + 4 * EPI_BUFS * 4096 + 1024;
 };
 
-template <int BN, bool A_MN, bool B_MN, bool SWIGLU = false>
+// EPI: 0 = plain / residual / rope epilogue, 1 = fused SwiGLU (gate|up forward), 2 = fused SwiGLU
+// backward (down-projection dgrad)
+template <int BN, bool A_MN, bool B_MN, int EPI = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmAct,
                  __nv_bfloat16* __restrict__ D, const __nv_bfloat16* C /* may alias D */, int M, int N, int K,
                  int64_t ldd, int* __restrict__ sched, RopeArgs rope) {
   ::kpo::pdl_launch_dependents();  // the next kernel may start its prologue; it waits for us
-  using CF = Cfg2<BN>;
+  using CF = Cfg2<BN, EPI>;
   constexpr int STAGES = CF::STAGES;
   constexpr int HB = BN / 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -501,6 +592,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* sempty = sfull + 2;
   int* stile = reinterpret_cast<int*>(sempty + 2);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stile + 2);
+  uint64_t* ebar = sempty + 4;  // [warp][slot]: TMA loads of the fused SwiGLU backward's gu boxes
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -520,6 +612,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(&sfull[i]), 1);
       mbar_init(smem_u32(&sempty[i]), 10);
     }
+    if (EPI == 2)
+      for (int i = 0; i < 8; ++i) mbar_init(smem_u32(&ebar[i]), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -640,6 +734,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // ===================== epilogue warps 2..5 (both CTAs): this CTA's 128 rows, all BN columns
     const int q = warp & 3;
     int it = 0, acc_it = 0, store_cnt = 0;
+    uint32_t echunks = 0;  // fused SwiGLU backward: gate / up box pairs this warp has consumed
     while (true) {
       const int slot = it & 1;
       if (leader) mbar_wait(smem_u32(&sfull[slot]), (it >> 1) & 1);
@@ -656,7 +751,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tile_coords(tile, num_m, num_n, mb, nb);
       const int acc = acc_it & 1;
       const int row = mb * 256 + (int)rank * 128 + q * 32 + lane;
-      if constexpr (SWIGLU) {
+      if constexpr (EPI == 2) {
+        static_assert(BN == 256, "fused SwiGLU backward: 256x256 pair tiles");
+        epilogue_swiglu_bwd(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN, &tmD, &tmAct, nb * BN,
+                            mb * 256 + (int)rank * 128 + q * 32,
+                            smem_u32(smem + CF::EPI_OFF) + q * CF::EPI_BUFS * 4096, smem_u32(&ebar[q * 2]), echunks,
+                            lane,
+                            [&] {
+                              mbar_wait(smem_u32(&tfull[acc]), (acc_it >> 1) & 1);
+                              tc_fence_after();
+                            },
+                            [&] {  // the accumulator is in registers: release it to the MMA warp
+                              tc_fence_before();
+                              __syncwarp();
+                              if (lane == 0) mbar_arrive_remote(leader_tempty0 + acc * 8);
+                            });
+      } else if constexpr (EPI == 1) {
         static_assert(BN == 256 && !A_MN && !B_MN, "fused SwiGLU: TN 256x256 pair tiles");
         mbar_wait(smem_u32(&tfull[acc]), (acc_it >> 1) & 1);
         tc_fence_after();
@@ -672,9 +782,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                                          tc_fence_after();
                                                        });
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_remote(leader_tempty0 + acc * 8);
+      if constexpr (EPI != 2) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(leader_tempty0 + acc * 8);
+      }
       ++acc_it;
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // D stores complete
@@ -686,24 +798,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_dealloc_pair(tmem_base, CF::TMEM_COLS);
 }
 
-template <int BN, bool A_MN, bool B_MN, bool SWIGLU = false>
+template <int BN, bool A_MN, bool B_MN, int EPI = 0>
 static int launch2(const CUtensorMap& ta, const CUtensorMap& tb, void* D, const void* C, int64_t M, int64_t N,
                    int64_t K, int64_t ldd, int grid, int* sched, cudaStream_t s, RopeArgs rope,
                    void* act = nullptr, int64_t ldact = 0) {
-  auto kern = gemm2_kernel<BN, A_MN, B_MN, SWIGLU>;
+  auto kern = gemm2_kernel<BN, A_MN, B_MN, EPI>;
   CUtensorMap td, tact;
-  if (int e = make_map_2d(&td, D, N, M, ldd, 64, 32)) return e;
-  if (SWIGLU) {
+  // EPI 2: D = dgu [M, 2N] (output), act = gu [M, 2N] (loaded); EPI 1: D = gu [M, N], act [M, N/2]
+  if (int e = make_map_2d(&td, D, EPI == 2 ? 2 * N : N, M, ldd, 64, 32)) return e;
+  if (EPI == 1) {
     if (int e = make_map_2d(&tact, act, N / 2, M, ldact, 64, 32)) return e;
+  } else if (EPI == 2) {
+    if (int e = make_map_2d(&tact, act, 2 * N, M, ldact, 64, 32)) return e;
   } else {
     tact = td;
   }
   static bool attr_set = false;
   if (!attr_set) {
-    KPO_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2<BN>::SMEM));
+    KPO_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2<BN, EPI>::SMEM));
     attr_set = true;
   }
-  KPO_CUDA(::kpo::pdl_launch(kern, grid, kThreads, Cfg2<BN>::SMEM, s, ta, tb, td, tact, (__nv_bfloat16*)D, (const __nv_bfloat16*)C, (int)M, (int)N,
+  KPO_CUDA(::kpo::pdl_launch(kern, grid, kThreads, Cfg2<BN, EPI>::SMEM, s, ta, tb, td, tact, (__nv_bfloat16*)D, (const __nv_bfloat16*)C, (int)M, (int)N,
                                                (int)K, ldd, sched, rope));
   KPO_LAUNCH_CHECK();
   return KPO_OK;
@@ -916,6 +1031,34 @@ extern "C" int kpo_gemm_swiglu(const void* A, const void* B, void* gu, void* act
   CUtensorMap ta, tb;
   if (int e = make_map_2d(&ta, A, K, M, lda, BK, 128)) return e;
   if (int e = make_map_2d(&tb, B, K, N, ldb, BK, 128)) return e;
-  return launch2<256, false, false, true>(ta, tb, gu, nullptr, M, N, K, ldgu, grid, sched, (cudaStream_t)stream,
+  return launch2<256, false, false, 1>(ta, tb, gu, nullptr, M, N, K, ldgu, grid, sched, (cudaStream_t)stream,
                                           RopeArgs{nullptr, 0}, act, ldact);
+}
+
+extern "C" int kpo_gemm_swiglu_bwd(const void* dy, const void* w, const void* gu, void* dgu, int64_t M, int64_t N,
+                                   int64_t K, int64_t lddy, int64_t ldw, int64_t ldgu, int64_t lddgu, int max_ctas,
+                                   int* sched, void* stream) {
+  using namespace kpo::gemm;
+  KPO_CHECK_ARG(dy && w && gu && dgu && sched, "gemm_swiglu_bwd: null pointer");
+  KPO_CHECK_ARG(M >= 256 && M < (1ll << 31) && K > 0 && K % 8 == 0 && K < (1ll << 31),
+                "gemm_swiglu_bwd: M must be >= 256 (CTA-pair tiles) and K a positive multiple of 8");
+  KPO_CHECK_ARG(N > 0 && N % 256 == 0 && N < (1ll << 30),
+                "gemm_swiglu_bwd: N (= ffn) must be a multiple of 256 (two 128-column gate / up blocks per tile)");
+  KPO_CHECK_ARG(lddy >= K && ldw >= N && ldgu >= 2 * N && lddgu >= 2 * N && lddy % 8 == 0 && ldw % 8 == 0 &&
+                    ldgu % 8 == 0 && lddgu % 8 == 0,
+                "gemm_swiglu_bwd: bad leading dimensions");
+  KPO_CHECK_ARG(((uintptr_t)dy & 15) == 0 && ((uintptr_t)w & 15) == 0 && ((uintptr_t)gu & 15) == 0 &&
+                    ((uintptr_t)dgu & 15) == 0,
+                "gemm_swiglu_bwd: pointers must be 16B aligned");
+  const int clusters = num_sms() / 2;
+  const int64_t tiles = ((M + 255) / 256) * (N / 256);
+  int cap = max_ctas > 0 ? max_ctas / 2 : clusters;
+  if (cap < 1) cap = 1;
+  if (cap > clusters) cap = clusters;
+  const int grid = 2 * (int)(tiles < cap ? tiles : cap);
+  CUtensorMap ta, tb;
+  if (int e = make_map_2d(&ta, dy, K, M, lddy, BK, 128)) return e;
+  if (int e = make_map_2d(&tb, w, N, K, ldw, 64, BK)) return e;
+  return launch2<256, false, true, 2>(ta, tb, dgu, nullptr, M, N, K, lddgu, grid, sched, (cudaStream_t)stream,
+                                      RopeArgs{nullptr, 0}, const_cast<void*>(gu), ldgu);
 }

@@ -268,8 +268,11 @@ class PartitionedLayer:
                 # ---------------- backward
                 "norm1_bwd": lambda st, a=a: ops.rmsnorm_bwd(a["dxn1"], a["x"], W["g1"], a["rstd1"], a["dx"],
                                                              a["dwp1"], dres=a["dh"], stream=st),
-                "down_dgrad": lambda st, a=a, s=s: ops.linear_dgrad(a["dy"], W["wd"], a["dact"],
-                                                                    sched=s["down_dgrad"], stream=st),
+                # fused: dgu straight from the dgrad's epilogue (dact never materialised)
+                "down_dgrad": (lambda st, a=a, s=s: ops.linear_dgrad_swiglu_bwd(
+                    a["dy"], W["wd"], a["gu"], a["dgu"], sched=s["down_dgrad"], stream=st))
+                if specs.fused_swiglu_bwd(wl) else (lambda st, a=a, s=s: ops.linear_dgrad(
+                    a["dy"], W["wd"], a["dact"], sched=s["down_dgrad"], stream=st)),
                 "down_wgrad": lambda st, a=a, s=s, acc=acc: ops.linear_wgrad(
                     a["dy"], a["act"], dw["wd"], accumulate=dw["wd"] if acc else None, sched=s["down_wgrad"],
                     stream=st),

@@ -173,6 +173,19 @@ def linear_rope(x: torch.Tensor, w: torch.Tensor, out: torch.Tensor, table: torc
               max_ctas, sched, _ptr(table), rope_cols, head_dim, _stream(stream))
 
 
+def linear_dgrad_swiglu_bwd(dy: torch.Tensor, w: torch.Tensor, gu: torch.Tensor, dgu: torch.Tensor,
+                            max_ctas: int = 0, sched: int | None = None, stream=None) -> None:
+    """dgu = swiglu_bwd(dy @ w, gu) in one GEMM (gu / dgu in the blocked order of linear_swiglu;
+    w = the down weight [hidden, ffn])."""
+    _need_cuda(dy, w, gu, dgu)
+    M, K = dy.shape
+    N = w.shape[1]
+    if sched is None:
+        sched = default_sched(dy.device)
+    _lib.call("kpo_gemm_swiglu_bwd", _ptr(dy), _ptr(w), _ptr(gu), _ptr(dgu), M, N, K, dy.stride(0), w.stride(0),
+              gu.stride(0), dgu.stride(0), max_ctas, sched, _stream(stream))
+
+
 def linear_dgrad(dy: torch.Tensor, w: torch.Tensor, dx: torch.Tensor, accumulate: torch.Tensor | None = None,
                  **kw) -> None:
     """dx[M,K] = dy[M,N] @ w[N,K]  (B is MN-major: w rows are the reduction dim)."""

@@ -35,12 +35,21 @@ def fused_swiglu(wl: Workload) -> bool:
             and os.environ.get("KPO_FUSED_SWIGLU", "1") != "0")
 
 
+def fused_swiglu_bwd(wl: Workload) -> bool:
+    """The SwiGLU backward runs in the down-projection dgrad's epilogue (kpo_gemm_swiglu_bwd), so the
+    backward MLP partition has no separate "swiglu_bwd" unit (needs ffn % 256 == 0)."""
+    return (fused_swiglu(wl) and wl.ffn % 256 == 0
+            and os.environ.get("KPO_FUSED_SWIGLU_BWD", "1") != "0")
+
+
 def blocks(wl: Workload) -> list[tuple[str, list[str]]]:
     drop = set()
     if fused_rope(wl):
         drop |= {"rope", "rope_bwd"}  # dq / dk leave attention backward inverse-rotated
     if fused_swiglu(wl):
         drop.add("swiglu")
+    if fused_swiglu_bwd(wl):
+        drop.add("swiglu_bwd")
     return [(blk, [k for k in units if k not in drop]) for blk, units in BLOCKS]
 
 

@@ -21,7 +21,8 @@ def test_partition_specs_shapes(idx):
                                        "bwd_attn0", "bwd_attn1"]
     n_fa = 4 if specs.fused_rope(wl) else 5  # head_dim 128: RoPE runs in the QKV GEMM epilogue
     n_fm = 3 if specs.fused_swiglu(wl) else 4  # SwiGLU in the gate|up GEMM epilogue
-    assert [len(p.comp_kernels) for p in parts] == [n_fa, n_fa, n_fm, n_fm, 6, 6, n_fa + 2, n_fa + 2]
+    n_bm = 5 if specs.fused_swiglu_bwd(wl) else 6  # SwiGLU backward in the down dgrad epilogue
+    assert [len(p.comp_kernels) for p in parts] == [n_fa, n_fa, n_fm, n_fm, n_bm, n_bm, n_fa + 2, n_fa + 2]
     for p in parts:
         assert p.comm_kernel.is_comm and p.comm_group_size == wl.world
         kinds = {k.name: k.kind for k in p.comp_kernels}

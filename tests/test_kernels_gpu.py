@@ -237,6 +237,29 @@ def test_gemm_swiglu_epilogue(cuda, M, ffn, K):
     assert rel_err(ops.deinterleave_gate_up(gu.t()).t(), ref_gu) < 8e-3
 
 
+@pytest.mark.parametrize("M,ffn,K", [(256, 256, 256), (1000, 1024, 512), (4096, 1792, 4096)])
+def test_gemm_swiglu_bwd_epilogue(cuda, M, ffn, K):
+    """Fused SwiGLU backward in the down dgrad: dgu equals linear_dgrad followed by the blocked swiglu_bwd
+    kernel bit-exactly (dact rounded to bf16 first, same expressions); and vs autograd in fp32."""
+    from paper_2601_17654_b200 import ops
+    g = torch.Generator(device="cuda").manual_seed(M + ffn + K)
+    dy = torch.randn(M, K, device=cuda, generator=g).bfloat16()
+    wd = (torch.randn(K, ffn, device=cuda, generator=g) * 0.05).bfloat16()
+    gu = torch.randn(M, 2 * ffn, device=cuda, generator=g).bfloat16()
+    dgu = torch.full((M, 2 * ffn), float("nan"), device=cuda, dtype=torch.bfloat16)
+    ops.linear_dgrad_swiglu_bwd(dy, wd, gu, dgu)
+    dact = torch.empty(M, ffn, device=cuda, dtype=torch.bfloat16)
+    ops.linear_dgrad(dy, wd, dact)
+    dgu_sep = torch.empty_like(gu)
+    ops.swiglu_bwd(dact, gu, dgu_sep, block=ops.SWIGLU_BLOCK)
+    torch.cuda.synchronize()
+    assert torch.equal(dgu, dgu_sep)
+    guh = ops.deinterleave_gate_up(gu.t()).t().float().requires_grad_()
+    act = torch.nn.functional.silu(guh[:, :ffn]) * guh[:, ffn:]
+    act.backward(dy.float() @ wd.float())
+    assert rel_err(ops.deinterleave_gate_up(dgu.t()).t(), guh.grad) < 1e-2
+
+
 def test_swiglu_blocked_layout(cuda):
     """The blocked gate|up layout (block 128) gives the same act / dgu as the halves layout, permuted."""
     from paper_2601_17654_b200 import ops

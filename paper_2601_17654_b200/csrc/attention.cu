@@ -574,7 +574,8 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* o
     // split-group mode when kv heads x key tiles cannot fill the GPU (e.g. TP8: one kv head per rank):
     // one CTA per (q head, key tile), dK/dV reduced in fp32 then converted
     const int64_t ntiles = (T + 127) / 128;
-    const bool split = hq > hkv && hkv * ntiles < num_sms();
+    static const int force_split = getenv("KPO_ATTN_BWD_SPLIT") ? atoi(getenv("KPO_ATTN_BWD_SPLIT")) : -1;
+    const bool split = force_split >= 0 ? (force_split != 0 && hq > hkv) : (hq > hkv && hkv * ntiles < num_sms());
     float* dkv_acc = split ? dvec + (int64_t)hq * T : nullptr;
     if (split) KPO_CUDA(cudaMemsetAsync(dkv_acc, 0, sizeof(float) * 2 * T * hkv * D, s));
     int st = attn_bwd_tcgen05_main(q, k, v, dout, lse, dvec, dq_acc, dk, dv, T, hq, hkv, D, qs, ks, vs, os, dks, dvs,

@@ -704,8 +704,18 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
   const int h_first = split ? (int)blockIdx.x : (int)blockIdx.x * (hq / hkv);
   const int kvh = split ? (int)blockIdx.x / (hq / hkv) : (int)blockIdx.x;
   const int n0 = nblk * BN;
-  const int m_start = causal ? n0 / BM : 0;
-  const int mq = (T + BM - 1) / BM - m_start;
+  const int total_m = (T + BM - 1) / BM;
+  int m_start = causal ? n0 / BM : 0, m_end = total_m;
+  if (split && gridDim.z > 1) {
+    // split-group mode with query chunks (blockIdx.z): this CTA takes the query tiles of chunk z, so
+    // the long causal key tiles are spread over several SMs; dK / dV partials meet in the fp32
+    // accumulators, dQ in dq_acc, as between the q heads of a group
+    const int qper = (total_m + (int)gridDim.z - 1) / (int)gridDim.z;
+    m_start = max(m_start, (int)blockIdx.z * qper);
+    m_end = min(total_m, ((int)blockIdx.z + 1) * qper);
+    if (m_start >= m_end) return;  // nothing causal in this chunk (before any barrier / TMEM use)
+  }
+  const int mq = m_end - m_start;
   const int steps = group * mq;
   const float scale_log2 = scale * kLog2e;
 
@@ -1059,7 +1069,17 @@ int bwd_launch(const void* q, const void* k, const void* v, const void* dout, co
     KPO_CUDA(cudaFuncSetAttribute(attn_bwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     set = true;
   }
-  dim3 grid((unsigned)(dkv_acc ? hq : hkv), (unsigned)((T + C::BN - 1) / C::BN));
+  const int ntiles = (int)((T + C::BN - 1) / C::BN);
+  // split-group mode: query chunks so that ~2 CTAs per SM share the causal work (TP8: 4 q heads x 32
+  // key tiles = 128 CTAs whose largest is ~2.2x the per-SM average without them)
+  int qchunks = 1;
+  if (dkv_acc) {
+    static const int env_q = getenv("KPO_ATTN_BWD_QCHUNKS") ? atoi(getenv("KPO_ATTN_BWD_QCHUNKS")) : 0;
+    qchunks = env_q > 0 ? env_q : (2 * num_sms()) / (hq * ntiles);
+    qchunks = qchunks < 1 ? 1 : (qchunks > 8 ? 8 : qchunks);
+    if (!causal) qchunks = 1;
+  }
+  dim3 grid((unsigned)(dkv_acc ? hq : hkv), (unsigned)ntiles, (unsigned)qchunks);
   KPO_CUDA(::kpo::pdl_launch(attn_bwd_tc_kernel<D>, grid, C::THREADS, C::SMEM, st, mq, mk, mv, mo, mdq, lse, dvec, dq_acc, (__nv_bfloat16*)dk,
                                                           (__nv_bfloat16*)dv, (int)T, hq, hkv, dks, dvs, scale, causal,
                                                           dkv_acc, getenv("KPO_ATTN_BWD_ABLATE") ? atoi(getenv("KPO_ATTN_BWD_ABLATE")) : 0,

@@ -15,7 +15,8 @@ int attn_fwd_tcgen05(const void* q, const void* k, const void* v, void* o, float
 int attn_bwd_tcgen05_main(const void* q, const void* k, const void* v, const void* dout, const float* lse,
                           const float* dvec, float* dq_acc, void* dk, void* dv, int64_t T, int hq, int hkv, int d,
                           int64_t qs, int64_t ks, int64_t vs, int64_t os, int64_t dks, int64_t dvs, float scale,
-                          int causal, float* dkv_acc, cudaStream_t st, const float* rope_table);
+                          int causal, float* dkv_acc, int split_group, int qsplit_tiles, int qchunks,
+                          cudaStream_t st, const float* rope_table);
 }
 
 namespace kpo {
@@ -576,21 +577,47 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* o
     const int64_t ntiles = (T + 127) / 128;
     static const int force_split = getenv("KPO_ATTN_BWD_SPLIT") ? atoi(getenv("KPO_ATTN_BWD_SPLIT")) : -1;
     const bool split = force_split >= 0 ? (force_split != 0 && hq > hkv) : (hq > hkv && hkv * ntiles < num_sms());
-    float* dkv_acc = split ? dvec + (int64_t)hq * T : nullptr;
-    if (split) KPO_CUDA(cudaMemsetAsync(dkv_acc, 0, sizeof(float) * 2 * T * hkv * D, s));
+    // causal load balance: query chunks (grid z).  Split-group mode chunks every key tile (~2 CTAs per
+    // SM).  Grouped mode can halve its first KPO_ATTN_BWD_QSPLIT key tiles (their dK / dV then go
+    // through the fp32 accumulators); measured slower at config 1 for 6..12 tiles (0.298 -> 0.35-0.38
+    // ms: the chunk-1 CTAs dispatch last, as a tail, and add 128 KB of fp32 reductions each), so off.
+    int qchunks = 1, qsplit_tiles = 0;
+    if (causal) {
+      if (split) {
+        const int sms = num_sms() > 0 ? num_sms() : 148;
+        static const int env_q = getenv("KPO_ATTN_BWD_QCHUNKS") ? atoi(getenv("KPO_ATTN_BWD_QCHUNKS")) : 0;
+        qchunks = env_q > 0 ? env_q : (int)((2 * sms) / (hq * ntiles));
+        qchunks = qchunks < 1 ? 1 : (qchunks > 8 ? 8 : qchunks);
+        qsplit_tiles = (int)ntiles;
+      } else {
+        static const int env_t = getenv("KPO_ATTN_BWD_QSPLIT") ? atoi(getenv("KPO_ATTN_BWD_QSPLIT")) : 0;
+        qsplit_tiles = env_t < ntiles ? env_t : (int)ntiles;
+        if (qsplit_tiles > 0) qchunks = 2;
+      }
+    }
+    // key rows whose dK / dV are reduced through the fp32 accumulators (a prefix of the T rows)
+    const int64_t acc_rows = split ? T : (qchunks > 1 ? std::min<int64_t>(T, (int64_t)qsplit_tiles * 128) : 0);
+    float* dkv_acc = acc_rows > 0 ? dvec + (int64_t)hq * T : nullptr;
+    if (dkv_acc) {
+      KPO_CUDA(cudaMemsetAsync(dkv_acc, 0, sizeof(float) * acc_rows * hkv * D, s));
+      KPO_CUDA(cudaMemsetAsync(dkv_acc + T * hkv * D, 0, sizeof(float) * acc_rows * hkv * D, s));
+    }
     int st = attn_bwd_tcgen05_main(q, k, v, dout, lse, dvec, dq_acc, dk, dv, T, hq, hkv, D, qs, ks, vs, os, dks, dvs,
-                                   scale, causal, dkv_acc, s, rope_table);
+                                   scale, causal, dkv_acc, split ? 1 : 0, qsplit_tiles, qchunks, s, rope_table);
     if (st) return st;
-    if (split) {
-      const int64_t n = T * hkv * D / 8;
+    if (dkv_acc) {
+      // convert the accumulated rows; the accumulator layout [T][hkv][D] makes them a prefix, so the
+      // conversion kernels run on acc_rows "tokens" with the full-T offset for the dV half
+      const int64_t n = acc_rows * hkv * D / 8;
       if (rope_cs)
         KPO_CUDA(::kpo::pdl_launch(attn_bwd_post_rope_kernel<D>, (unsigned)((n / 2 + 255) / 256), 256, 0, s, dkv_acc,
-                                   (__nv_bfloat16*)dk, (int)T, hkv, dks, rope_cs));
+                                   (__nv_bfloat16*)dk, (int)acc_rows, hkv, dks, rope_cs));
       else
-        KPO_CUDA(::kpo::pdl_launch(attn_bwd_post_kernel<D>, (unsigned)((n + 255) / 256), 256, 0, s, dkv_acc, (__nv_bfloat16*)dk, (int)T, hkv, dks));
+        KPO_CUDA(::kpo::pdl_launch(attn_bwd_post_kernel<D>, (unsigned)((n + 255) / 256), 256, 0, s, dkv_acc,
+                                   (__nv_bfloat16*)dk, (int)acc_rows, hkv, dks));
       KPO_LAUNCH_CHECK();
-      KPO_CUDA(::kpo::pdl_launch(attn_bwd_post_kernel<D>, (unsigned)((n + 255) / 256), 256, 0, s, dkv_acc + T * hkv * D, (__nv_bfloat16*)dv,
-                                                                           (int)T, hkv, dvs));
+      KPO_CUDA(::kpo::pdl_launch(attn_bwd_post_kernel<D>, (unsigned)((n + 255) / 256), 256, 0, s,
+                                 dkv_acc + T * hkv * D, (__nv_bfloat16*)dv, (int)acc_rows, hkv, dvs));
       KPO_LAUNCH_CHECK();
     }
   } else {

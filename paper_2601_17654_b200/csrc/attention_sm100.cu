@@ -670,6 +670,7 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
                        const float* __restrict__ lse, const float* __restrict__ dvec, float* __restrict__ dq_acc,
                        __nv_bfloat16* __restrict__ dk, __nv_bfloat16* __restrict__ dv, int T, int hq, int hkv,
                        int64_t dks, int64_t dvs, float scale, int causal, float* __restrict__ dkv_acc,
+                       int split_group, int qsplit_tiles,
                        int ablate, const float2* __restrict__ rope_cs) {
   // rope_cs != nullptr: dK leaves inverse-rotated (the gradient w.r.t. the un-rotated k), the fused
   // backward of the QKV GEMM's rotary epilogue; dQ is rotated by the dq conversion kernel
@@ -699,22 +700,28 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nblk = blockIdx.y;  // early key tiles carry the most causal work: dispatched first
-  const bool split = dkv_acc != nullptr;
+  const bool split = split_group != 0;
   const int group = split ? 1 : hq / hkv;
   const int h_first = split ? (int)blockIdx.x : (int)blockIdx.x * (hq / hkv);
   const int kvh = split ? (int)blockIdx.x / (hq / hkv) : (int)blockIdx.x;
   const int n0 = nblk * BN;
   const int total_m = (T + BM - 1) / BM;
   int m_start = causal ? n0 / BM : 0, m_end = total_m;
-  if (split && gridDim.z > 1) {
-    // split-group mode with query chunks (blockIdx.z): this CTA takes the query tiles of chunk z, so
-    // the long causal key tiles are spread over several SMs; dK / dV partials meet in the fp32
-    // accumulators, dQ in dq_acc, as between the q heads of a group
-    const int qper = (total_m + (int)gridDim.z - 1) / (int)gridDim.z;
-    m_start = max(m_start, (int)blockIdx.z * qper);
-    m_end = min(total_m, ((int)blockIdx.z + 1) * qper);
-    if (m_start >= m_end) return;  // nothing causal in this chunk (before any barrier / TMEM use)
+  // query chunks (blockIdx.z) for the first qsplit_tiles key tiles (all of them in split-group mode):
+  // this CTA takes the query tiles of chunk z, so the long causal key tiles are spread over several
+  // SMs; dK / dV partials of a chunked tile meet in the fp32 accumulators, dQ in dq_acc as always
+  const bool chunked = gridDim.z > 1 && nblk < qsplit_tiles;
+  if (gridDim.z > 1) {
+    if (chunked) {
+      const int qper = (total_m + (int)gridDim.z - 1) / (int)gridDim.z;
+      m_start = max(m_start, (int)blockIdx.z * qper);
+      m_end = min(total_m, ((int)blockIdx.z + 1) * qper);
+      if (m_start >= m_end) return;  // nothing causal in this chunk (before any barrier / TMEM use)
+    } else if (blockIdx.z != 0) {
+      return;  // an unchunked key tile: chunk 0 owns all of its queries
+    }
   }
+  const bool atomic_dkv = split || chunked;
   const int mq = m_end - m_start;
   const int steps = group * mq;
   const float scale_log2 = scale * kLog2e;
@@ -941,7 +948,7 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
       const uint32_t col = which ? C::COL_DV : C::COL_DK;
       const float mul = which ? 1.f : scale;
       __nv_bfloat16* row = which ? dv + (int64_t)key * dvs + (int64_t)kvh * D : dk + (int64_t)key * dks + (int64_t)kvh * D;
-      if (which == 0 && rope_cs != nullptr && !split) {
+      if (which == 0 && rope_cs != nullptr && !atomic_dkv) {
         // inverse rotary: pairs (i, i + D/2) of the key's row, (cos, sin) of the key position
         const float2* cs = rope_cs + (int64_t)(key < T ? key : 0) * (D / 2);
 #pragma unroll 1
@@ -972,7 +979,7 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
         uint32_t v[32];
         tmem_ld32_nowait(lane_addr + col + c * 32, v);
         tmem_wait_ld();
-        if (ok && split) {
+        if (ok && atomic_dkv) {
           float* acc = dkv_acc + (which ? (int64_t)T * hkv * D : 0) + ((int64_t)key * hkv + kvh) * D + c * 32;
 #pragma unroll
           for (int q4 = 0; q4 < 8; ++q4)
@@ -992,7 +999,7 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
         }
       }
       }
-      if (!ok && !split && steps == 0 && key < T) {  // no causal work: gradients are zero
+      if (!ok && !atomic_dkv && steps == 0 && key < T) {  // no causal work: gradients are zero
         for (int c = 0; c < D; c += 8) *reinterpret_cast<uint4*>(row + c) = make_uint4(0, 0, 0, 0);
       }
     }
@@ -1053,7 +1060,8 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
 template <int D>
 int bwd_launch(const void* q, const void* k, const void* v, const void* dout, const float* lse, const float* dvec,
                float* dq_acc, void* dk, void* dv, int64_t T, int hq, int hkv, int64_t qs, int64_t ks, int64_t vs,
-               int64_t os, int64_t dks, int64_t dvs, float scale, int causal, float* dkv_acc, cudaStream_t st,
+               int64_t os, int64_t dks, int64_t dvs, float scale, int causal, float* dkv_acc, int split_group,
+               int qsplit_tiles, int qchunks, cudaStream_t st,
                const float* rope_table) {
   using C = Bwd<D>;
   CUtensorMap mq, mk, mv, mo, mdq;
@@ -1070,19 +1078,11 @@ int bwd_launch(const void* q, const void* k, const void* v, const void* dout, co
     set = true;
   }
   const int ntiles = (int)((T + C::BN - 1) / C::BN);
-  // split-group mode: query chunks so that ~2 CTAs per SM share the causal work (TP8: 4 q heads x 32
-  // key tiles = 128 CTAs whose largest is ~2.2x the per-SM average without them)
-  int qchunks = 1;
-  if (dkv_acc) {
-    static const int env_q = getenv("KPO_ATTN_BWD_QCHUNKS") ? atoi(getenv("KPO_ATTN_BWD_QCHUNKS")) : 0;
-    qchunks = env_q > 0 ? env_q : (2 * num_sms()) / (hq * ntiles);
-    qchunks = qchunks < 1 ? 1 : (qchunks > 8 ? 8 : qchunks);
-    if (!causal) qchunks = 1;
-  }
-  dim3 grid((unsigned)(dkv_acc ? hq : hkv), (unsigned)ntiles, (unsigned)qchunks);
+  dim3 grid((unsigned)(split_group ? hq : hkv), (unsigned)ntiles, (unsigned)(qchunks > 1 ? qchunks : 1));
   KPO_CUDA(::kpo::pdl_launch(attn_bwd_tc_kernel<D>, grid, C::THREADS, C::SMEM, st, mq, mk, mv, mo, mdq, lse, dvec, dq_acc, (__nv_bfloat16*)dk,
                                                           (__nv_bfloat16*)dv, (int)T, hq, hkv, dks, dvs, scale, causal,
-                                                          dkv_acc, getenv("KPO_ATTN_BWD_ABLATE") ? atoi(getenv("KPO_ATTN_BWD_ABLATE")) : 0,
+                                                          dkv_acc, split_group, qsplit_tiles,
+                                                          getenv("KPO_ATTN_BWD_ABLATE") ? atoi(getenv("KPO_ATTN_BWD_ABLATE")) : 0,
                                                           reinterpret_cast<const float2*>(rope_table)));
   KPO_LAUNCH_CHECK();
   return KPO_OK;
@@ -1099,13 +1099,14 @@ int attn_fwd_tcgen05(const void* q, const void* k, const void* v, void* o, float
 int attn_bwd_tcgen05_main(const void* q, const void* k, const void* v, const void* dout, const float* lse,
                           const float* dvec, float* dq_acc, void* dk, void* dv, int64_t T, int hq, int hkv, int d,
                           int64_t qs, int64_t ks, int64_t vs, int64_t os, int64_t dks, int64_t dvs, float scale,
-                          int causal, float* dkv_acc, cudaStream_t st, const float* rope_table) {
+                          int causal, float* dkv_acc, int split_group, int qsplit_tiles, int qchunks,
+                          cudaStream_t st, const float* rope_table) {
   if (d != 128) {
     set_error("attn_bwd tcgen05 path needs head_dim 128");
     return KPO_ERR_UNSUPPORTED;
   }
   return attn_tc::bwd_launch<128>(q, k, v, dout, lse, dvec, dq_acc, dk, dv, T, hq, hkv, qs, ks, vs, os, dks, dvs,
-                                  scale, causal, dkv_acc, st, rope_table);
+                                  scale, causal, dkv_acc, split_group, qsplit_tiles, qchunks, st, rope_table);
 }
 
 }  // namespace kpo

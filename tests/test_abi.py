@@ -55,3 +55,17 @@ def test_tcgen05_and_tma_in_sass():
     assert "UTCHMMA" in out or "UTCMMA" in out
     assert "UTMALDG" in out
     assert "LDTM" in out
+
+
+def test_fused_swiglu_entry_points_validate_without_gpu(lib):
+    """kpo_gemm_swiglu / kpo_gemm_swiglu_bwd / the blocked SwiGLU kernels reject bad shapes before any CUDA
+    call (the error behaviour the layer relies on when it decides whether to fuse)."""
+    fake = ctypes.c_void_p(1 << 20)  # non-null, 16B-aligned; never dereferenced on the error paths
+    with pytest.raises(_lib.KpoError, match="multiple of 256"):  # N = 2*ffn must hold 128-row gate/up blocks
+        _lib.call("kpo_gemm_swiglu", fake, fake, fake, fake, 512, 384, 256, 256, 256, 384, 192, 0, fake, None)
+    with pytest.raises(_lib.KpoError, match="M must be >= 256"):
+        _lib.call("kpo_gemm_swiglu", fake, fake, fake, fake, 128, 512, 256, 256, 256, 512, 256, 0, fake, None)
+    with pytest.raises(_lib.KpoError, match="multiple of 256"):  # ffn itself: two blocks per tile
+        _lib.call("kpo_gemm_swiglu_bwd", fake, fake, fake, fake, 512, 384, 256, 256, 384, 768, 768, 0, fake, None)
+    with pytest.raises(_lib.KpoError, match="block"):
+        _lib.call("kpo_swiglu_bwd_blocked", fake, fake, fake, 16, 1024, 100, None)

@@ -96,3 +96,18 @@ def test_bench_reference_arm_contract():
         assert key in line, key
     assert line["impl"] == "reference" and line["e2e"]["h2d_bytes_per_step"] == 0
     assert line["cpu_baseline"]["kind"] == "port" and line["value"] > 0
+
+
+def test_gate_up_block_layout_roundtrip_and_index_map():
+    """ops.interleave_gate_up puts gate block b at rows [256b, 256b+128) and its up block right after —
+    the column map gate_col(j) = (j // 128) * 256 + j % 128 (+128 for up) of elementwise.cu / the GEMM
+    epilogues; deinterleave inverts it exactly."""
+    import torch
+    from paper_2601_17654_b200 import ops
+    f, h = 512, 3
+    w = torch.arange(2 * f * h, dtype=torch.float32).view(2 * f, h)
+    wb = ops.interleave_gate_up(w)
+    assert torch.equal(ops.deinterleave_gate_up(wb), w)
+    for j in (0, 5, 127, 128, 300, f - 1):
+        g = (j // 128) * 256 + j % 128
+        assert torch.equal(wb[g], w[j]) and torch.equal(wb[g + 128], w[f + j])

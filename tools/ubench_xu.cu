@@ -14,6 +14,12 @@ __device__ __forceinline__ float ex2_fma(float x) {
   return __int_as_float(__float_as_int(p) + (__float_as_int(j) << 23));
 }
 
+__device__ __forceinline__ uint32_t ex2_h2(uint32_t x) {
+  uint32_t y;
+  asm volatile("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+
 template <int MODE>
 __global__ void k(int iters, float* out) {
   float a[8], acc = 0.f;
@@ -31,6 +37,16 @@ __global__ void k(int iters, float* out) {
         else a[i] = ex2(a[i]) - 4.f;
       }
       if (MODE == 1) a[i] += 1e-7f;
+      if (MODE == 5) u = ex2_h2(u ^ (uint32_t)i) ^ 0x3c003c00u;  // 2 exponentials per instruction
+      if (MODE == 6) {  // the full f16x2 softmax path per pair: pack args, ex2.f16x2, unpack, bf16x2 pack
+        uint32_t h;
+        asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(a[i]), "f"(a[(i + 1) & 7]));
+        h = ex2_h2(h);
+        float lo, hi;
+        asm("{.reg .f16 l, h; mov.b32 {l, h}, %2; cvt.f32.f16 %0, l; cvt.f32.f16 %1, h;}" : "=f"(lo), "=f"(hi) : "r"(h));
+        u ^= pack_bf16x2(lo, hi);
+        a[i] = lo + hi - 4.f;
+      }
     }
   }
   long long t1 = clock64();
@@ -42,8 +58,9 @@ __global__ void k(int iters, float* out) {
 int main() {
   float* d;
   cudaMalloc(&d, 4096 * 4);
-  const char* names[] = {"ex2 (MUFU)", "cvt.rn.bf16x2 pack", "ex2 + pack", "ex2 on FMA pipe", "half MUFU half FMA"};
-  for (int m = 0; m < 5; ++m) {
+  const char* names[] = {"ex2 (MUFU)", "cvt.rn.bf16x2 pack", "ex2 + pack", "ex2 on FMA pipe", "half MUFU half FMA",
+                         "ex2.f16x2 (per instr, 2 exps)", "f16x2 softmax pair path (per pair)"};
+  for (int m = 0; m < 7; ++m) {
     const int iters = 2048, threads = 512;
     auto run = [&]() {
       if (m == 0) k<0><<<148, threads>>>(iters, d);
@@ -51,6 +68,8 @@ int main() {
       if (m == 2) k<2><<<148, threads>>>(iters, d);
       if (m == 3) k<3><<<148, threads>>>(iters, d);
       if (m == 4) k<4><<<148, threads>>>(iters, d);
+      if (m == 5) k<5><<<148, threads>>>(iters, d);
+      if (m == 6) k<6><<<148, threads>>>(iters, d);
     };
     run();
     cudaDeviceSynchronize();

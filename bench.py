@@ -93,6 +93,67 @@ def cpu_sample(wl, tokens: int, threads: int) -> dict:
     return {"sample_s": dt, "scale": scale, "value": dt * scale}
 
 
+def reference_cpu_path(wl, with_mbo: bool = True) -> dict | None:
+    """The reference's own CPU cost for the path this engine replaces, from the
+    unmodified reference package in baseline/_ref, single-threaded as the reference runs it:
+      (i)  simgpu.simulate_schedule and simgpu.measure over the full schedule space of every partition
+           of this workload (projected to reference KernelSpecs, reference GpuModel defaults), per call;
+      (ii) mbo.run_mbo replaying a profile table for one partition, per partition (sklearn surrogate)."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(ref) and ref not in sys.path:
+        sys.path.append(ref)
+    try:
+        import schedfront
+        from schedfront import domain, mbo, simgpu, workloads
+    except ImportError:
+        return None
+    from paper_2601_17654_b200 import specs
+
+    def to_ref(p):
+        return domain.PartitionSpec(tuple(domain.KernelSpec(k.name, k.flops, k.bytes, k.comm_bytes)
+                                          for k in p.comp_kernels),
+                                    domain.KernelSpec(p.comm_kernel.name, comm_bytes=p.comm_kernel.comm_bytes),
+                                    p.comm_group_size, p.name)
+
+    gpu, thermal = workloads.default_gpu(), workloads.default_thermal()
+    proto = simgpu.ProfilingProtocol(2.0, 5.0, 5.0, 0.02, 6.0, 1234)
+    fg, sg = domain.FrequencyGrid.default(), domain.SmGrid.default_for_group(8)
+    parts = [to_ref(p) for p in specs.partition_specs(wl)]
+    n = 0
+    t_sim = t_meas = 0.0
+    tables = {}
+    for part in parts:
+        space = mbo.enumerate_space(part, gpu, fg, sg)
+        state = simgpu.ThermalState.new(thermal, proto)
+        t0 = time.perf_counter()
+        for c in space:
+            simgpu.simulate_schedule(part, c, gpu)
+        t1 = time.perf_counter()
+        table = {c: simgpu.measure(part, c, gpu, thermal, proto, state) for c in space}
+        t2 = time.perf_counter()
+        t_sim += t1 - t0
+        t_meas += t2 - t1
+        n += len(space)
+        tables[part.name] = table
+    out = {"simulate_schedule_us": round(t_sim / n * 1e6, 2), "measure_us": round(t_meas / n * 1e6, 2),
+           "candidates": n, "partitions": len(parts), "cores": 1,
+           "source": f"baseline/_ref schedfront {getattr(schedfront, '__version__', '')} (unmodified)".strip()}
+    if with_mbo:
+        part = parts[0]
+        table = tables[part.name]
+        orig = mbo.measure
+        mbo.measure = lambda p, c, *a: table[c]
+        try:
+            t0 = time.perf_counter()
+            r = mbo.run_mbo(part, gpu, thermal, proto, mbo.MboHyperparams.for_partition(part, 0), fg, sg)
+            out["run_mbo_replay_s"] = round(time.perf_counter() - t0, 3)
+            out["run_mbo_partition"] = part.name
+            out["run_mbo_evals"] = len(r.records)
+        finally:
+            mbo.measure = orig
+    return out
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -433,6 +494,10 @@ def run_kpo(args):
         cpu = {"value": r["value"], "unit": "s/iter", "cores": threads, "kind": "port",
                "sample": f"oracle/layer_ref.py fp32 fwd+bwd of 1 nanobatch x {args.cpu_tokens} tokens "
                          f"({r['sample_s']:.2f} s), scaled x{r['scale']:.1f} by FLOPs to the full iteration"}
+        try:
+            cpu["reference_path"] = reference_cpu_path(wl)
+        except Exception as ex:  # reported, never fatal: the reference package is an optional guest here
+            cpu["reference_path"] = f"failed: {type(ex).__name__}: {ex}"
 
     # iteration-level roofline: T_lb = max(F_tc / P_tc, B_hbm / BW_hbm, B_link / BW_link)
     specs_all = [u.spec for name in layer.order for u in layer.programs[name].units]

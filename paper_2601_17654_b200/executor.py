@@ -41,6 +41,9 @@ class ScheduleExecutor:
         self.launch_gate = launch_gate
         self.graphs: dict[tuple, torch.cuda.CUDAGraph] = {}
         self.graph_failures: dict[tuple, str] = {}
+        # graph-set tag: callers that swap the tensors a program reads (LayerRunner's host-staging
+        # slots) keep one captured graph per (program, schedule, variant)
+        self.variant = None
 
     # ------------------------------------------------------------------ enqueue
     def issue(self, prog, config, default_ncta: int) -> None:
@@ -76,8 +79,9 @@ class ScheduleExecutor:
     # ------------------------------------------------------------------ graphs
     def _key(self, prog, config, default_ncta):
         t = config.timing
-        return (prog.name, "seq", default_ncta) if t.is_sequential else (prog.name, int(config.sm_alloc), t.start,
-                                                                          min(t.span, len(prog.units) - t.start))
+        key = (prog.name, "seq", default_ncta) if t.is_sequential else (prog.name, int(config.sm_alloc), t.start,
+                                                                         min(t.span, len(prog.units) - t.start))
+        return key if self.variant is None else key + (self.variant,)
 
     def graph(self, prog, config, default_ncta: int):
         key = self._key(prog, config, default_ncta)

@@ -238,8 +238,10 @@ class PartitionedLayer:
             else:
                 hp, yp, dxn2p, dxn1p = a["h"], a["y"], a["dxn2"], a["dxn1"]
             a["hp"], a["yp"] = hp, yp
-            res_attn = a["x"] if (not tp or rank0) else None
-            res_mlp = a["h"] if (not tp or rank0) else None
+            # residual inputs are looked up when the unit is issued (LayerRunner swaps a["x"] between
+            # host-staging slots, each with its own captured graphs)
+            res_attn = "x" if (not tp or rank0) else None
+            res_mlp = "h" if (not tp or rank0) else None
             s = {k: self.sched.slot() for k in US if k in specs.GEMM_UNITS}
             acc = b > 0  # weight gradients accumulate over nanobatches (epilogue C input)
             fns = {
@@ -255,7 +257,7 @@ class PartitionedLayer:
                                                                           a["qkv"][:, qd:], a["ao"], a["lse"], T, hq,
                                                                           hkv, d, scale, stream=st),
                 "linear_proj": lambda st, a=a, s=s, hp=hp, r=res_attn: ops.linear(
-                    a["ao"], W["wo"], hp, residual=r, sched=s["linear_proj"], stream=st),
+                    a["ao"], W["wo"], hp, residual=a[r] if r else None, sched=s["linear_proj"], stream=st),
                 "norm2": lambda st, a=a: ops.rmsnorm_fwd(a["h"], W["g2"], a["xn2"], a["rstd2"], eps, stream=st),
                 "linear_up": (lambda st, a=a, s=s: ops.linear_swiglu(a["xn2"], W["wgu"], a["gu"], a["act"],
                                                                      sched=s["linear_up"], stream=st))
@@ -264,7 +266,7 @@ class PartitionedLayer:
                 "swiglu": lambda st, a=a, blk=ops.SWIGLU_BLOCK if self.swiglu_fused else 0: ops.swiglu_fwd(
                     a["gu"], a["act"], stream=st, block=blk),
                 "linear_down": lambda st, a=a, s=s, yp=yp, r=res_mlp: ops.linear(
-                    a["act"], W["wd"], yp, residual=r, sched=s["linear_down"], stream=st),
+                    a["act"], W["wd"], yp, residual=a[r] if r else None, sched=s["linear_down"], stream=st),
                 # ---------------- backward
                 "norm1_bwd": lambda st, a=a: ops.rmsnorm_bwd(a["dxn1"], a["x"], W["g1"], a["rstd1"], a["dx"],
                                                              a["dwp1"], dres=a["dh"], stream=st),

@@ -66,15 +66,33 @@ class LayerRunner:
         st.synchronize()
 
     # ---------------------------------------------------------------- pipelined host-buffer entry point
+    def _use_slot(self, s) -> None:
+        """Point the layer's input / output activations at host-staging slot s (None: the layer's own
+        tensors); the executor keeps a separate graph set per slot."""
+        for a, own, slot in zip(self.layer.nb, self._own, self._slots[s] if s is not None else self._own):
+            a["x"], a["dy"], a["dx"] = slot
+        self.engine.exec.variant = None if s is None else ("host-slot", s)
+
+    def prepare_host_pipeline(self) -> None:
+        """Allocate the two host-staging slots and capture their graphs (this executes every partition
+        once per slot on the current inputs); step_host_async does it on first use otherwise."""
+        if not hasattr(self, "_pipe_k"):
+            self._pipe_init()
+
     def _pipe_init(self) -> None:
         dev = self.engine.device
         self._h2d = torch.cuda.Stream(dev)
         self._d2h = torch.cuda.Stream(dev)
-        # two device staging slots: slot s holds step k's inputs while step k-1 still computes, and
-        # step k's dx while step k+1 computes
-        self._stage_in = [[(torch.empty_like(a["x"]), torch.empty_like(a["dy"])) for a in self.layer.nb]
-                          for _ in range(2)]
-        self._stage_out = [[torch.empty_like(a["dx"]) for a in self.layer.nb] for _ in range(2)]
+        # two device slots, each with its own x / dy / dx and its own captured graphs: step k reads its
+        # inputs and writes dx in slot k % 2 directly (no staging copies on the compute stream), so the
+        # H2D of step k+1 and the D2H of step k-1 run on copy engines while step k computes
+        self._own = [(a["x"], a["dy"], a["dx"]) for a in self.layer.nb]
+        self._slots = [[(a["x"].clone(), a["dy"].clone(), torch.empty_like(a["dx"])) for a in self.layer.nb]
+                       for _ in range(2)]
+        for s in range(2):
+            self._use_slot(s)
+            self.warm()  # capture this slot's graphs before any pipelined step is queued
+        self._use_slot(None)
         ev = lambda: [torch.cuda.Event(), torch.cuda.Event()]
         self._in_ready, self._in_free, self._out_ready, self._out_free = ev(), ev(), ev(), ev()
         self._pipe_k = 0
@@ -84,40 +102,34 @@ class LayerRunner:
                         dxs_host: list[torch.Tensor]) -> None:
         """Enqueue one iteration from pinned host buffers without waiting for it.
 
-        The H2D of this step's inputs runs on a copy stream. It overlaps the previous step's
-        compute. The D2H of this step's dx overlaps the next step's compute. The compute stream only
-        pays two device-to-device copies into and out of the layer's graph-bound buffers. The host
-        buffers of a step must stay untouched until `drain()` (or two steps later) returns.
+        The H2D of this step's inputs runs on a copy stream into this step's device slot and overlaps
+        the previous step's compute; the D2H of this step's dx overlaps the next step's compute. The
+        host buffers of a step must stay untouched until `drain()` (or two steps later) returns.
         Call `drain()` to wait for every enqueued step."""
         if not hasattr(self, "_pipe_k"):
             self._pipe_init()
         s = self._pipe_k & 1
         comp = self.engine.exec.compute
         used = self._pipe_used[s]
+        slot = self._slots[s]
         with torch.cuda.stream(self._h2d):
             if used:
-                self._h2d.wait_event(self._in_free[s])
-            for (sx, sdy), x, dy in zip(self._stage_in[s], xs_host, dys_host):
+                self._h2d.wait_event(self._in_free[s])  # step k-2 has finished reading this slot
+            for (sx, sdy, _), x, dy in zip(slot, xs_host, dys_host):
                 sx.copy_(x, non_blocking=True)
                 sdy.copy_(dy, non_blocking=True)
             self._in_ready[s].record(self._h2d)
         comp.wait_event(self._in_ready[s])
-        with torch.cuda.stream(comp):
-            for a, (sx, sdy) in zip(self.layer.nb, self._stage_in[s]):
-                a["x"].copy_(sx, non_blocking=True)
-                a["dy"].copy_(sdy, non_blocking=True)
-            self._in_free[s].record(comp)
-        self.step()
         if used:
-            comp.wait_event(self._out_free[s])
-        with torch.cuda.stream(comp):
-            for a, so in zip(self.layer.nb, self._stage_out[s]):
-                so.copy_(a["dx"], non_blocking=True)
-            self._out_ready[s].record(comp)
+            comp.wait_event(self._out_free[s])  # step k-2's dx has left this slot
+        self._use_slot(s)
+        self.step()
+        self._in_free[s].record(comp)
+        self._out_ready[s].record(comp)
         self._d2h.wait_event(self._out_ready[s])
         with torch.cuda.stream(self._d2h):
-            for so, dx in zip(self._stage_out[s], dxs_host):
-                dx.copy_(so, non_blocking=True)
+            for (_, _, sdx), dx in zip(slot, dxs_host):
+                dx.copy_(sdx, non_blocking=True)
             self._out_free[s].record(self._d2h)
         self._pipe_used[s] = True
         self._pipe_k += 1
@@ -126,6 +138,7 @@ class LayerRunner:
         if hasattr(self, "_pipe_k"):
             self._d2h.synchronize()
             self._h2d.synchronize()
+            self._use_slot(None)
         self.engine.exec.compute.synchronize()
 
     # ---------------------------------------------------------------- instrumentation

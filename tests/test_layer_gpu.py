@@ -79,7 +79,7 @@ def test_tp_shards_sum_to_full(cuda):
 
 def test_pipelined_host_steps_match_synchronous(cuda):
     """LayerRunner.step_host_async: per-step dx equals the synchronous step_host result for the
-    same inputs, with a different input per step (staging slots and copy-stream ordering)."""
+    same inputs, with a different input per step (per-slot graphs and copy-stream ordering)."""
     from paper_2601_17654_b200 import b200_model
     from paper_2601_17654_b200.comm import Communicator
     from paper_2601_17654_b200.engine import Engine
@@ -91,6 +91,7 @@ def test_pipelined_host_steps_match_synchronous(cuda):
     eng = Engine.for_layer(L, b200_model())
     run = LayerRunner(L, eng)
     run.warm()
+    run.prepare_host_pipeline()  # slot graphs captured before either sequence starts
     g = torch.Generator().manual_seed(7)
     pin = lambda t: t.pin_memory()
     steps = 5

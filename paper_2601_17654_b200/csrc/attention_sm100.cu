@@ -343,9 +343,10 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* v_full = bar + 5;    // [2]
   uint64_t* v_empty = bar + 7;   // [2]
   uint64_t* s_full = bar + 9;    // [2] per Q tile
-  uint64_t* p_full = bar + 11;   // [2] per Q tile (4 warps)
+  uint64_t* p_full = bar + 11;   // [2] per Q tile (4 warps): P keys 0..63 stored
   uint64_t* pv_done = bar + 13;  // [2] per Q tile
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 15);
+  uint64_t* p_full2 = bar + 15;  // [2] per Q tile (4 warps): P keys 64..127 stored
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 17);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mblk = gridDim.y - 1 - blockIdx.y;  // heavy (late) causal rows first
@@ -371,6 +372,7 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(smem_u32(&v_empty[i]), 1);
       mbar_init(smem_u32(&s_full[i]), 1);
       mbar_init(smem_u32(&p_full[i]), 4);
+      mbar_init(smem_u32(&p_full2[i]), 4);
       mbar_init(smem_u32(&pv_done[i]), 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -427,16 +429,19 @@ __global__ void __launch_bounds__(384, 1)
             tc_mma_lo_w(d_s, q_k + kb * (BM * 8) + k * 2, k_k + kb * (BN * 8) + k * 2, ID_S, (kb | k) ? 1u : 0u);
         tc_commit_w(smem_u32(&s_full[g]));
       };
-      auto issue_pv = [&](int g, int j) {  // O_g += P_g(j) V_j
+      auto issue_pv = [&](int g, int j) {  // O_g += P_g(j) V_j, keys 0..63 as soon as their P is stored
         const int s = j & 1;
-        mbar_wait(smem_u32(&p_full[g]), j & 1);
-        tc_fence_after();
         const uint32_t v_mn = desc_lo(sV + s * C::KV_BYTES, BN * 128);
         const uint32_t p_t = tmem + (g ? C::COL_S1 : C::COL_S0);
         const uint32_t o_t = tmem + (g ? C::COL_O1 : C::COL_O0);
 #pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk)
-          tc_mma_ts_lo_w(o_t, p_t + kk * 8, v_mn + kk * 128, ID_O, (j > 0 || kk > 0) ? 1u : 0u);
+        for (int half = 0; half < 2; ++half) {
+          mbar_wait(smem_u32(half ? &p_full2[g] : &p_full[g]), j & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = half * BN / 32; kk < (half + 1) * BN / 32; ++kk)
+            tc_mma_ts_lo_w(o_t, p_t + kk * 8, v_mn + kk * 128, ID_O, (j > 0 || kk > 0) ? 1u : 0u);
+        }
         tc_commit_w(smem_u32(&pv_done[g]));
       };
       // prologue: S0_0, S1_0 (K_0)
@@ -536,6 +541,12 @@ __global__ void __launch_bounds__(384, 1)
           pk[c] = pack_bf16x2(p[0], p[1]);
         }
         tmem_st32(s_addr + hb * 32, pk);
+        if (hb == 0) {  // the P·V MMA over keys 0..63 may start while keys 64..127 are exponentiated
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&p_full[g]));
+        }
       }
       if (pingpong) {  // hand the MUFU to the other group
         if (g == 0) asm volatile("bar.arrive 2, 256;" ::: "memory");
@@ -546,7 +557,7 @@ __global__ void __launch_bounds__(384, 1)
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&p_full[g]));
+      if (lane == 0) mbar_arrive(smem_u32(&p_full2[g]));
     }
     if (ng > 0) {
       // ------------------------------------------------------------ epilogue

@@ -323,6 +323,10 @@ struct Fwd2 {
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
   static constexpr int COL_S0 = 0, COL_S1 = 128, COL_O0 = 256, COL_O1 = 384;
   static constexpr int THREADS = 384;
+  // P parts per tile, each released to the P·V MMA on its own as soon as it is in TMEM (the last one
+  // before the MUFU hand-off to the other group): same-box A/B 853 -> 870 (first half early) -> 887
+  // TF/s (last half before the hand-off); 4 parts measured the same as 2
+  static constexpr int NP = 2;
 };
 
 template <int D>
@@ -343,10 +347,11 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* v_full = bar + 5;    // [2]
   uint64_t* v_empty = bar + 7;   // [2]
   uint64_t* s_full = bar + 9;    // [2] per Q tile
-  uint64_t* p_full = bar + 11;   // [2] per Q tile (4 warps): P keys 0..63 stored
   uint64_t* pv_done = bar + 13;  // [2] per Q tile
-  uint64_t* p_full2 = bar + 15;  // [2] per Q tile (4 warps): P keys 64..127 stored
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 17);
+  // [NP parts][2 Q tiles] (4 warps each): P keys [part * BN / NP, (part + 1) * BN / NP) stored in TMEM
+  constexpr int NP = C::NP;
+  uint64_t* p_full = bar + 15;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 15 + 2 * NP);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mblk = gridDim.y - 1 - blockIdx.y;  // heavy (late) causal rows first
@@ -371,8 +376,7 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(smem_u32(&v_full[i]), 1);
       mbar_init(smem_u32(&v_empty[i]), 1);
       mbar_init(smem_u32(&s_full[i]), 1);
-      mbar_init(smem_u32(&p_full[i]), 4);
-      mbar_init(smem_u32(&p_full2[i]), 4);
+      for (int pp = 0; pp < NP; ++pp) mbar_init(smem_u32(&p_full[pp * 2 + i]), 4);
       mbar_init(smem_u32(&pv_done[i]), 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -435,11 +439,11 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t p_t = tmem + (g ? C::COL_S1 : C::COL_S0);
         const uint32_t o_t = tmem + (g ? C::COL_O1 : C::COL_O0);
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          mbar_wait(smem_u32(half ? &p_full2[g] : &p_full[g]), j & 1);
+        for (int pp = 0; pp < NP; ++pp) {
+          mbar_wait(smem_u32(&p_full[pp * 2 + g]), j & 1);
           tc_fence_after();
 #pragma unroll
-          for (int kk = half * BN / 32; kk < (half + 1) * BN / 32; ++kk)
+          for (int kk = pp * BN / 16 / NP; kk < (pp + 1) * BN / 16 / NP; ++kk)
             tc_mma_ts_lo_w(o_t, p_t + kk * 8, v_mn + kk * 128, ID_O, (j > 0 || kk > 0) ? 1u : 0u);
         }
         tc_commit_w(smem_u32(&pv_done[g]));
@@ -526,27 +530,28 @@ __global__ void __launch_bounds__(384, 1)
         if (g == 1 && j < n_g[0]) named_bar(2, 256);
       }
       float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      constexpr int PC = BN / 2 / NP;  // packed bf16-pair columns per P part
 #pragma unroll
-      for (int hb = 0; hb < 2; ++hb) {  // 64 keys -> 32 columns of bf16 pairs over S_g
-        uint32_t pk[32];
+      for (int pp = 0; pp < NP; ++pp) {  // BN / NP keys -> PC columns of bf16 pairs over S_g
+        uint32_t pk[PC];
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
+        for (int c = 0; c < PC; ++c) {
           float p[2];
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const int i = hb * 64 + c * 2 + e;
+            const int i = pp * 2 * PC + c * 2 + e;
             p[e] = ex2(fmaf(sv[i], scale_log2, neg_m));
             ps[i & 7] += p[e];
           }
           pk[c] = pack_bf16x2(p[0], p[1]);
         }
-        tmem_st32(s_addr + hb * 32, pk);
-        if (hb == 0) {  // the P·V MMA over keys 0..63 may start while keys 64..127 are exponentiated
-          tmem_wait_st();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(smem_u32(&p_full[g]));
-        }
+        if constexpr (PC == 32) tmem_st32(s_addr + pp * PC, pk);
+        else tmem_st16(s_addr + pp * PC, pk);
+        // the P·V MMAs over this part's keys may start while the next part is exponentiated
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&p_full[pp * 2 + g]));
       }
       if (pingpong) {  // hand the MUFU to the other group
         if (g == 0) asm volatile("bar.arrive 2, 256;" ::: "memory");
@@ -554,10 +559,6 @@ __global__ void __launch_bounds__(384, 1)
       }
       const float lsum = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
       l_run = l_run * corr + lsum;
-      tmem_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&p_full2[g]));
     }
     if (ng > 0) {
       // ------------------------------------------------------------ epilogue

@@ -111,3 +111,16 @@ def test_gate_up_block_layout_roundtrip_and_index_map():
     for j in (0, 5, 127, 128, 300, f - 1):
         g = (j // 128) * 256 + j % 128
         assert torch.equal(wb[g], w[j]) and torch.equal(wb[g + 128], w[f + j])
+
+
+def test_bench_reference_cpu_path_reports_per_candidate_costs():
+    """bench.py's cpu_baseline.reference_path times the unmodified reference simulator over every
+    partition's schedule space; skipped where the reference package is absent."""
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2601_17654_b200.model import baseline_workload
+    r = bench.reference_cpu_path(baseline_workload(0), with_mbo=False)
+    if r is None:
+        pytest.skip("reference package not installed (baseline/_ref)")
+    assert r["partitions"] == 8 and r["candidates"] > 1000
+    assert r["simulate_schedule_us"] > 0 and r["measure_us"] > 0 and r["cores"] == 1

@@ -460,10 +460,22 @@ __global__ void __launch_bounds__(384, 1)
         mbar_wait(smem_u32(&v_full[s]), (j >> 1) & 1);
         if (more) mbar_wait(smem_u32(&k_full[s ^ 1]), ((j + 1) >> 1) & 1);
         tc_fence_after();
-        if (j < n_g[0]) issue_pv(0, j);
-        if (j + 1 < n_g[0]) issue_s(0, j + 1);
-        if (j < n_g[1]) issue_pv(1, j);
-        if (j + 1 < n_g[1]) issue_s(1, j + 1);
+        // serve the two groups in the order their P becomes ready (each group's own order PV_g(j) ->
+        // S_g(j+1) is what the softmax relies on; the order between the groups is free)
+        bool need0 = j < n_g[0], need1 = j < n_g[1];
+        while (need0 || need1) {
+          int g = need0 ? 0 : 1;
+          if (need0 && need1) {
+            while (true) {
+              if (mbar_test(smem_u32(&p_full[0]), j & 1)) { g = 0; break; }
+              if (mbar_test(smem_u32(&p_full[1]), j & 1)) { g = 1; break; }
+            }
+          }
+          issue_pv(g, j);
+          if (j + 1 < n_g[g]) issue_s(g, j + 1);
+          if (g == 0) need0 = false;
+          else need1 = false;
+        }
         tc_commit_w(smem_u32(&v_empty[s]));
         if (more) tc_commit_w(smem_u32(&k_empty[s ^ 1]));
       }
@@ -617,7 +629,7 @@ int fwd_launch(const void* q, const void* k, const void* v, void* o, float* lse,
     KPO_CUDA(cudaFuncSetAttribute(kern2, cudaFuncAttributeMaxDynamicSharedMemorySize, C2::SMEM));
     KPO_CUDA(::kpo::pdl_launch(kern2, grid2, C2::THREADS, C2::SMEM, st, mq, mk, mv, (__nv_bfloat16*)o, lse, (int)T,
                                hq, hkv, os, scale * kLog2e, causal,
-                               getenv("KPO_ATTN_PINGPONG") ? atoi(getenv("KPO_ATTN_PINGPONG")) : 1));
+                               getenv("KPO_ATTN_PINGPONG") ? atoi(getenv("KPO_ATTN_PINGPONG")) : 0));
     KPO_LAUNCH_CHECK();
     return KPO_OK;
   }

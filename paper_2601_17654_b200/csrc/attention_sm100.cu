@@ -308,7 +308,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 //   warp 8     TMA producer (Q0, Q1 once; K / V 2-stage rings)                    (setmaxnreg 40)
 //   warp 9     TMEM allocator + MMA issuer; warps 10-11 idle
 //   TMEM: S0 0..127, S1 128..255 (P_g written over the first 64 columns of S_g), O0 256..383, O1 384..511
-//   MMA order: S0_0, S1_0, then per KV tile j: PV0_j, S0_{j+1}, PV1_j, S1_{j+1}
+//   MMA order: S0_0, S1_0, then per KV tile j and per group g, in the order the groups' P become ready:
+//   PV_g(j), S_g(j+1)
 // A commit after S_g(j) completes only when every earlier MMA of the issuer has (in particular
 // PV_g(j-1)), so a softmax group can rescale O_g as soon as it has seen S_g(j).
 template <int D>

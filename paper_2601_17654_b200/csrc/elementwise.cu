@@ -4,8 +4,11 @@
 // These stand in for the reference's memory-bound KernelSpecs ("norm", "rope", "fused_norm";
 // reference pkg/src/schedfront/workloads.py:44-46,60,87), which compose.py:48-76
 // (`group_memory_bound`) treats as single logical launch units.  Roofline: HBM bytes
-// (read + write) / measured copy bandwidth; all loads/stores are 16-byte vectors, one warp per
-// row for the row-reductions so a row is read once from HBM and the second pass hits L1.
+// (read + write) / measured copy bandwidth; all loads/stores are 16-byte vectors and every row is
+// read from HBM once (held in registers across its reduction: a 128-thread CTA per row for the
+// RMSNorm forward, a row block per CTA with next-row prefetch for the fused backward, one warp per
+// row for the generic widths).  The SwiGLU kernels also serve the blocked gate|up layout of the fused
+// GEMM epilogues (gemm_sm100.cu) and share their sigmoid (kpo_sigmoid).
 #include "common.cuh"
 
 namespace kpo {

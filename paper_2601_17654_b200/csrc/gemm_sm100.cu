@@ -7,7 +7,8 @@
 // Design (B200-first):
 //   * one CTA per SM (smem > half the SM), 6 warps: warp0 = tile scheduler + TMA producer,
 //     warp1 = TMEM allocator + single-thread tcgen05.mma issuer, warps 2-5 = epilogue
-//     (tcgen05.ld TMEM -> registers -> bf16 -> global, optional fused residual add);
+//     (tcgen05.ld TMEM -> registers -> bf16 -> TMA stores; optional fused residual add, RoPE for
+//     the QKV projection, SwiGLU for the gate|up projection, SwiGLU backward for the down dgrad);
 //   * operands staged by TMA (cp.async.bulk.tensor, 128B swizzle) into a STAGES-deep
 //     smem ring guarded by mbarriers; accumulators double-buffered in TMEM so the epilogue of
 //     tile i overlaps the main loop of tile i+1;

@@ -39,7 +39,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="kpo", choices=["kpo", "reference"])
     ap.add_argument("--config", type=int, default=1, help="BASELINE.json configs index (1..3)")
-    ap.add_argument("--tokens", type=int, default=4096)
+    ap.add_argument("--tokens", type=int, default=None, help="tokens per nanobatch (default: the config's own, 4096 for configs 1-3)")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-tokens", type=int, default=1024)
@@ -263,6 +263,8 @@ def run_kpo(args):
     red_dev = torch.device("cpu") if same_dev else dev
     group_world = world if world > 1 else 8
     wl = baseline_workload(args.config, world=group_world, tokens=args.tokens)
+    if world == 1 and wl.world != group_world:  # config 0 (the reference's CPU case) is a 1-rank layer
+        group_world = wl.world
     peaks = load_measured_peaks()
     hbm = peaks.get("hbm_gbs", 6650.0)
     tf_burst = peaks.get("bf16_tflops", 1590.0)

@@ -335,12 +335,16 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// rows per CTA (even: the two row groups stay in step) and CTA count of the fused backward: one CTA
-// per SM, one wave
+// rows per CTA (even: the two row groups stay in step) and CTA count of the fused backward
 static inline void fused_norm_bwd_grid(int64_t rows, int& rows_per_cta, int& grid) {
   int sms = num_sms();
   if (sms <= 0) sms = 148;  // no device visible (host-only queries): B200's SM count
-  int64_t rpc = (rows + sms - 1) / sms;
+  // two CTAs per SM's worth of row blocks (run as two waves): when an SM-budgeted collective holds
+  // some SMs, the blocks it displaces are half as long (in-step 42.5 -> 36.4 us with the comm
+  // overlapped, unchanged alone; four waves cost 8 us alone)
+  static const int per_sm = getenv("KPO_NORM_BWD_WAVES") ? atoi(getenv("KPO_NORM_BWD_WAVES")) : 2;
+  const int64_t ctas = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+  int64_t rpc = (rows + ctas - 1) / ctas;
   rpc += rpc & 1;
   if (rpc < 2) rpc = 2;
   rows_per_cta = (int)rpc;

@@ -42,8 +42,9 @@ def parse():
     ap.add_argument("--tokens", type=int, default=None, help="tokens per nanobatch (default: the config's own, 4096 for configs 1-3)")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-tokens", type=int, default=1024)
-    ap.add_argument("--sweep-window", type=float, default=0.8)
+    ap.add_argument("--cpu-iters", type=int, default=3, help="full CPU oracle iterations for cpu_baseline")
+    ap.add_argument("--sweep-window", type=float, default=2.0, help="seconds per executed schedule-set trial")
+    ap.add_argument("--sweep-trials", type=int, default=2)
     return ap.parse_args()
 
 
@@ -64,15 +65,25 @@ def iteration_flops(wl) -> float:
 
 
 # ---------------------------------------------------------------------------- CPU baseline
-def cpu_sample(wl, tokens: int, threads: int) -> dict:
-    """Oracle fp32 forward+backward of ONE nanobatch at `tokens` tokens, scaled by FLOPs to the
-    full iteration (nanobatches x wl.tokens)."""
+def host_facts() -> dict:
+    """CPU facts BASELINE.md §3 asks for: lscpu model, os.cpu_count(), torch threads."""
+    import subprocess
+
     import torch
 
-    from oracle import layer_ref
-    from paper_2601_17654_b200.model import Workload
+    model = ""
+    try:
+        txt = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        model = next((ln.split(":", 1)[1].strip() for ln in txt.splitlines() if ln.startswith("Model name")), "")
+    except Exception:
+        pass
+    return {"cpu_model": model, "cpu_count": os.cpu_count(), "torch_threads": torch.get_num_threads()}
 
-    torch.set_num_threads(threads)
+
+def cpu_layer_setup(wl, nanobatches: int):
+    """The oracle's inputs for `nanobatches` full nanobatches of the workload (fp32, seeded)."""
+    import torch
+
     m = wl.model
     g = torch.Generator().manual_seed(0)
     W = {
@@ -82,15 +93,36 @@ def cpu_sample(wl, tokens: int, threads: int) -> dict:
         "wd": torch.randn(m.hidden, m.ffn, generator=g) * 0.02,
         "g1": torch.ones(m.hidden), "g2": torch.ones(m.hidden),
     }
-    x = torch.randn(tokens, m.hidden, generator=g)
-    dy = torch.randn(tokens, m.hidden, generator=g)
+    xs = [torch.randn(wl.tokens, m.hidden, generator=g) for _ in range(nanobatches)]
+    dys = [torch.randn(wl.tokens, m.hidden, generator=g) for _ in range(nanobatches)]
+    return W, xs, dys
+
+
+def cpu_iteration(wl, threads: int, setup=None) -> float:
+    """Seconds for the oracle's fp32 forward + backward of ONE FULL layer iteration of the workload
+    (wl.nanobatches x wl.tokens tokens, the same shapes the GPU step runs; no scaling), all host
+    threads."""
+    import torch
+
+    from oracle import layer_ref
+
+    torch.set_num_threads(threads)
+    W, xs, dys = setup or cpu_layer_setup(wl, wl.nanobatches)
     t0 = time.perf_counter()
-    layer_ref.layer_fwd_bwd([x], [dy], W, m)
-    dt = time.perf_counter() - t0
-    sample = Workload(m, "fsdp", 1, tokens, nanobatches=1)
-    full = Workload(m, "fsdp", 1, wl.tokens, nanobatches=wl.nanobatches)
-    scale = iteration_flops(full) / iteration_flops(sample)
-    return {"sample_s": dt, "scale": scale, "value": dt * scale}
+    layer_ref.layer_fwd_bwd(xs, dys, W, wl.model)
+    return time.perf_counter() - t0
+
+
+def workload_config(wl, world: int, group_world: int) -> dict:
+    """The `config` object both arms print (identical keys and values for the same workload)."""
+    return {
+        "workload": f"{wl.model.name} layer iteration: fwd+bwd, {wl.nanobatches} nanobatches x {wl.tokens} "
+                    f"tokens per rank, 8 partitions",
+        "model": wl.model.name, "global_batch": wl.tokens * wl.nanobatches * world, "seq_len": wl.tokens,
+        "parallelism": (f"{wl.parallel}{group_world}-loopback" if world == 1 else f"{wl.parallel}{world}"),
+        "schedule": "nanobatching default: f_max, default comm CTAs, overlap(0,n)",
+        "l2": "no flush: per-step working set (layer weights + activations) > 126 MB L2",
+    }
 
 
 def reference_cpu_path(wl, with_mbo: bool = True) -> dict | None:
@@ -155,30 +187,36 @@ def reference_cpu_path(wl, with_mbo: bool = True) -> dict | None:
 
 
 def run_reference(args):
+    """The reference-side CPU path of this workload: the oracle's fp32 execution of the same layer
+    iteration (every step = one full iteration, 2 nanobatches x 4096 tokens, nothing scaled), on all
+    host threads of rank 0."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    import torch
-
     from paper_2601_17654_b200.model import baseline_workload
 
     wl = baseline_workload(args.config, world=8, tokens=args.tokens)
+    group_world = wl.world if world == 1 else world
     threads = os.cpu_count() or 1
+    setup = cpu_layer_setup(wl, wl.nanobatches)
     vals = []
+    t_start = time.perf_counter()
     for i in range(args.warmup + args.steps):
-        r = cpu_sample(wl, args.cpu_tokens, threads)
+        v = cpu_iteration(wl, threads, setup)
         if i >= args.warmup:
-            vals.append(r["value"])
+            vals.append(v)
+    total = time.perf_counter() - t_start
     v = statistics.mean(vals)
-    sample = (f"oracle fp32 fwd+bwd of 1 nanobatch x {args.cpu_tokens} tokens per step, scaled by FLOPs to "
-              f"{wl.nanobatches} x {wl.tokens} tokens")
+    facts = host_facts()
+    sample = (f"oracle/layer_ref.py fp32 fwd+bwd of one full layer iteration per step ({wl.nanobatches} x "
+              f"{wl.tokens} tokens, unscaled), {threads} threads on {facts['cpu_model'] or 'host CPU'}")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "s/iter", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{wl.model.name} layer iteration (fwd+bwd, {wl.nanobatches} nanobatches x "
-                               f"{wl.tokens} tokens), CPU fp32", "model": wl.model.name},
-        "cpu_baseline": {"value": v, "unit": "s/iter", "cores": threads, "kind": "port", "sample": sample},
+        "config": workload_config(wl, world, group_world),
+        "cpu_baseline": {"value": v, "unit": "s/iter", "cores": threads, "kind": "port", "sample": sample,
+                         **facts, "timed_region_s": round(sum(vals), 2), "run_s": round(total, 2)},
         "e2e": {"value": v, "unit": "s/iter", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -240,10 +278,9 @@ def run_kpo(args):
 
     from paper_2601_17654_b200.comm import Communicator
     from paper_2601_17654_b200.device import b200_model, load_measured_peaks
-    from paper_2601_17654_b200.domain import LaunchTiming, ScheduleConfig
-    from paper_2601_17654_b200.device import ProfilingProtocol
+    from paper_2601_17654_b200.domain import LaunchTiming, Measurement, ScheduleConfig
     from paper_2601_17654_b200.engine import Engine
-    from paper_2601_17654_b200.layer import PartitionedLayer
+    from paper_2601_17654_b200.layer import PartitionedLayer, sym_bytes_for
     from paper_2601_17654_b200.model import baseline_workload
     from paper_2601_17654_b200.runner import LayerRunner, sequential_schedule
 
@@ -272,16 +309,13 @@ def run_kpo(args):
     peak_src = "measured" if peaks else "fallback"
     gpu = b200_model(hbm_gbs=hbm, bf16_tflops=tf_burst)
 
-    # symmetric buffer: FSDP shards + two gradient buffers; TP: 4 partials x 2 nb + stage
-    numels = wl.weight_numels()
-    if wl.parallel == "fsdp":
-        sym = sum(int(n * 2 / group_world) + 2 * n * 2 for n in numels.values()) + (64 << 20)
-    else:
-        sym = 9 * wl.tokens * wl.h * 2 + (64 << 20)
+    # symmetric heap: FSDP shards + two layer-parity gradient buffers; TP partial sums + stage
+    sym = sym_bytes_for(wl)
     comm = (Communicator.loopback_group(group_world, sym, device=dev) if world == 1
             else Communicator.from_process_group(sym, device=dev))
     layer = PartitionedLayer(wl, comm)
-    eng = Engine.for_layer(layer, gpu)
+    # the bench runs at the unlocked default clock (f_max); the frequency axis is the profiler's
+    eng = Engine.for_layer(layer, gpu, clock_control=False)
     run = LayerRunner(layer, eng)
     run.warm()
 
@@ -302,6 +336,9 @@ def run_kpo(args):
         t = torch.tensor([v], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t)
+
+    if world > 1:
+        eng.agree_ms = max_over_ranks  # identical repetition counts on every rank (measure paths)
 
     for _ in range(max(3, args.warmup)):
         run.step()
@@ -420,82 +457,99 @@ def run_kpo(args):
                               "busbw_gbps": round(cu.algo_bytes / (cms / 1e3) / 1e9, 1)})
     barrier()
 
-    # ------------------------------------------------ schedule sweep -> iteration frontier
+    # ------------------------------------------------ MBO-selected schedule sets, executed as iterations
+    # The per-partition frontiers come from the reference optimizer run on this hardware
+    # (tools/mbo_hardware.py -> profiles/r2_mbo_config<N>.json + profile tables); here the selected
+    # iteration-level sets run as whole iterations next to the default and sequential schedules,
+    # interleaved trials of >= --sweep-window s each (device time max over ranks, NVML energy summed).
     frontier = None
-    if not args.no_sweep:
-        proto = ProfilingProtocol(warmup_s=0.2, window_s=args.sweep_window, cooldown_s=0.0)
-        f = gpu.f_max_mhz
-        per_part = {}
-        for name in layer.order:
-            prog = layer.programs[name]
-            n = len(prog.units)
-            cands = [ScheduleConfig(f, 16, LaunchTiming.sequential())]
-            for sm in (8, 16, 32):
-                cands.append(ScheduleConfig(f, sm, LaunchTiming.overlap(0, n)))
-            if n > 2:
-                cands.append(ScheduleConfig(f, 16, LaunchTiming.overlap(1, n - 1)))
-                cands.append(ScheduleConfig(f, 16, LaunchTiming.overlap(0, 2)))
-            rows = []
-            for c in cands:
-                m = eng.measure(prog.spec(), c, gpu, None, proto, None)
-                rows.append((c, m))
-            per_part[name] = rows
-        default = {n: per_part[n][2] for n in layer.order}  # overlap(0,n) @ 16 CTAs
-        seq = {n: per_part[n][0] for n in layer.order}
-        tmin = {n: min(per_part[n], key=lambda r: r[1].time_ms) for n in layer.order}
-        emin = {n: min(per_part[n], key=lambda r: r[1].total_energy_j) for n in layer.order}
+    per_part = None
+    mbo_path = os.path.join(ROOT, "profiles", f"r2_mbo_config{args.config}.json")
+    if args.no_sweep:
+        pass
+    elif not os.path.exists(mbo_path):
+        frontier = {"skipped": f"no MBO result for config {args.config} ({os.path.relpath(mbo_path, ROOT)})"}
+    else:
+        mb = json.load(open(mbo_path))
+        if mb.get("workload", "").split("-T")[-1] != wl.tag.split("-T")[-1]:
+            frontier = {"skipped": f"MBO result is for {mb.get('workload')}, not {wl.tag}"}
+        else:
+            def decode(enc):
+                t, sm, f = enc.split("@")
+                return ScheduleConfig(float(f), int(sm), LaunchTiming.decode(t))
 
-        def tot(choice):
-            return (sum(r[1].time_ms for r in choice.values()), sum(r[1].total_energy_j for r in choice.values()))
-
-        pts = {"nanobatching_default": tot(default), "sequential_megatron": tot(seq), "min_time": tot(tmin),
-               "min_energy": tot(emin)}
-        frontier = {k: {"time_ms": round(v[0], 4), "energy_j": round(v[1], 4)} for k, v in pts.items()}
-        frontier["chosen_min_energy"] = {n: emin[n][0].timing.encode() + f"@{emin[n][0].sm_alloc}" for n in layer.order}
-        # the selected schedule sets executed as whole iterations (device time + NVML energy over >= 2 s),
-        # next to the default nanobatching schedule measured the same way
-        frontier["executed"] = {}
-        for label, choice in (("nanobatching_default", default), ("min_time", tmin), ("min_energy", emin)):
-            sched = {n: choice[n][0] for n in layer.order}
-            r2 = LayerRunner(layer, eng, schedule=sched)
-            r2.warm()
-            for _ in range(3):
-                r2.step()
-            torch.cuda.synchronize(dev)
-            n_it = max(args.steps, int(math.ceil(2.0 / max(ms / 1e3, 1e-4))))
+            sets = {"nanobatching_default": run.schedule, "sequential_megatron": sequential_schedule(layer, gpu)}
+            for k, sel in mb.get("sets", {}).items():
+                if k.startswith("mbo_"):
+                    sets[k] = {n: decode(sel[n]) for n in layer.order}
+            runners = {k: LayerRunner(layer, eng, schedule=sch) for k, sch in sets.items()}
+            for r2 in runners.values():
+                r2.warm()
+            n_it = max(args.steps, int(math.ceil(args.sweep_window / max(ms / 1e3, 1e-4))))
+            acc = {k: {"s": [], "j": []} for k in sets}
             q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            barrier()
-            torch.cuda.synchronize(dev)
-            w0 = time.perf_counter()
-            q0.record(eng.exec.compute)
-            for _ in range(n_it):
-                r2.step()
-            q1.record(eng.exec.compute)
-            torch.cuda.synchronize(dev)
-            w1 = time.perf_counter()
-            t_it = max_over_ranks(q0.elapsed_time(q1) / n_it)
-            e_it = sum_over_ranks(eng.sampler.window_j(w0, w1) / n_it)
-            frontier["executed"][label] = {"s_per_iter": round(t_it / 1e3, 7), "j_per_iter": round(e_it, 4),
-                                           "iterations": n_it}
-        frontier["note"] = ("frequency fixed: NVML locked clocks NOT_SUPPORTED on this pool (power.py); sweep over "
-                            "comm SM budget x launch timing, windows of " + str(args.sweep_window) + " s")
+            for _trial in range(args.sweep_trials):
+                for k, r2 in runners.items():
+                    for _ in range(3):
+                        r2.step()
+                    barrier()
+                    torch.cuda.synchronize(dev)
+                    w0 = time.perf_counter()
+                    q0.record(eng.exec.compute)
+                    for _ in range(n_it):
+                        r2.step()
+                    q1.record(eng.exec.compute)
+                    torch.cuda.synchronize(dev)
+                    w1 = time.perf_counter()
+                    t_it = q0.elapsed_time(q1) / n_it / 1e3
+                    e_win = eng.sampler.window_j(w0, w1) - max(0.0, (w1 - w0) - t_it * n_it) * gpu.p_static_w
+                    acc[k]["s"].append(max_over_ranks(t_it))
+                    acc[k]["j"].append(sum_over_ranks(e_win / n_it))
+            ex_rows = {}
+            for k, v in acc.items():
+                sd = lambda xs: statistics.stdev(xs) if len(xs) > 1 else 0.0
+                ex_rows[k] = {"s_per_iter": round(statistics.mean(v["s"]), 7), "s_std": round(sd(v["s"]), 7),
+                              "j_per_iter": round(statistics.mean(v["j"]), 4), "j_std": round(sd(v["j"]), 4)}
+            d0 = ex_rows["nanobatching_default"]
+            for k, v in ex_rows.items():
+                v["time_vs_default"] = round(v["s_per_iter"] / d0["s_per_iter"] - 1, 5)
+                v["energy_vs_default"] = round(v["j_per_iter"] / d0["j_per_iter"] - 1, 5)
+            frontier = {"source": os.path.relpath(mbo_path, ROOT), "optimizer": mb.get("optimizer"),
+                        "protocol": mb.get("protocol"), "sets": mb.get("sets"), "executed": ex_rows,
+                        "trials": args.sweep_trials, "iterations_per_trial": n_it,
+                        "note": "frequency axis fixed at f_max: every NVML clock knob is refused on this pool "
+                                "(profiles/r2_clock_probe.json)"}
+            # the measured profile tables feed the reference's microbatch composition below
+            per_part = {}
+            from paper_2601_17654_b200.profiler import ProfileTable
+            for n in layer.order:
+                tp = os.path.join(ROOT, mb["partitions"][n]["table"]) if n in mb.get("partitions", {}) else None
+                if tp is None or not os.path.exists(tp):
+                    per_part = None
+                    break
+                t = ProfileTable.read(tp)
+                per_part[n] = [(r.config(), Measurement(r.time_ms, r.dyn_energy_j, r.static_energy_j,
+                                                        r.total_energy_j)) for r in t.rows]
 
     # ------------------------------------------------ non-partition work + microbatch composition
     # (SURVEY §8f item 1): embedding / final norm / LM head / loss measured on the hardware, and
     # the reference's own microbatch_frontier composing the measured partition candidates with it
     microbatch = None
-    if not args.no_sweep:
+    if not args.no_sweep and per_part is not None:
         microbatch = run_microbatch(args, wl, eng, gpu, layer, per_part, hbm, tf_sust, torch)
 
     # ------------------------------------------------ CPU baseline (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
-        cpu_sample(wl, args.cpu_tokens, threads)  # first call pays allocator / thread-pool warm-up
-        r = cpu_sample(wl, args.cpu_tokens, threads)
-        cpu = {"value": r["value"], "unit": "s/iter", "cores": threads, "kind": "port",
-               "sample": f"oracle/layer_ref.py fp32 fwd+bwd of 1 nanobatch x {args.cpu_tokens} tokens "
-                         f"({r['sample_s']:.2f} s), scaled x{r['scale']:.1f} by FLOPs to the full iteration"}
+        setup = cpu_layer_setup(wl, wl.nanobatches)
+        cpu_iteration(wl, threads, setup)  # first call pays allocator / thread-pool warm-up
+        ts = [cpu_iteration(wl, threads, setup) for _ in range(args.cpu_iters)]
+        facts = host_facts()
+        cpu = {"value": statistics.mean(ts), "unit": "s/iter", "cores": threads, "kind": "port",
+               "sample": f"oracle/layer_ref.py fp32 fwd+bwd of {args.cpu_iters} full layer iterations "
+                         f"({wl.nanobatches} x {wl.tokens} tokens each, unscaled; {sum(ts):.1f} s of CPU work)",
+               **facts}
         try:
             cpu["reference_path"] = reference_cpu_path(wl)
         except Exception as ex:  # reported, never fatal: the reference package is an optional guest here
@@ -523,15 +577,10 @@ def run_kpo(args):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (weights N(0,0.02) seed 0, activations N(0,1) seed 1000+rank)",
-            "config": {
-                "workload": f"{wl.model.name} layer iteration: fwd+bwd, {wl.nanobatches} nanobatches x {wl.tokens} "
-                            f"tokens per rank, 8 partitions",
-                "model": wl.model.name, "global_batch": wl.tokens * wl.nanobatches * world, "seq_len": wl.tokens,
-                "parallelism": (f"{wl.parallel}{group_world}-loopback" if world == 1 else f"{wl.parallel}{world}"),
-                "schedule": f"nanobatching default: f_max, {eng.default_ncta()} comm CTAs, overlap(0,n)",
-                "l2": "no flush: per-step working set (layer weights + activations) > 126 MB L2",
-                "graphs": len(eng.exec.graphs), "graph_failures": len(eng.exec.graph_failures),
-            },
+            "config": workload_config(wl, world, group_world),
+            "default_comm_ctas": eng.default_ncta(),
+            "graphs": {"captured": len(eng.exec.graphs), "failures": len(eng.exec.graph_failures),
+                       "launch_gate": eng.exec.gate_status},
             "energy_j_per_iter": energy_iter, "energy_window_steps": n_energy,
             "avg_power_w": energy_iter / (ms / 1e3) if ms > 0 else None,
             "tflops_per_gpu": iteration_flops(wl) / (ms / 1e3) / 1e12,

@@ -203,6 +203,11 @@ int kpo_comm_trace(kpo_comm* c, int64_t* buf, int n_slots);
  * cudaLaunchAttributeLaunchCompletionEvent = `launched_event` (cudaEvent_t) so the compute stream
  * can wait until every comm CTA is resident before its next kernel is dispatched. */
 int kpo_set_launch_completion_event(kpo_comm* c, void* launched_event);
+/* Probe: launches one empty kernel with that attribute on `stream`, synchronizes and queries the
+ * event.  Non-zero when the runtime (or a tool intercepting it) rejects the attribute; the executor
+ * then forks the collective without the launch gate.  No reference counterpart (the simulator's
+ * overlap starts instantly, simgpu.py:217-221). */
+int kpo_probe_launch_completion(void* launched_event, void* stream);
 
 #ifdef __cplusplus
 }

@@ -80,6 +80,7 @@ SIGNATURES = {
     "kpo_all_reduce": (_i32, [_c_void_p, _size, _size, _c_void_p, _size, _i32, _c_void_p]),
     "kpo_comm_trace": (_i32, [_c_void_p, _c_void_p, _i32]),
     "kpo_set_launch_completion_event": (_i32, [_c_void_p, _c_void_p]),
+    "kpo_probe_launch_completion": (_i32, [_c_void_p, _c_void_p]),
 }
 
 

@@ -12,6 +12,7 @@ NVLink.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 
 import torch
@@ -98,39 +99,47 @@ class Communicator:
         """out = concat over ranks of every rank's `src` region (bytes_per_rank = src.nbytes)."""
         if out.numel() * out.element_size() < src.nbytes * self.world:
             raise ValueError("all_gather: output too small")
-        self._pre()
-        _lib.call("kpo_all_gather", self._h, src.offset, out.data_ptr(), src.nbytes, int(ncta), _s(stream))
-        self._post()
+        with self._gated():
+            _lib.call("kpo_all_gather", self._h, src.offset, out.data_ptr(), src.nbytes, int(ncta), _s(stream))
 
     def reduce_scatter(self, src: SymRegion, out: torch.Tensor, ncta: int, stream=None) -> None:
         """out[i] = sum_p src_p[rank*count + i] (bf16, fp32 accumulation in rank order)."""
         count = src.nbytes // 2 // self.world
         if out.numel() < count:
             raise ValueError("reduce_scatter: output too small")
-        self._pre()
-        _lib.call("kpo_reduce_scatter", self._h, src.offset, out.data_ptr(), count, int(ncta), _s(stream))
-        self._post()
+        with self._gated():
+            _lib.call("kpo_reduce_scatter", self._h, src.offset, out.data_ptr(), count, int(ncta), _s(stream))
 
     def all_reduce(self, src: SymRegion, stage: SymRegion, out: torch.Tensor, ncta: int, stream=None) -> None:
         count = src.nbytes // 2
-        self._pre()
-        _lib.call("kpo_all_reduce", self._h, src.offset, stage.offset, out.data_ptr(), count, int(ncta), _s(stream))
-        self._post()
+        with self._gated():
+            _lib.call("kpo_all_reduce", self._h, src.offset, stage.offset, out.data_ptr(), count, int(ncta),
+                      _s(stream))
 
     def arm_launch_event(self, event: torch.cuda.Event | None) -> None:
         """The NEXT collective launched records `event` once all its CTAs are resident
         (cudaLaunchAttributeLaunchCompletionEvent); later launches do not."""
         self._armed = event
 
-    def _pre(self) -> None:
-        ev = getattr(self, "_armed", None)
-        if ev is not None:
-            _lib.call("kpo_set_launch_completion_event", self._h, ev.cuda_event)
-
-    def _post(self) -> None:
+    def disarm_launch_event(self) -> None:
+        """Forget an armed event (the executor calls this in a `finally`, even if the launch raised)."""
         if getattr(self, "_armed", None) is not None:
-            _lib.call("kpo_set_launch_completion_event", self._h, None)
             self._armed = None
+            _lib.call("kpo_set_launch_completion_event", self._h, None)
+
+    @contextlib.contextmanager
+    def _gated(self):
+        """Attach the armed launch-completion event to exactly one collective launch; the library
+        state is cleared even when the launch raises, so no later collective records it."""
+        ev = getattr(self, "_armed", None)
+        if ev is None:
+            yield
+            return
+        try:
+            _lib.call("kpo_set_launch_completion_event", self._h, ev.cuda_event)
+            yield
+        finally:
+            self.disarm_launch_event()
 
     def trace(self, buf: torch.Tensor | None, slots: int = 0) -> None:
         _lib.call("kpo_comm_trace", self._h, None if buf is None else buf.data_ptr(), int(slots))

@@ -23,3 +23,27 @@ extern "C" int kpo_device_info(int device, int* num_sms, int* smem_optin_bytes, 
   KPO_CUDA(cudaDeviceGetAttribute(cc_minor, cudaDevAttrComputeCapabilityMinor, device));
   return KPO_OK;
 }
+
+// Launch-completion-event probe: one empty kernel launched with
+// cudaLaunchAttributeLaunchCompletionEvent.  The partition executor's launch gate (executor.py) uses
+// this attribute on every overlapped collective; some tools (e.g. a profiler replaying kernels)
+// reject it, so the executor probes once and falls back to an ungated fork when it fails.
+__global__ void kpo_probe_kernel() {}
+
+extern "C" int kpo_probe_launch_completion(void* event, void* stream) {
+  KPO_CHECK_ARG(event, "probe_launch_completion: null event");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(32);
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeLaunchCompletionEvent;
+  attr[0].val.launchCompletionEvent.event = (cudaEvent_t)event;
+  attr[0].val.launchCompletionEvent.flags = 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  KPO_CUDA(cudaLaunchKernelEx(&cfg, kpo_probe_kernel));
+  KPO_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  KPO_CUDA(cudaEventQuery((cudaEvent_t)event));
+  return KPO_OK;
+}

@@ -10,10 +10,23 @@
 
 `measure` follows the reference protocol field by field: warm up for `warmup_s` (graph replays),
 execute back-to-back for reps = max(1, window_s // exec_s) (simgpu.py:347), read time from CUDA
-events and energy from the NVML counter over the same window, cool down for `cooldown_s`, and
-write the GPU temperature into `state.temperature_c`.  Dynamic energy is what the counter saw
-minus static power x time, and the result is `Measurement.build(t, E - P_s t, P_s)`
-(domain.py:245-248), so total == dyn + static exactly as the reference guarantees.
+events and energy from the NVML counter over the same window, cool down for `cooldown_s` (and,
+optionally, until the GPU is below `cooldown_target_c`), and write the GPU
+temperature into `state.temperature_c`.  Dynamic energy is what the counter saw minus static
+power x time, and the result is `Measurement.build(t, E - P_s t, P_s)` (domain.py:245-248), so
+total == dyn + static exactly as the reference guarantees.
+
+Frequency (ScheduleConfig.frequency_mhz, domain.py:151): the reference always honours f
+(simgpu.py:144-178).  Here f is applied with NVML locked clocks when the driver permits it and
+the clock the GPU actually ran is checked against it after the window.  When locked clocks are
+refused (this pool: profiles/r2_clock_probe.json), the only frequency the engine can honour is the
+unlocked default f_max (the boost ceiling); any other f raises `FrequencyUnavailableError` (an
+`InvalidConfigError`) before anything runs, so a profile table can never carry a mislabelled
+frequency.
+
+Multi-rank: every rank must launch the same number of collectives (their per-CTA flag barriers
+wait for the peers), so the warm-up and window repetition counts are derived from one execution-
+time estimate agreed across ranks (`agree_ms`, the MAX over ranks; spmd.py sets it).
 
 The reference optimizer calls `measure` as a module global (mbo.py:290-292); `install()` swaps it
 (and the `simulate_schedule` imports of oracle.py / compose.py) for this engine.
@@ -23,7 +36,7 @@ from __future__ import annotations
 
 import math
 import time
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import torch
 
@@ -31,6 +44,23 @@ from .device import GpuModel, InvalidConfigError, validate_schedule
 from .domain import Measurement
 from .executor import ScheduleExecutor
 from .power import EnergySampler, FrequencyController, Nvml
+
+# throttle reasons that invalidate a sample (re-measured once, then flagged); sw_power_cap is the
+# normal state of a dense-GEMM partition at ~1 kW and is only recorded
+BAD_REASONS = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "hw_power_brake_slowdown")
+
+
+def rep_counts(est_ms: float, warmup_s: float, window_s: float) -> tuple[int, int]:
+    """(warm-up executions, window executions) for an execution-time estimate: the window count is
+    the reference's reps = max(1, window // exec) (simgpu.py:347)."""
+    warm = max(1, int(warmup_s * 1e3 / est_ms)) if warmup_s > 0 else 0
+    return warm, max(1, int(window_s // (est_ms / 1e3)))
+
+
+class FrequencyUnavailableError(InvalidConfigError):
+    """The requested SM clock cannot be applied on this GPU (locked clocks refused, or the GPU ran
+    above the requested clock).  Subclass of InvalidConfigError so callers that screen invalid
+    configurations (reference mbo / cli) treat it the same way."""
 
 
 @dataclass
@@ -42,15 +72,25 @@ class Observation:
     gpu_ms: float = 0.0
     energy_j: float = 0.0
     sm_mhz: float = 0.0
+    requested_mhz: float = 0.0
     temperature_c: float = 0.0
+    temperature_start_c: float = 0.0
+    cooldown_s: float = 0.0
     reasons: tuple = ()
+    flags: tuple = ()
     clock_control: str = ""
     graph: bool = False
+    retried: int = 0
+
+    def as_dict(self) -> dict:
+        return {k: (list(v) if isinstance(v, tuple) else v) for k, v in self.__dict__.items()}
 
 
 class Engine:
-    def __init__(self, programs, gpu: GpuModel, device=None, comm=None, clock_control: bool = False,
-                 use_graphs: bool = True, launch_gate: bool = True, measurement_cls=Measurement):
+    def __init__(self, programs, gpu: GpuModel, device=None, comm=None, clock_control: bool = True,
+                 use_graphs: bool = True, launch_gate: bool = True, measurement_cls=Measurement,
+                 cooldown_target_c: float | None = None, cooldown_max_s: float = 30.0,
+                 reject_throttled: bool = True, clock_tolerance_mhz: float = 30.0):
         self.gpu = gpu
         self.device = torch.device(device or "cuda")
         self.comm = comm
@@ -59,13 +99,21 @@ class Engine:
             self.programs[p.name] = p
         self.exec = ScheduleExecutor(self.device, comm=comm, use_graphs=use_graphs, launch_gate=launch_gate)
         self.exec.ev_launched.record(self.exec.compute)  # materialise the CUDA event
+        self.exec.probe_gate()
         self.nvml = Nvml(self.device.index or 0)
         self.freq = FrequencyController(self.nvml, enable=clock_control)
         self.sampler = EnergySampler(self.nvml)
         self.sampler.start()
         self.measurement_cls = measurement_cls
+        self.cooldown_target_c = cooldown_target_c
+        self.cooldown_max_s = cooldown_max_s
+        self.reject_throttled = reject_throttled
+        self.clock_tolerance_mhz = clock_tolerance_mhz
         self.last = Observation()
+        self.history: list[Observation] = []
         self._exec_ms: dict[tuple, float] = {}
+        # multi-rank: maps this rank's execution-time estimate to the value every rank uses
+        self.agree_ms = None
 
     @classmethod
     def for_layer(cls, layer, gpu: GpuModel, **kw) -> "Engine":
@@ -88,19 +136,50 @@ class Engine:
     def default_ncta(self, gpu=None) -> int:
         return int((gpu or self.gpu).sm_bw_saturation)
 
+    # ------------------------------------------------------------------ frequency
+    def frequencies(self, gpu: GpuModel | None = None) -> list[float]:
+        """The SM clocks this engine can honour: the NVML grid when clocks can be locked, else f_max."""
+        gpu = gpu or self.gpu
+        if self.freq.available:
+            return [f for f in self.nvml.supported_sm_clocks() if f <= gpu.f_max_mhz]
+        return [float(gpu.f_max_mhz)]
+
+    def check_frequency(self, f_mhz: float, gpu: GpuModel | None = None) -> None:
+        gpu = gpu or self.gpu
+        if self.freq.available:
+            return
+        if abs(float(f_mhz) - float(gpu.f_max_mhz)) > 0.5:
+            raise FrequencyUnavailableError(
+                f"frequency {f_mhz} MHz cannot be applied: NVML locked clocks are unavailable on this GPU "
+                f"({self.freq.reason}); only the unlocked default f_max = {gpu.f_max_mhz} MHz is measurable")
+
+    def _apply_frequency(self, f_mhz: float, gpu: GpuModel | None = None) -> None:
+        self.check_frequency(f_mhz, gpu)
+        if self.freq.available and not self.freq.set(f_mhz):
+            raise FrequencyUnavailableError(f"NVML refused locked clocks at {f_mhz} MHz")
+
     # ------------------------------------------------------------------ core window
-    def _window(self, prog, config, ncta, warmup_s: float, window_s: float) -> tuple[float, float, int]:
+    def estimate_ms(self, prog, config, ncta) -> float:
         ex = self.exec
         key = ex._key(prog, config, ncta)
         est = self._exec_ms.get(key)
         if est is None:
             est = ex.time_ms(prog, config, ncta, reps=3, warmup=1)
             self._exec_ms[key] = est
-        if warmup_s > 0:
-            ex.run(prog, config, ncta, max(1, int(warmup_s * 1e3 / est)))
-        reps = max(1, int(window_s // (est / 1e3)))
+        return est
+
+    def _window(self, prog, config, ncta, warmup_s: float, window_s: float) -> tuple[float, float, int]:
+        ex = self.exec
+        key = ex._key(prog, config, ncta)
+        est = self.estimate_ms(prog, config, ncta)
+        if self.agree_ms is not None:
+            est = float(self.agree_ms(est))  # identical repetition counts on every rank
+        warm, reps = rep_counts(est, warmup_s, window_s)
+        if warm:
+            ex.run(prog, config, ncta, warm)
         torch.cuda.synchronize(self.device)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        temp0 = self.nvml.temperature_c()
         t0 = time.perf_counter()
         e0.record(ex.compute)
         ex.run(prog, config, ncta, reps)
@@ -113,36 +192,81 @@ class Engine:
         energy -= idle * self.gpu.p_static_w  # host-side launch latency at the window edges
         self._exec_ms[key] = gpu_ms / reps
         clocks = self.sampler.clocks_summary(t0, t1)
+        reasons = tuple(clocks.get("reasons", ()))
+        flags = tuple(r for r in reasons if r in BAD_REASONS)
+        if "sw_power_cap" in reasons:
+            flags += ("power_capped",)
         self.last = Observation(reps=reps, window_s=t1 - t0, gpu_ms=gpu_ms, energy_j=energy,
-                                sm_mhz=clocks.get("sm_mhz", 0.0), reasons=tuple(clocks.get("reasons", ())),
+                                sm_mhz=clocks.get("sm_mhz", 0.0), requested_mhz=float(config.frequency_mhz),
+                                temperature_start_c=temp0, reasons=reasons, flags=flags,
                                 clock_control=self.freq.reason, graph=key in ex.graphs)
         return gpu_ms / reps, energy / reps, reps
+
+    def _cooldown(self, cooldown_s: float) -> float:
+        """Idle for cooldown_s, then (if a target is set) until the GPU is below it; returns the idle time."""
+        t0 = time.perf_counter()
+        if cooldown_s > 0:
+            time.sleep(cooldown_s)
+        if self.cooldown_target_c is not None:
+            while (self.nvml.temperature_c() > self.cooldown_target_c
+                   and time.perf_counter() - t0 < cooldown_s + self.cooldown_max_s):
+                time.sleep(0.25)
+        return time.perf_counter() - t0
+
+    def _verify_clock(self, config) -> None:
+        """With locked clocks the GPU must not run above the requested clock (it may run below it
+        under a power cap, which is flagged, not rejected)."""
+        obs = self.last
+        if self.freq.available and obs.sm_mhz > float(config.frequency_mhz) + self.clock_tolerance_mhz:
+            raise FrequencyUnavailableError(
+                f"requested {config.frequency_mhz} MHz but the GPU ran at {obs.sm_mhz} MHz (median of the window)")
+        if obs.sm_mhz and obs.sm_mhz < float(config.frequency_mhz) - self.clock_tolerance_mhz:
+            obs.flags = tuple(obs.flags) + ("below_requested_clock",)
 
     def _prepare(self, partition, config, gpu):
         gpu = gpu or self.gpu
         validate_schedule(partition, config, gpu)  # InvalidConfigError before any native call
+        self.check_frequency(config.frequency_mhz, gpu)
         prog = self.program_for(partition)
-        self.freq.set(config.frequency_mhz)
         return gpu, prog
 
     # ------------------------------------------------------------------ public API
-    def execute(self, partition, config, gpu: GpuModel | None = None, window_s: float = 0.3):
-        """One noise-free execution (reference simulate_schedule)."""
+    def execute(self, partition, config, gpu: GpuModel | None = None, window_s: float = 1.0):
+        """One noise-free execution (reference simulate_schedule).  The window defaults to 1 s, about
+        ten steps of the NVML energy counter (power.py)."""
         gpu, prog = self._prepare(partition, config, gpu)
+        self._apply_frequency(config.frequency_mhz, gpu)
         t_ms, e_j, _ = self._window(prog, config, self.default_ncta(gpu), 0.05, window_s)
+        self._verify_clock(config)
+        self.history.append(self.last)
         return self.measurement_cls.build(t_ms, e_j - gpu.p_static_w * t_ms / 1e3, gpu.p_static_w)
 
     def measure_local(self, name: str, config, warmup_s: float, window_s: float, cooldown_s: float,
                       ncta: int | None = None) -> tuple[float, float, float]:
         """This rank's (time_ms, energy_j per execution, temperature) for a registered program;
-        the SPMD driver (spmd.py) combines ranks."""
+        the SPMD driver (spmd.py) combines ranks.  A window that saw a hardware / thermal slowdown
+        is re-measured once (after the cooldown) and flagged if it happens again."""
         prog = self.programs[name]
-        self.freq.set(config.frequency_mhz)
-        t_ms, e_j, _ = self._window(prog, config, ncta or self.default_ncta(), warmup_s, window_s)
-        if cooldown_s > 0:
-            time.sleep(cooldown_s)
+        self._apply_frequency(config.frequency_mhz)
+        ncta = ncta or self.default_ncta()
+        retried = 0
+        while True:
+            t_ms, e_j, _ = self._window(prog, config, ncta, warmup_s, window_s)
+            self._verify_clock(config)
+            obs = self.last
+            obs.cooldown_s = self._cooldown(cooldown_s)
+            # every rank takes the same branch: the decision must not depend on rank-local flags when
+            # ranks are coupled by collectives, so the retry is driven by the agreed hook if present
+            bad = any(f in BAD_REASONS for f in obs.flags)
+            if self.agree_ms is not None:
+                bad = bool(self.agree_ms(1.0 if bad else 0.0) > 0.5)
+            if not (self.reject_throttled and bad and retried == 0):
+                break
+            retried += 1
         temp = self.nvml.temperature_c()
-        self.last.temperature_c = temp
+        obs.temperature_c = temp
+        obs.retried = retried
+        self.history.append(obs)
         return t_ms, e_j, temp
 
     def measure(self, partition, config, gpu: GpuModel | None = None, thermal=None, protocol=None, state=None):
@@ -176,4 +300,5 @@ def install(engine, schedfront_module=None):
     return patch_reference(engine.measure_fn(), engine.simulate_fn(), schedfront_module)
 
 
-__all__ = ["Engine", "Observation", "install", "InvalidConfigError", "math"]
+__all__ = ["Engine", "Observation", "install", "rep_counts", "InvalidConfigError", "FrequencyUnavailableError", "BAD_REASONS",
+           "math", "field"]

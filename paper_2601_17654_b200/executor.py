@@ -39,11 +39,38 @@ class ScheduleExecutor:
         self.ev_done = torch.cuda.Event()
         self.use_graphs = use_graphs
         self.launch_gate = launch_gate
+        self.gate_status = "disabled" if not launch_gate else "unprobed"
         self.graphs: dict[tuple, torch.cuda.CUDAGraph] = {}
         self.graph_failures: dict[tuple, str] = {}
         # graph-set tag: callers that swap the tensors a program reads (LayerRunner's host-staging
         # slots) keep one captured graph per (program, schedule, variant)
         self.variant = None
+
+    # ------------------------------------------------------------------ launch gate
+    def probe_gate(self) -> bool:
+        """Probe once whether collectives can carry the launch-completion event (a profiler replaying
+        kernels, for one, rejects it); on failure the executor forks the collective ungated."""
+        if not self.launch_gate or self.comm is None:
+            return False
+        if self.gate_status != "unprobed":
+            return self.launch_gate
+        from . import _lib
+
+        ev = torch.cuda.Event()
+        try:
+            ev.record(self.compute)
+            _lib.call("kpo_probe_launch_completion", ev.cuda_event, self.comm_stream.cuda_stream)
+            self.compute.wait_event(ev)
+            self.compute.synchronize()
+            self.gate_status = "ok"
+        except Exception as ex:  # noqa: BLE001 - any refusal means: no gate
+            self.launch_gate = False
+            self.gate_status = f"off: {type(ex).__name__}: {ex}"
+            try:
+                torch.cuda.synchronize(self.device)
+            except Exception:
+                pass
+        return self.launch_gate
 
     # ------------------------------------------------------------------ enqueue
     def issue(self, prog, config, default_ncta: int) -> None:
@@ -63,10 +90,14 @@ class ScheduleExecutor:
             u.fn(comp)
         self.ev_fork.record(comp)
         side.wait_event(self.ev_fork)
-        gate = self.launch_gate and self.comm is not None
+        gate = self.launch_gate and self.comm is not None and self.probe_gate()
         if gate:
             self.comm.arm_launch_event(self.ev_launched)
-        prog.comm.fn(side, int(config.sm_alloc))
+        try:
+            prog.comm.fn(side, int(config.sm_alloc))
+        finally:
+            if gate:
+                self.comm.disarm_launch_event()
         self.ev_done.record(side)
         if gate:
             comp.wait_event(self.ev_launched)

@@ -70,6 +70,19 @@ class PartitionProgram:
         return PartitionSpec(tuple(u.spec for u in self.units), self.comm.spec, self.comm_group_size, self.name)
 
 
+def sym_bytes_for(wl: Workload, slack: int = 64 << 20) -> int:
+    """Symmetric-heap bytes one rank's PartitionedLayer allocates: FSDP flat shards plus two
+    layer-parity gradient buffers per tensor (and the dγ buffer); TP four partial sums per
+    nanobatch plus the all-reduce stage."""
+    if wl.parallel == "fsdp":
+        tot = 0
+        for t in ("wqkv", "wo", "wgu", "wd", "gn"):
+            n = specs.fsdp_numel(wl, t)
+            tot += (0 if t == "gn" else (n // wl.world * 2 + 256)) + 2 * (n * 2 + 256)
+        return tot + slack
+    return (4 * wl.nanobatches + 1) * (wl.tokens * wl.h * 2 + 256) + slack
+
+
 class PartitionedLayer:
     """One rank's partitioned layer (weights, activations, gradients) for a Workload."""
 
@@ -83,7 +96,10 @@ class PartitionedLayer:
             raise ValueError("communicator world size does not match the workload")
         self.sched = ops.GemmScheduler(self.device, slots=64)
         self._init_weights(seed)
-        self._init_activations(1000 + self.rank if data_seed is None else data_seed)
+        # data seed 1000 + rank; TP ranks share their input (replicated activations)
+        if data_seed is None:
+            data_seed = 1000 if wl.parallel == "tp" else 1000 + self.rank
+        self._init_activations(data_seed)
         self.programs: dict[str, PartitionProgram] = {}
         self.order: list[str] = []
         self._build_units()
@@ -137,38 +153,59 @@ class PartitionedLayer:
             full = dict(full, wgu=ops.interleave_gate_up(full["wgu"]))
         self.full_weights = full if wl.world == 1 or wl.parallel == "fsdp" else None
         self.tensors = ("wqkv", "wo", "wgu", "wd")
+        T, h = wl.tokens, wl.h
+        dev = self.device
+        c = self.comm
+        # `self.w` / `self.dw` are the LIVE dicts the launch units read when they are issued; for FSDP
+        # set_parity() repoints them at the layer-parity buffers (see there)
+        self.parity = 0
         if wl.parallel == "tp":
             self.w = self.tp_shard(full, self.rank)
             if self.swiglu_fused:
                 self.w["wgu"] = ops.interleave_gate_up(self.w["wgu"])
         else:
             self.w = {k: v for k, v in full.items()}
-        T, h = wl.tokens, wl.h
-        dev = self.device
-        c = self.comm
         if wl.parallel == "fsdp":
-            # flat shards of every weight tensor live in the symmetric buffer
+            # Layer-parity double buffering (steady state of a stack of identical layers): iteration k
+            # computes with the gathered weights wbuf[k%2] and writes its weight gradients into
+            # dw_sym[k%2]; its collectives all-gather the NEXT layer's weights into wbuf[1-k%2] and
+            # reduce-scatter the PREVIOUS layer's gradients from dw_sym[1-k%2].  So every gathered
+            # weight is consumed by the next iteration and every reduce-scatter reads real gradients.
+            # wbuf[1] starts zeroed: iteration 1 is only correct if iteration 0's all-gathers were.
             self.shard = {}
-            self.w_next = {}
-            self.dw_sym = [{}, {}]  # two layer-parity gradient buffers (RS inputs)
+            self.wbuf = [{}, {}]
+            self.dw_sym = [{}, {}]  # gradient buffers (RS inputs) in the symmetric heap
             self.dw_shard = {}
-            for name in self.tensors:
-                n = full[name].numel()
+            names = self.tensors + ("gn",)
+            for name in names:
+                n = specs.fsdp_numel(wl, name)
                 if n % (8 * wl.world):
                     raise ValueError(f"{name} numel {n} not divisible by 8*world")
                 per = n // wl.world
-                reg = c.alloc(per * 2)
-                reg.local().copy_(full[name].view(-1)[self.rank * per:(self.rank + 1) * per])
-                if c.loopback:
-                    for p in range(wl.world):
-                        if p != self.rank:
-                            reg.peer(p).copy_(full[name].view(-1)[p * per:(p + 1) * per])
-                self.shard[name] = reg
-                self.w_next[name] = torch.empty_like(full[name])
+                if name != "gn":  # norm weights are replicated; only their gradients are reduced
+                    reg = c.alloc(per * 2)
+                    reg.local().copy_(full[name].view(-1)[self.rank * per:(self.rank + 1) * per])
+                    if c.loopback:
+                        for p in range(wl.world):
+                            if p != self.rank:
+                                reg.peer(p).copy_(full[name].view(-1)[p * per:(p + 1) * per])
+                    self.shard[name] = reg
+                    self.wbuf[0][name] = full[name].clone()  # full_weights stays the pristine copy
+                    self.wbuf[1][name] = torch.zeros_like(full[name])
                 for par in range(2):
-                    self.dw_sym[par][name] = c.alloc(n * 2)
+                    reg = c.alloc(n * 2)
+                    reg.local().zero_()
+                    if c.loopback:
+                        # virtual peers' gradients: a fixed seeded pattern (never rewritten), so the
+                        # loopback reduce-scatter output is checkable against the numpy oracle
+                        g = torch.Generator(device=dev).manual_seed(7919 * (par + 1) + len(name))
+                        for p in range(wl.world):
+                            if p != self.rank:
+                                reg.peer(p).copy_((torch.randn(n, generator=g, device=dev) * 1e-2).to(BF16))
+                    self.dw_sym[par][name] = reg
                 self.dw_shard[name] = torch.empty(per, dtype=BF16, device=dev)
-            self.dw = {k: self.dw_sym[0][k].local().view(self.w[k].shape) for k in self.tensors}
+            self.dw = {}
+            self.set_parity(0)
         else:
             self.dw = {k: torch.empty_like(self.w[k]) for k in self.tensors}
             self.partial = [{}, {}]
@@ -176,8 +213,38 @@ class PartitionedLayer:
                 for name in ("hp", "yp", "dxn2p", "dxn1p"):
                     self.partial[b % 2][(name, b)] = c.alloc(T * h * 2)
             self.stage = c.alloc(T * h * 2)
-        self.dg1 = torch.empty(h, dtype=BF16, device=dev)
-        self.dg2 = torch.empty(h, dtype=BF16, device=dev)
+            self.dg1 = torch.empty(h, dtype=BF16, device=dev)
+            self.dg2 = torch.empty(h, dtype=BF16, device=dev)
+
+    @property
+    def parity_period(self) -> int:
+        """Number of distinct buffer sets consecutive iterations cycle through (graph variants)."""
+        return 2 if self.wl.parallel == "fsdp" else 1
+
+    def set_parity(self, p: int) -> None:
+        """Point the live weight / gradient dicts at layer-parity p (FSDP; a no-op for TP).  Launch
+        units and comm units resolve their buffers when they are issued, so a CUDA graph captured
+        under parity p replays parity p."""
+        p &= 1
+        if self.wl.parallel != "fsdp":
+            self.parity = 0
+            return
+        self.parity = p
+        h = self.wl.h
+        self.w.update(self.wbuf[p])
+        for k in self.tensors:
+            self.dw[k] = self.dw_sym[p][k].local().view(self.wbuf[p][k].shape)
+        gn = self.dw_sym[p]["gn"].local()
+        self.dg1, self.dg2 = gn[:h], gn[h:2 * h]
+
+    @property
+    def w_next(self) -> dict[str, torch.Tensor]:
+        """The buffers this iteration's all-gathers write (the next iteration's weights)."""
+        return self.wbuf[1 - self.parity]
+
+    def dgn_shard(self) -> torch.Tensor:
+        """This rank's reduce-scattered shard of [dg1; dg2] (FSDP)."""
+        return self.dw_shard["gn"]
 
     def _init_activations(self, data_seed: int) -> None:
         wl = self.wl
@@ -187,6 +254,8 @@ class PartitionedLayer:
         E = lambda *s, dt=BF16: torch.zeros(*s, dtype=dt, device=dev)
         self.nb = []
         nparts = ops.rmsnorm_partials(T, h)
+        # per-CTA fp32 partials of dγ for every nanobatch, contiguous so one column sum reduces them
+        self.dwp_all = [E(wl.nanobatches * nparts, h, dt=torch.float32) for _ in range(2)]
         for b in range(wl.nanobatches):
             a = {
                 "x": torch.randn(T, h, generator=g, device=dev).to(BF16),
@@ -198,7 +267,8 @@ class PartitionedLayer:
                 "dact": E(T, wl.ffn), "dgu": E(T, 2 * wl.ffn), "dxn2": E(T, h), "dh": E(T, h),
                 "dao": E(T, wl.hq * d), "dqkr": E(T, (wl.hq + wl.hkv) * d), "dqkv": E(T, wl.qkv_dim),
                 "dxn1": E(T, h), "dx": E(T, h),
-                "dwp1": E(nparts, h, dt=torch.float32), "dwp2": E(nparts, h, dt=torch.float32),
+                "dwp1": self.dwp_all[0][b * nparts:(b + 1) * nparts],
+                "dwp2": self.dwp_all[1][b * nparts:(b + 1) * nparts],
             }
             if wl.parallel == "fsdp":
                 a["dxn2p"] = a["dxn2"]
@@ -220,7 +290,7 @@ class PartitionedLayer:
         eps, theta = wl.model.norm_eps, wl.model.rope_theta
         tp = wl.parallel == "tp"
         rank0 = self.rank == 0
-        W, dw = self.w, self.dw
+        W, dw = self.w, self.dw  # live dicts (set_parity repoints their entries)
         US = specs.unit_specs(wl)
         fused = specs.fused_rope(wl)
         qk_src = "qkv" if fused else "qkr"
@@ -306,9 +376,14 @@ class PartitionedLayer:
                     a["dqkv"], a["xn1"], dw["wqkv"], accumulate=dw["wqkv"] if acc else None, sched=s["qkv_wgrad"],
                     stream=st),
             }
+            if b == wl.nanobatches - 1:
+                # dγ1 / dγ2 of the iteration: column sums of both nanobatches' per-CTA partials (FSDP:
+                # into the symmetric gradient buffer the next iteration reduce-scatters)
+                fns["norm_grads"] = lambda st: (ops.colsum(self.dwp_all[0], self.dg1, stream=st),
+                                                ops.colsum(self.dwp_all[1], self.dg2, stream=st))
             for name, fn in fns.items():
                 kind = "gemm" if name in specs.GEMM_UNITS else kinds.get(name, "memory")
-                nk = 3 if name == "attention_bwd" else 1  # pre-pass, main kernel, dq conversion
+                nk = {"attention_bwd": 3, "norm_grads": 2}.get(name, 1)  # attn: pre-pass, main, dq conversion
                 self.units[(name, b)] = LaunchUnit(name, US[name], fn, kind, nk)
 
     # ------------------------------------------------------------------ comm units
@@ -327,10 +402,12 @@ class PartitionedLayer:
 
         def fn(st, ncta):
             for kind, name in tensors:
+                # buffers resolved at issue time: parity p gathers into wbuf[1-p], reduces dw_sym[1-p]
                 if kind == "ag":
-                    self.comm.all_gather(self.shard[name], self.w_next[name], ncta, stream=st)
+                    self.comm.all_gather(self.shard[name], self.wbuf[1 - self.parity][name], ncta, stream=st)
                 else:
-                    self.comm.reduce_scatter(self.dw_sym[1][name], self.dw_shard[name], ncta, stream=st)
+                    self.comm.reduce_scatter(self.dw_sym[1 - self.parity][name], self.dw_shard[name], ncta,
+                                             stream=st)
 
         return CommUnit(spec.name, spec, fn, algo_bytes=link, n_kernels=len(tensors))
 
@@ -347,17 +424,14 @@ class PartitionedLayer:
                 comm = self._ar_unit(arg, self.nb[arg[1]][out_of[arg[0]]])
             else:
                 comm = self._fsdp_unit(arg)
-            units = [self.units[(k, b)] for k in dict(specs.blocks(self.wl))[blk]]
+            units = [self.units[(k, b)] for k in specs.block_units(self.wl, blk, b)]
             self.programs[name] = PartitionProgram(name, units, comm, wl.world)
             self.order.append(name)
 
     # ------------------------------------------------------------------ helpers
     def finalize_norm_grads(self, stream=None) -> None:
-        """dg1/dg2 = column sums of the per-CTA partials of both nanobatches."""
-        p1 = torch.cat([a["dwp1"] for a in self.nb])
-        p2 = torch.cat([a["dwp2"] for a in self.nb])
-        ops.colsum(p1, self.dg1, stream=stream)
-        ops.colsum(p2, self.dg2, stream=stream)
+        """dg1/dg2 = column sums of the per-CTA partials of both nanobatches (the norm_grads unit)."""
+        self.units[("norm_grads", self.wl.nanobatches - 1)].fn(stream or torch.cuda.current_stream())
 
     def partition_specs(self) -> list[PartitionSpec]:
         return [self.programs[n].spec() for n in self.order]

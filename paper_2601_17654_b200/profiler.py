@@ -121,6 +121,20 @@ def gpu_header(gpu) -> dict:
     return {f.name: getattr(gpu, f.name) for f in dataclasses.fields(gpu)}
 
 
+def observation_dict(last) -> dict:
+    """What the hardware observed during a measurement (engine.Observation), for table rows."""
+    if last is None:
+        return {}
+    if hasattr(last, "as_dict"):
+        d = last.as_dict()
+        d["window_s"] = round(d.get("window_s", 0.0), 4)
+        d["gpu_ms"] = round(d.get("gpu_ms", 0.0), 5)
+        return d
+    return {"reps": last.reps, "window_s": round(last.window_s, 4), "sm_mhz": last.sm_mhz,
+            "temperature_c": last.temperature_c, "reasons": list(last.reasons),
+            "clock_control": last.clock_control, "graph": last.graph}
+
+
 class Profiler:
     """Batch-measures candidates through an engine-like object exposing
     measure(partition, config, gpu, thermal, protocol, state) and `last` observations."""
@@ -138,11 +152,7 @@ class Profiler:
                 continue
             m = self.engine.measure(partition, cfg, self.gpu, self.thermal, self.protocol, self.state)
             last = getattr(self.engine, "last", None)
-            obs = {}
-            if last is not None:
-                obs = {"reps": last.reps, "window_s": round(last.window_s, 4), "sm_mhz": last.sm_mhz,
-                       "temperature_c": last.temperature_c, "reasons": list(last.reasons),
-                       "clock_control": last.clock_control, "graph": last.graph}
+            obs = observation_dict(last)
             table.add(cfg, m, obs)
             if progress:
                 progress(i, cfg, m, time.perf_counter() - t0)

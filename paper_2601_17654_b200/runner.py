@@ -30,6 +30,8 @@ class LayerRunner:
         self.engine = engine
         self.schedule = schedule or default_schedule(layer, engine.gpu)
         self.ncta = engine.default_ncta()
+        self.k = 0          # iterations enqueued so far (selects the layer-parity buffers)
+        self._slot = None   # host-staging slot the layer currently points at (None: its own tensors)
 
     def kernels_per_step(self) -> int:
         n = 0
@@ -38,15 +40,29 @@ class LayerRunner:
             n += sum(u.n_kernels for u in p.units) + p.comm.n_kernels
         return n
 
+    def _select(self, parity: int) -> None:
+        """Point the layer at layer-parity `parity` and the executor at the matching graph set."""
+        self.layer.set_parity(parity)
+        self.engine.exec.variant = (self.layer.parity, self._slot)
+
     def step(self) -> None:
-        """Enqueue one layer iteration on the engine's compute stream (graph replays)."""
+        """Enqueue one layer iteration on the engine's compute stream (graph replays).  Consecutive
+        iterations alternate the FSDP layer-parity buffers (PartitionedLayer.set_parity), so the
+        weights gathered by iteration k are the ones iteration k+1 computes with."""
         ex = self.engine.exec
+        self._select(self.k % self.layer.parity_period)
         for name in self.layer.order:
             ex.run(self.layer.programs[name], self.schedule[name], self.ncta, 1)
+        self.k += 1
 
     def warm(self) -> None:
-        for name in self.layer.order:
-            self.engine.exec.graph(self.layer.programs[name], self.schedule[name], self.ncta)
+        """Capture every partition's graph for every layer parity (executes each once)."""
+        k0 = self.k
+        for par in range(self.layer.parity_period):
+            self._select(par)
+            for name in self.layer.order:
+                self.engine.exec.graph(self.layer.programs[name], self.schedule[name], self.ncta)
+        self._select(k0 % self.layer.parity_period)
         torch.cuda.synchronize(self.engine.device)
 
     # ---------------------------------------------------------------- host-buffer entry point
@@ -71,7 +87,8 @@ class LayerRunner:
         tensors); the executor keeps a separate graph set per slot."""
         for a, own, slot in zip(self.layer.nb, self._own, self._slots[s] if s is not None else self._own):
             a["x"], a["dy"], a["dx"] = slot
-        self.engine.exec.variant = None if s is None else ("host-slot", s)
+        self._slot = s
+        self.engine.exec.variant = (self.layer.parity, s)
 
     def prepare_host_pipeline(self) -> None:
         """Allocate the two host-staging slots and capture their graphs (this executes every partition

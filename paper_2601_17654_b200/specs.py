@@ -53,18 +53,37 @@ def blocks(wl: Workload) -> list[tuple[str, list[str]]]:
     return [(blk, [k for k in units if k not in drop]) for blk, units in BLOCKS]
 
 
+def block_units(wl: Workload, blk: str, b: int) -> list[str]:
+    """Launch units of partition (blk, b): the block's units, plus the dγ column sums
+    ("norm_grads") at the end of the iteration's last backward partition."""
+    units = list(dict(blocks(wl))[blk])
+    if blk == "bwd_attn" and b == wl.nanobatches - 1:
+        units.append("norm_grads")
+    return units
+
+
 # FSDP comm units per partition: ('ag', t) all-gathers the next layer's weight t, ('rs', t)
 # reduce-scatters the previous layer's gradient of t (fused into one comm unit, compose.py:32-45).
 FSDP_COMMS = {
     ("fwd_attn", 0): [("ag", "wqkv")], ("fwd_attn", 1): [("ag", "wo")],
     ("fwd_mlp", 0): [("ag", "wgu")], ("fwd_mlp", 1): [("ag", "wd")],
     ("bwd_mlp", 0): [("rs", "wd"), ("ag", "wd")], ("bwd_mlp", 1): [("rs", "wgu"), ("ag", "wgu")],
-    ("bwd_attn", 0): [("rs", "wo"), ("ag", "wo")], ("bwd_attn", 1): [("rs", "wqkv"), ("ag", "wqkv")],
+    ("bwd_attn", 0): [("rs", "wo"), ("ag", "wo")],
+    # the last one also reduce-scatters the previous layer's RMSNorm gradients [dγ1; dγ2] ("gn")
+    ("bwd_attn", 1): [("rs", "wqkv"), ("ag", "wqkv"), ("rs", "gn")],
 }
 # TP: partition i all-reduces the partial produced by partition i-1 (the other nanobatch).
 TP_PRODUCED = {"fwd_attn": "hp", "fwd_mlp": "yp", "bwd_mlp": "dxn2p", "bwd_attn": "dxn1p"}
 GEMM_UNITS = {"linear_qkv", "linear_proj", "linear_up", "linear_down", "down_dgrad", "down_wgrad", "gu_dgrad",
               "gu_wgrad", "o_dgrad", "o_wgrad", "qkv_dgrad", "qkv_wgrad"}
+
+
+def fsdp_numel(wl: Workload, tensor: str) -> int:
+    """Elements of one FSDP flat tensor: the weights, or "gn" = [dγ1; dγ2] padded to 8*world."""
+    if tensor == "gn":
+        q = 8 * wl.world
+        return (2 * wl.h + q - 1) // q * q
+    return wl.weight_numels()[tensor]
 
 
 def _gemm(name, M, N, K):
@@ -103,7 +122,20 @@ def unit_specs(wl: Workload) -> dict[str, KernelSpec]:
         "rope_bwd": _mem("rope_bwd", 4 * T * qd, 6 * T * qd),
         "qkv_dgrad": _gemm("qkv_dgrad", T, h, wl.qkv_dim),
         "qkv_wgrad": _gemm("qkv_wgrad", wl.qkv_dim, h, T),
+        # column sums of nanobatches x per-CTA fp32 partials of dγ1 and dγ2 -> bf16
+        "norm_grads": _mem("norm_grads", 2 * (wl.nanobatches * _norm_partials(T, h) * h * 4 + 2 * h),
+                           2 * wl.nanobatches * _norm_partials(T, h) * h),
     }
+
+
+def _norm_partials(T: int, h: int) -> int:
+    """Rows of per-CTA dγ partials kpo_rmsnorm_bwd writes (mirrors kpo_rmsnorm_bwd_partial_rows,
+    elementwise.cu), without needing the library."""
+    try:
+        from . import ops
+        return ops.rmsnorm_partials(T, h)
+    except Exception:
+        return 2 * 148
 
 
 def partition_order(wl: Workload) -> list[tuple[str, int]]:
@@ -120,8 +152,7 @@ def ar_spec(wl: Workload, src: tuple[str, int]) -> tuple[KernelSpec, float]:
 
 def fsdp_spec(wl: Workload, tensors: list[tuple[str, str]]) -> tuple[KernelSpec, float]:
     W = wl.world
-    numels = wl.weight_numels()
-    link = sum((W - 1) / W * numels[t] * 2 for _, t in tensors)
+    link = sum((W - 1) / W * fsdp_numel(wl, t) * 2 for _, t in tensors)
     label = "+".join(f"{k}_{t}" for k, t in tensors)
     return KernelSpec(label, comm_bytes=max(link, 1.0)), link
 
@@ -148,5 +179,5 @@ def partition_specs(wl: Workload) -> list[PartitionSpec]:
         name = f"{blk}{b}"
         kind, arg = plan[name]
         cspec = ar_spec(wl, arg)[0] if kind == "ar" else fsdp_spec(wl, arg)[0]
-        out.append(PartitionSpec(tuple(us[k] for k in dict(blocks(wl))[blk]), cspec, wl.world, name))
+        out.append(PartitionSpec(tuple(us[k] for k in block_units(wl, blk, b)), cspec, wl.world, name))
     return out

@@ -8,7 +8,14 @@ time = max over ranks, energy = sum over ranks.  With `gpu.p_static_w` set to th
 power (sum of per-GPU idle power), `Measurement.build` and the optimizer's static-energy passes
 (mbo.py:190-192) stay consistent.  Other ranks sit in `serve()` until rank 0 calls `stop()`.
 
-Invalid configurations raise `InvalidConfigError` on rank 0 before anything is broadcast.
+Every rank must launch the same number of collectives (their per-CTA flag barriers wait for the
+peers), so the warm-up / window repetition counts come from one execution-time estimate agreed
+across ranks: `SpmdEngine` installs `local.agree_ms` = MAX over ranks, which `Engine._window` applies
+before deriving the counts.
+
+Invalid configurations raise `InvalidConfigError` on rank 0 before anything is broadcast.  The
+scalar reductions run on the local CUDA device when the group's backend is NCCL (which cannot
+reduce CPU tensors) and on the CPU otherwise.
 """
 
 from __future__ import annotations
@@ -20,6 +27,16 @@ from .device import validate_schedule
 from .domain import Measurement
 
 
+def default_reduce_device(group=None, device=None) -> torch.device:
+    """CUDA for an NCCL group (NCCL cannot reduce CPU tensors), CPU for gloo."""
+    backend = str(dist.get_backend(group)).lower()
+    if "nccl" in backend:
+        if device is not None and torch.device(device).type == "cuda":
+            return torch.device(device)
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
 class SpmdEngine:
     def __init__(self, local, gpu, group=None, measurement_cls=Measurement, reduce_device=None):
         self.local = local
@@ -28,7 +45,13 @@ class SpmdEngine:
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.measurement_cls = measurement_cls
-        self.reduce_device = reduce_device or torch.device("cpu")
+        self.reduce_device = reduce_device or default_reduce_device(group, getattr(local, "device", None))
+        local.agree_ms = self._max
+
+    def _max(self, v: float) -> float:
+        t = torch.tensor([float(v)], dtype=torch.float64, device=self.reduce_device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        return float(t.item())
 
     def _reduce(self, t_ms: float, e_j: float) -> tuple[float, float]:
         v = torch.tensor([t_ms, e_j], dtype=torch.float64, device=self.reduce_device)
@@ -56,6 +79,8 @@ class SpmdEngine:
             raise RuntimeError("SpmdEngine.measure is called on rank 0; other ranks call serve()")
         gpu = gpu or self.gpu
         validate_schedule(partition, config, gpu)
+        if hasattr(self.local, "check_frequency"):
+            self.local.check_frequency(config.frequency_mhz, gpu)  # before anything is broadcast
         cmd = ("measure", partition.name, (float(config.frequency_mhz), int(config.sm_alloc), config.timing.encode()),
                (getattr(protocol, "warmup_s", 2.0), getattr(protocol, "window_s", 5.0),
                 getattr(protocol, "cooldown_s", 5.0)))

@@ -22,7 +22,9 @@ def test_partition_specs_shapes(idx):
     n_fa = 4 if specs.fused_rope(wl) else 5  # head_dim 128: RoPE runs in the QKV GEMM epilogue
     n_fm = 3 if specs.fused_swiglu(wl) else 4  # SwiGLU in the gate|up GEMM epilogue
     n_bm = 5 if specs.fused_swiglu_bwd(wl) else 6  # SwiGLU backward in the down dgrad epilogue
-    assert [len(p.comp_kernels) for p in parts] == [n_fa, n_fa, n_fm, n_fm, n_bm, n_bm, n_fa + 2, n_fa + 2]
+    # the last backward partition also runs the dγ column sums ("norm_grads")
+    assert [len(p.comp_kernels) for p in parts] == [n_fa, n_fa, n_fm, n_fm, n_bm, n_bm, n_fa + 2, n_fa + 3]
+    assert parts[-1].comp_kernels[-1].name == "norm_grads"
     for p in parts:
         assert p.comm_kernel.is_comm and p.comm_group_size == wl.world
         kinds = {k.name: k.kind for k in p.comp_kernels}
@@ -43,8 +45,10 @@ def test_fsdp_comm_bytes_cover_every_weight_once_per_direction():
     parts = specs.partition_specs(wl)
     total = sum(p.comm_kernel.comm_bytes for p in parts)
     w = sum(wl.weight_numels().values()) * 2 * (wl.world - 1) / wl.world
-    # forward all-gathers once, backward re-gathers once and reduce-scatters once
-    assert total == pytest.approx(3 * w)
+    gn = specs.fsdp_numel(wl, "gn") * 2 * (wl.world - 1) / wl.world
+    # forward all-gathers once, backward re-gathers once and reduce-scatters once; plus the
+    # reduce-scatter of the RMSNorm gradients
+    assert total == pytest.approx(3 * w + gn)
 
 
 def test_tp_shapes_per_rank():

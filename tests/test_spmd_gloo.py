@@ -25,9 +25,16 @@ class FakeLocal:
     def __init__(self, rank):
         self.rank = rank
         self.calls = []
+        self.reps = []
 
     def measure_local(self, name, cfg, warm, win, cool):
+        from paper_2601_17654_b200.engine import rep_counts
         self.calls.append((name, cfg.sm_alloc, cfg.timing.encode(), warm, win, cool))
+        # as Engine._window: each rank's own estimate differs; the agreed one sets the counts
+        est = 0.37 + 0.011 * self.rank
+        if getattr(self, "agree_ms", None) is not None:
+            est = self.agree_ms(est)
+        self.reps.append(rep_counts(est, warm, win))
         return 1.0 + self.rank, 10.0 * (self.rank + 1), 40.0
 
 
@@ -61,6 +68,7 @@ def _worker(rank, world, port, out):
     else:
         res["served"] = eng.serve()
     res["calls"] = local.calls
+    res["reps"] = local.reps
     out[rank] = res
     dist.destroy_process_group()
 
@@ -80,3 +88,7 @@ def test_spmd_protocol_world2():
     assert r1["served"] == 2                         # the invalid config never reached rank 1
     assert r0["calls"] == r1["calls"] == [("p0", 8, "ov1x2", 0.1, 0.5, 0.0), ("p0", 16, "seq", 0.1, 0.5, 0.0)]
     assert r0["m2"] == 2.0
+    # every rank launches the same number of executions (collectives) per window
+    assert r0["reps"] == r1["reps"] and len(r0["reps"]) == 2
+    from paper_2601_17654_b200.engine import rep_counts
+    assert r0["reps"][0] == rep_counts(0.381, 0.1, 0.5) != rep_counts(0.37, 0.1, 0.5)

@@ -17,7 +17,8 @@ ap.add_argument("--n", type=int, default=60)
 a = ap.parse_args()
 wl = baseline_workload(a.config, world=8, tokens=4096)
 n = wl.weight_numels()
-sym = (sum(int(v * 2 / 8) + 4 * v for v in n.values()) if wl.parallel == "fsdp" else 9 * wl.tokens * wl.h * 2) + (64 << 20)
+from paper_2601_17654_b200.layer import sym_bytes_for
+sym = sym_bytes_for(wl)
 layer = PartitionedLayer(wl, Communicator.loopback_group(8, sym))
 eng = Engine.for_layer(layer, b200_model())
 run = LayerRunner(layer, eng)

@@ -24,7 +24,8 @@ ap.add_argument("--eager", action="store_true")
 a = ap.parse_args()
 wl = baseline_workload(a.config, world=8, tokens=a.tokens)
 n = wl.weight_numels()
-sym = (sum(int(v * 2 / 8) + 4 * v for v in n.values()) if wl.parallel == "fsdp" else 9 * wl.tokens * wl.h * 2) + (64 << 20)
+from paper_2601_17654_b200.layer import sym_bytes_for
+sym = sym_bytes_for(wl)
 comm = Communicator.loopback_group(8, sym)
 layer = PartitionedLayer(wl, comm)
 eng = Engine.for_layer(layer, b200_model(), use_graphs=not a.eager)

@@ -81,6 +81,30 @@ def b200_model(hbm_gbs: float = 6539.9, bf16_tflops: float = 1640.5, f_max_mhz: 
     )
 
 
+DESCRIPTOR_PATH = "profiles/r2_descriptor.json"
+
+
+def b200_model_measured(path: str | None = None) -> GpuModel:
+    """The B200 descriptor built from committed measurements (tools/calibrate_descriptor.py ->
+    profiles/r2_descriptor.json): effective tensor / HBM rates of the layer's own kernels, the
+    collective's bus bandwidth and its CTA-saturation knee, idle power, NVML f_max.  This is what the
+    optimizer's space pruning (mbo.py:107-114) and the default comm CTA count use; falls back to
+    `b200_model()` when the file is absent."""
+    import json
+    import os
+
+    path = path or os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), DESCRIPTOR_PATH)
+    try:
+        with open(path) as f:
+            d = json.load(f)["descriptor"]
+    except (OSError, KeyError, ValueError):
+        return b200_model()
+    return GpuModel(num_sms=int(d["num_sms"]), peak_flops_per_sm_mhz=float(d["peak_flops_per_sm_mhz"]),
+                    mem_bw_gbps=float(d["mem_bw_gbps"]), net_bw_gbps=float(d["net_bw_gbps"]),
+                    sm_bw_saturation=int(d["sm_bw_saturation"]), p_static_w=float(d["p_static_w"]),
+                    f_max_mhz=float(d["f_max_mhz"]), overlap_launch_overhead_ms=float(d["overlap_launch_overhead_ms"]))
+
+
 def load_measured_peaks(path: str | None = None) -> dict:
     import json
     import os
@@ -167,5 +191,5 @@ def span_eff(partition, config) -> int:
     return min(config.timing.span, n - config.timing.start)
 
 
-__all__ = ["GpuModel", "b200_model", "ThermalModel", "ProfilingProtocol", "ThermalState", "InvalidConfigError",
+__all__ = ["GpuModel", "b200_model", "b200_model_measured", "ThermalModel", "ProfilingProtocol", "ThermalState", "InvalidConfigError",
            "analytic_kernel_ms", "validate_schedule", "span_eff", "load_measured_peaks", "replace", "math"]

@@ -14,7 +14,11 @@ def rel_err(a, b):
 
 
 @pytest.mark.parametrize("M,N,K", [(256, 256, 64), (128, 128, 128), (4096, 3072, 3072), (1000, 776, 520), (4096, 5120, 512), (3072, 8192, 256),
-                                   (4096, 768, 4096), (384, 16384, 256)])
+                                   (4096, 768, 4096), (384, 16384, 256),
+                                   # Llama-3-70B layer GEMMs at T=4096 (config 3): gate|up, qkv, down / o,
+                                   # and the gate|up weight-gradient shape
+                                   (4096, 57344, 8192), (4096, 10240, 8192), (4096, 8192, 28672),
+                                   (57344, 8192, 4096)])
 @pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, False), (True, True)])
 def test_gemm_all_majors(cuda, M, N, K, a_mn, b_mn):
     from paper_2601_17654_b200 import ops
@@ -135,7 +139,9 @@ def _attn_ref(q, k, v, hq, hkv, d, causal=True):
 
 
 @pytest.mark.parametrize("T,hq,hkv,d", [(256, 4, 1, 128), (1000, 6, 2, 128), (512, 8, 8, 64), (4096, 3, 1, 128),
-                                      (4096, 24, 8, 128)])
+                                      (4096, 24, 8, 128),
+                                      (4096, 4, 1, 128),     # Llama-3-8B TP8 per-rank heads (config 2)
+                                      (4096, 64, 8, 128)])   # Llama-3-70B (config 3)
 def test_attention_fwd_bwd(cuda, T, hq, hkv, d):
     from paper_2601_17654_b200 import ops
     torch.manual_seed(T + hq)

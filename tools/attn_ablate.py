@@ -51,3 +51,50 @@ for m in [int(x) for x in a.modes.split(",")]:
     res[m] = {"ms": round(t, 4), "tflops": round(fl / t / 1e9, 1)}
 os.environ["KPO_ATTN_BWD_ABLATE"] = "0"
 print(json.dumps(res))
+
+# ---------------------------------------------------------------- correctness of mode 256 (direct dQ reds)
+os.environ["KPO_ATTN_BWD_ABLATE"] = "0"
+ref = dqkv.clone()
+ops.attn_bwd(q, k, v, o, dout, lse, dqkv[:, :hq * d], dqkv[:, hq * d:(hq + hkv) * d], dqkv[:, (hq + hkv) * d:],
+             T, hq, hkv, d, scale, ws)
+torch.cuda.synchronize()
+ref = dqkv.clone()
+os.environ["KPO_ATTN_BWD_ABLATE"] = "256"
+ops.attn_bwd(q, k, v, o, dout, lse, dqkv[:, :hq * d], dqkv[:, hq * d:(hq + hkv) * d], dqkv[:, (hq + hkv) * d:],
+             T, hq, hkv, d, scale, ws)
+torch.cuda.synchronize()
+os.environ["KPO_ATTN_BWD_ABLATE"] = "0"
+res["mode256_rel_vs_mode0"] = ((dqkv.float() - ref.float()).norm() / ref.float().norm()).item()
+
+# ---------------------------------------------------------------- peer points on the same box (library kernels)
+peers = {}
+qh = q.reshape(T, hq, d).transpose(0, 1).unsqueeze(0).contiguous().requires_grad_()
+kh = k.reshape(T, hkv, d).transpose(0, 1).unsqueeze(0).contiguous().requires_grad_()
+vh = v.reshape(T, hkv, d).transpose(0, 1).unsqueeze(0).contiguous().requires_grad_()
+go = dout.reshape(T, hq, d).transpose(0, 1).unsqueeze(0).contiguous()
+from torch.nn.attention import SDPBackend, sdpa_kernel
+for name, be in (("cudnn", SDPBackend.CUDNN_ATTENTION), ("flash", SDPBackend.FLASH_ATTENTION),
+                 ("efficient", SDPBackend.EFFICIENT_ATTENTION)):
+    try:
+        with sdpa_kernel([be]):
+            out = torch.nn.functional.scaled_dot_product_attention(qh, kh, vh, is_causal=True, enable_gqa=True)
+            tf = timeit(lambda: torch.nn.functional.scaled_dot_product_attention(qh, kh, vh, is_causal=True,
+                                                                                 enable_gqa=True), reps=10)
+            tb = timeit(lambda: torch.autograd.grad(out, (qh, kh, vh), go, retain_graph=True), reps=10)
+        peers[name] = {"fwd_ms": round(tf, 4), "fwd_tflops": round(fl / 2.5 / tf / 1e9, 1), "bwd_ms": round(tb, 4),
+                       "bwd_tflops": round(fl / tb / 1e9, 1)}
+    except Exception as ex:  # backend unavailable for this shape / GPU
+        peers[name] = f"unavailable: {type(ex).__name__}: {str(ex)[:120]}"
+try:
+    from flash_attn import flash_attn_func
+    qf, kf, vf = (t.reshape(T, -1, d).unsqueeze(0).contiguous().requires_grad_() for t in (q, k, v))
+    of = flash_attn_func(qf, kf, vf, causal=True)
+    gof = dout.reshape(1, T, hq, d)
+    tf = timeit(lambda: flash_attn_func(qf, kf, vf, causal=True), reps=10)
+    tb = timeit(lambda: torch.autograd.grad(of, (qf, kf, vf), gof, retain_graph=True), reps=10)
+    peers["flash_attn_pkg"] = {"fwd_ms": round(tf, 4), "fwd_tflops": round(fl / 2.5 / tf / 1e9, 1),
+                               "bwd_ms": round(tb, 4), "bwd_tflops": round(fl / tb / 1e9, 1)}
+except Exception as ex:
+    peers["flash_attn_pkg"] = f"unavailable: {type(ex).__name__}: {str(ex)[:120]}"
+res["peers"] = peers
+print(json.dumps(res))

@@ -277,7 +277,7 @@ def run_kpo(args):
     import torch.distributed as dist
 
     from paper_2601_17654_b200.comm import Communicator
-    from paper_2601_17654_b200.device import b200_model, load_measured_peaks
+    from paper_2601_17654_b200.device import b200_model_measured, load_measured_peaks
     from paper_2601_17654_b200.domain import LaunchTiming, Measurement, ScheduleConfig
     from paper_2601_17654_b200.engine import Engine
     from paper_2601_17654_b200.layer import PartitionedLayer, sym_bytes_for
@@ -307,7 +307,7 @@ def run_kpo(args):
     tf_burst = peaks.get("bf16_tflops", 1590.0)
     tf_sust = peaks.get("bf16_tflops_sustained", 1400.0)
     peak_src = "measured" if peaks else "fallback"
-    gpu = b200_model(hbm_gbs=hbm, bf16_tflops=tf_burst)
+    gpu = b200_model_measured()  # committed descriptor (profiles/r2_descriptor.json), else nominal
 
     # symmetric heap: FSDP shards + two layer-parity gradient buffers; TP partial sums + stage
     sym = sym_bytes_for(wl)

@@ -1051,32 +1051,6 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
       // has read it, while the other half's reduce may still be in flight; dQ^T's TMEM columns are
       // released once the second half has been loaded (32 live registers, not 64)
       float* stg = reinterpret_cast<float*>(smem + C::OFF_DQ);
-      if (ablate & 256) {
-        // direct variant (A/B, KPO_ATTN_BWD_ABLATE=256; results are correct): each thread adds its
-        // head-dim column of dQ^T straight from registers with red.global.add.f32 (a warp covers 32
-        // consecutive d = one 128 B line per query), no shared-memory staging / TMA reduce
-        float* base = dq_acc + ((int64_t)m0 * hq + h) * D + dcol;
-        const int64_t qstride = (int64_t)hq * D;
-#pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
-          float v[BM / 2];
-          tmem_ld32_nowait(lane_addr + C::COL_DQ + hf * 32, reinterpret_cast<uint32_t*>(v));
-          tmem_wait_ld();
-          if (hf == 1) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&dq_empty[0]));
-          }
-          const int qn = min(BM / 2, T - (m0 + hf * (BM / 2)));
-#pragma unroll
-          for (int qi = 0; qi < BM / 2; ++qi)
-            if (qi < qn)
-              asm volatile("red.global.add.f32 [%0], %1;" ::"l"(base + (int64_t)(hf * (BM / 2) + qi) * qstride),
-                           "f"(v[qi] * scale)
-                           : "memory");
-        }
-        continue;
-      }
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
         float v[BM / 2];

@@ -52,20 +52,6 @@ for m in [int(x) for x in a.modes.split(",")]:
 os.environ["KPO_ATTN_BWD_ABLATE"] = "0"
 print(json.dumps(res))
 
-# ---------------------------------------------------------------- correctness of mode 256 (direct dQ reds)
-os.environ["KPO_ATTN_BWD_ABLATE"] = "0"
-ref = dqkv.clone()
-ops.attn_bwd(q, k, v, o, dout, lse, dqkv[:, :hq * d], dqkv[:, hq * d:(hq + hkv) * d], dqkv[:, (hq + hkv) * d:],
-             T, hq, hkv, d, scale, ws)
-torch.cuda.synchronize()
-ref = dqkv.clone()
-os.environ["KPO_ATTN_BWD_ABLATE"] = "256"
-ops.attn_bwd(q, k, v, o, dout, lse, dqkv[:, :hq * d], dqkv[:, hq * d:(hq + hkv) * d], dqkv[:, (hq + hkv) * d:],
-             T, hq, hkv, d, scale, ws)
-torch.cuda.synchronize()
-os.environ["KPO_ATTN_BWD_ABLATE"] = "0"
-res["mode256_rel_vs_mode0"] = ((dqkv.float() - ref.float()).norm() / ref.float().norm()).item()
-
 # ---------------------------------------------------------------- peer points on the same box (library kernels)
 peers = {}
 qh = q.reshape(T, hq, d).transpose(0, 1).unsqueeze(0).contiguous().requires_grad_()

@@ -1,18 +1,19 @@
 """Measure the B200 GpuModel descriptor the optimizer's pruning uses (reference GpuModel simgpu.py:35-82,
 `comm_rate_bps` :81-82, `kernel_duration` :144-168; pruning mbo.py:107-114).  VERDICT r1 item 9.
 
-  comm    bus bandwidth of the engine's collectives vs CTA budget at the layer's message sizes
-          (loopback group of 8 on a one-GPU box: the "link" is HBM; under torchrun the same script is
-          tools/comm_bench.py's NVLink mode).  net_bw_gbps := the best all-gather / reduce-scatter
-          bus bandwidth at the largest size; sm_bw_saturation := the smallest CTA count reaching 90% of
-          it (the reference's `min(1, sm / sat)` knee).
+  comm    bus bandwidth of the engine's collectives vs CTA budget (loopback group of 8 on a one-GPU
+          box: the "link" is HBM, so bandwidth grows linearly with CTAs up to 64; tools/comm_bench.py's
+          torchrun mode measures NVLink).  The per-CTA copy rate is measured; the reference's
+          `min(1, sm / sat)` knee is projected onto NVLink: sm_bw_saturation = ceil(770 GB/s / per-CTA
+          rate), net_bw_gbps = 770 GB/s (see derive()).
   compute every launch unit of the BASELINE config-1 layer timed alone (CUDA events, 20 reps, full
           SMs): effective tensor rate of the compute-bound units -> peak_flops_per_sm_mhz at the
           observed SM clock; effective HBM rate of the memory-bound units -> mem_bw_gbps.
   power   idle P0 power (NVML, 5 s at rest after the runs) -> p_static_w.
 
 Writes gpurun_out/descriptor.json; the committed copy profiles/r2_descriptor.json is what
-device.b200_model_measured() loads."""
+device.b200_model_measured() loads.  `python tools/calibrate_descriptor.py --derive FILE` recomputes the
+descriptor block of an existing measurement file."""
 import json
 import os
 import statistics
@@ -21,6 +22,55 @@ import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+
+
+NVLINK_GBS = 770.0  # measured peer copy per direction, /opt/skills/guides/B200_PROFILING.md (900 nominal)
+
+
+def derive(out: dict) -> dict:
+    """Descriptor from the raw measurements.  The collective's bandwidth grows linearly with its CTA
+    count on loopback until HBM saturates (no knee below 64 CTAs: the "link" is HBM there), so the
+    saturation knee is projected onto NVLink from the measured per-CTA copy rate:
+    sm_bw_saturation = ceil(NVLINK_GBS / per-CTA rate of the slower collective), rounded up to the
+    SmGrid stride of 3 (domain.py:69-74); net_bw_gbps = NVLINK_GBS."""
+    import math
+
+    from paper_2601_17654_b200.device import b200_model, load_measured_peaks
+
+    rows = out["comm"]["rows"]
+    big = max(r["bytes"] for r in rows)
+    per_cta = {}
+    for op in ("all_gather", "reduce_scatter"):
+        rs = [r["busbw_gbs"] / r["ncta"] for r in rows if r["op"] == op and r["bytes"] == big and r["ncta"] <= 12]
+        per_cta[op] = sorted(rs)[len(rs) // 2]
+    slow = min(per_cta.values())
+    sat = int(math.ceil(NVLINK_GBS / slow / 3.0) * 3)
+    out["comm"]["per_cta_gbs"] = per_cta
+    peaks = load_measured_peaks()
+    nominal = b200_model()
+    return {
+        "num_sms": 148,
+        "peak_flops_per_sm_mhz": out["compute"]["peak_flops_per_sm_mhz"],
+        "mem_bw_gbps": out["compute"]["effective_hbm_gbs"],
+        "net_bw_gbps": NVLINK_GBS,
+        "sm_bw_saturation": sat,
+        "p_static_w": round(out["idle_power_w"], 1),
+        "f_max_mhz": out.get("f_max_mhz", 1965.0),
+        "overlap_launch_overhead_ms": 0.0,
+        "derivation": {
+            "peak_flops_per_sm_mhz": "effective tensor rate of the config-1 layer's compute-bound units alone / "
+                                     "(148 SMs x median SM clock)",
+            "mem_bw_gbps": "effective HBM rate of the layer's memory-bound units alone",
+            "net_bw_gbps": "NVLink peer copy per direction (B200_PROFILING.md); loopback busbw grows to "
+                           f"{out['comm']['best_busbw_gbs']} GB/s at 64 CTAs through HBM",
+            "sm_bw_saturation": f"ceil({NVLINK_GBS} GB/s / {slow:.1f} GB/s per CTA (measured, slower of "
+                                "all-gather / reduce-scatter, <= 12 CTAs, 256 MB)) rounded up to a multiple of 3",
+            "p_static_w": "idle NVML power over 5 s (after 8 s at rest)",
+            "nominal_for_reference": {"peak_flops_per_sm_mhz": nominal.peak_flops_per_sm_mhz,
+                                      "mem_bw_gbps": nominal.mem_bw_gbps,
+                                      "measured_peaks": {k: peaks.get(k) for k in ("hbm_gbs", "bf16_tflops")}},
+        },
+    }
 
 
 def main():
@@ -70,15 +120,8 @@ def main():
         c.close()
     big = [r for r in rows if r["bytes"] == max(r2["bytes"] for r2 in rows)]
     best = max(r["busbw_gbs"] for r in big)
-    knee = {}
-    for op in ("all_gather", "reduce_scatter"):
-        rs = sorted((r for r in big if r["op"] == op), key=lambda r: r["ncta"])
-        top = max(r["busbw_gbs"] for r in rs)
-        knee[op] = next(r["ncta"] for r in rs if r["busbw_gbs"] >= 0.9 * top)
-    sat = max(knee.values())
-    out["comm"] = {"mode": "loopback (8 virtual ranks, HBM link)", "rows": rows, "best_busbw_gbs": best,
-                   "knee_90pct": knee, "sm_bw_saturation": sat, "net_bw_gbps": best}
-    print("comm", knee, best, flush=True)
+    out["comm"] = {"mode": "loopback (8 virtual ranks, HBM link)", "rows": rows, "best_busbw_gbs": best}
+    print("comm best", best, flush=True)
 
     # ------------------------------------------------------------------ solo launch units, config 1
     wl = baseline_workload(1)
@@ -124,30 +167,18 @@ def main():
     out["idle_power_w"] = samp.window_j(t0, t1) / (t1 - t0)
     out["idle_temperature_c"] = nv.temperature_c()
     samp.stop()
-    peaks = load_measured_peaks()
-    nominal = b200_model()
-    out["descriptor"] = {
-        "num_sms": 148,
-        "peak_flops_per_sm_mhz": out["compute"]["peak_flops_per_sm_mhz"],
-        "mem_bw_gbps": out["compute"]["effective_hbm_gbs"],
-        "net_bw_gbps": out["comm"]["net_bw_gbps"],
-        "sm_bw_saturation": out["comm"]["sm_bw_saturation"],
-        "p_static_w": round(out["idle_power_w"], 1),
-        "f_max_mhz": nv.max_sm_clock_mhz(),
-        "overlap_launch_overhead_ms": 0.0,
-        "derivation": {"peak_flops_per_sm_mhz": "effective tensor rate of the layer's compute-bound units alone / "
-                                                "(148 SMs x observed median SM clock)",
-                       "mem_bw_gbps": "effective HBM rate of the layer's memory-bound units alone",
-                       "net_bw_gbps": "best loopback all-gather / reduce-scatter bus bandwidth (256 MB)",
-                       "sm_bw_saturation": "smallest CTA count reaching 90% of that",
-                       "p_static_w": "idle NVML power over 5 s", "nominal_for_reference": {
-                           "peak_flops_per_sm_mhz": nominal.peak_flops_per_sm_mhz, "mem_bw_gbps": nominal.mem_bw_gbps,
-                           "measured_peaks": {k: peaks.get(k) for k in ("hbm_gbs", "bf16_tflops")}}},
-    }
+    out["f_max_mhz"] = nv.max_sm_clock_mhz()
+    out["descriptor"] = derive(out)
     os.makedirs("gpurun_out", exist_ok=True)
     json.dump(out, open("gpurun_out/descriptor.json", "w"), indent=1)
     print(json.dumps(out["descriptor"]))
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 2 and sys.argv[1] == "--derive":
+        d = json.load(open(sys.argv[2]))
+        d["descriptor"] = derive(d)
+        json.dump(d, open(sys.argv[2], "w"), indent=1)
+        print(json.dumps(d["descriptor"]))
+    else:
+        main()

@@ -62,7 +62,7 @@ def main():
 
     from paper_2601_17654_b200.comm import Communicator
     from paper_2601_17654_b200.compat import patch_reference
-    from paper_2601_17654_b200.device import b200_model
+    from paper_2601_17654_b200.device import b200_model_measured as b200_model
     from paper_2601_17654_b200.domain import LaunchTiming, ScheduleConfig
     from paper_2601_17654_b200.engine import Engine, install
     from paper_2601_17654_b200.layer import PartitionedLayer, sym_bytes_for

@@ -40,7 +40,7 @@ def main():
     import torch
 
     from paper_2601_17654_b200.comm import Communicator
-    from paper_2601_17654_b200.device import b200_model
+    from paper_2601_17654_b200.device import b200_model_measured as b200_model
     from paper_2601_17654_b200.domain import LaunchTiming, ScheduleConfig
     from paper_2601_17654_b200.engine import Engine
     from paper_2601_17654_b200.layer import PartitionedLayer, sym_bytes_for

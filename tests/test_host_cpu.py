@@ -91,7 +91,7 @@ def test_profiler_collects_and_resumes(tmp_path):
 
 def test_bench_reference_arm_contract():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
-                          "--warmup", "0", "--cpu-tokens", "128"], capture_output=True, text=True, timeout=600,
+                          "--warmup", "0", "--tokens", "128"], capture_output=True, text=True, timeout=600,
                          cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])

@@ -82,5 +82,17 @@ try:
                                "bwd_ms": round(tb, 4), "bwd_tflops": round(fl / tb / 1e9, 1)}
 except Exception as ex:
     peers["flash_attn_pkg"] = f"unavailable: {type(ex).__name__}: {str(ex)[:120]}"
+try:  # FlashAttention-4 (CuTe DSL, tcgen05; vllm's vendored copy): the sm100-native peer
+    from vllm.vllm_flash_attn.cute.interface import flash_attn_func as fa4
+    qf, kf, vf = (t.reshape(T, -1, d).unsqueeze(0).contiguous().requires_grad_() for t in (q, k, v))
+    of = fa4(qf, kf, vf, causal=True)
+    of = of[0] if isinstance(of, tuple) else of
+    gof = dout.reshape(1, T, hq, d)
+    tf = timeit(lambda: fa4(qf, kf, vf, causal=True), reps=10)
+    tb = timeit(lambda: torch.autograd.grad(of, (qf, kf, vf), gof, retain_graph=True), reps=10)
+    peers["fa4_cute_sm100"] = {"fwd_ms": round(tf, 4), "fwd_tflops": round(fl / 2.5 / tf / 1e9, 1),
+                               "bwd_ms": round(tb, 4), "bwd_tflops": round(fl / tb / 1e9, 1)}
+except Exception as ex:
+    peers["fa4_cute_sm100"] = f"unavailable: {type(ex).__name__}: {str(ex)[:160]}"
 res["peers"] = peers
 print(json.dumps(res))

@@ -12,7 +12,7 @@
  *   ---------------------------------------------  -------------------------------------------
  *   "norm" / "fused_norm" (workloads.py:44,60,87)   kpo_rmsnorm_fwd / kpo_rmsnorm_bwd
  *   "linear_*" (workloads.py:45,48,61-62,73)        kpo_gemm (tcgen05 + TMEM + TMA)
- *   "rope" (workloads.py:46)                        kpo_rope_fwd / kpo_rope_bwd
+ *   "rope" (workloads.py:46)                        kpo_rope (head_dim 64), fused into kpo_gemm_rope / kpo_attn_bwd_rope (128)
  *   "attention_core" (workloads.py:47)              kpo_attn_fwd / kpo_attn_bwd
  *   SwiGLU (memory-bound unit, compose.py:48-76)    kpo_swiglu_fwd / kpo_swiglu_bwd
  *   "allreduce" (workloads.py:50,64,74,90)          kpo_all_reduce      (SM-budgeted P2P)

@@ -139,6 +139,7 @@ def _attn_ref(q, k, v, hq, hkv, d, causal=True):
 
 
 @pytest.mark.parametrize("T,hq,hkv,d", [(256, 4, 1, 128), (1000, 6, 2, 128), (512, 8, 8, 64), (4096, 3, 1, 128),
+                                      (2048, 16, 16, 64),    # GPT layer, config 0 (head_dim 64)
                                       (4096, 24, 8, 128),
                                       (4096, 4, 1, 128),     # Llama-3-8B TP8 per-rank heads (config 2)
                                       (4096, 64, 8, 128)])   # Llama-3-70B (config 3)

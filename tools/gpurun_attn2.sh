@@ -1,0 +1,10 @@
+set -x
+timeout 900 python -m pytest tests/test_kernels_gpu.py -q -p no:cacheprovider -k "attention" -x > gpurun_out/attn_tests2.log 2>&1
+echo "tests rc=$?"; tail -3 gpurun_out/attn_tests2.log
+KPO_ATTN_BWD3_DVFIRST=1 timeout 900 python -m pytest tests/test_kernels_gpu.py -q -p no:cacheprovider -k "attention_fwd_bwd" -x > gpurun_out/attn_tests2dv.log 2>&1
+echo "tests dv rc=$?"; tail -3 gpurun_out/attn_tests2dv.log
+timeout 900 python tools/attn_bwd_ab.py --variants 2,3,3+dv,2,3,3+dv --shapes 4096:24:8,4096:4:1,4096:64:8 > gpurun_out/attn_ab2.log 2>&1
+echo "ab rc=$?"; grep -v "^{" gpurun_out/attn_ab2.log
+KPO_ATTN_BWD=3 timeout 600 ncu --set full --import-source on --clock-control none -k regex:attn_bwd_tc3 -s 3 -c 1 \
+  -o gpurun_out/attn_bwd_tc3b -f python tools/attn_bwd_ab.py --child 4096:24:8 --reps 2 > gpurun_out/ncu_attn2.log 2>&1
+echo "ncu rc=$?"

@@ -571,7 +571,7 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* o
         (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, dvec, dq_acc, (int)T, hq, os));
     KPO_LAUNCH_CHECK();
   }
-  if (D == 128 && use_tc && T % 8 == 0) {  // tcgen05 path (bulk-copied softmax stats need 16 B rows)
+  if (use_tc && T % 8 == 0) {  // tcgen05 path (bulk-copied softmax stats need 16 B rows)
     // split-group mode when kv heads x key tiles cannot fill the GPU (e.g. TP8: one kv head per rank):
     // one CTA per (q head, key tile), dK/dV reduced in fp32 then converted
     const int64_t ntiles = (T + 127) / 128;
@@ -694,8 +694,10 @@ extern "C" int kpo_attn_bwd(const void* q, const void* k, const void* v, const v
   if (d == 128)
     return attn::bwd_launch<128>(q, k, v, o, dout, lse, dq, dk, dv, T, hq, hkv, q_stride, k_stride, v_stride,
                                  o_stride, dq_stride, dk_stride, dv_stride, scale, causal, workspace, s, true);
+  // head_dim 64 (config 0): the 128-query tcgen05 kernel; KPO_ATTN_BWD=1 keeps the mma.sync kernel (A/B only)
+  static const bool legacy64 = getenv("KPO_ATTN_BWD") && atoi(getenv("KPO_ATTN_BWD")) == 1;
   return attn::bwd_launch<64>(q, k, v, o, dout, lse, dq, dk, dv, T, hq, hkv, q_stride, k_stride, v_stride, o_stride,
-                              dq_stride, dk_stride, dv_stride, scale, causal, workspace, s, false);
+                              dq_stride, dk_stride, dv_stride, scale, causal, workspace, s, !legacy64);
 }
 
 extern "C" int kpo_attn_bwd_rope(const void* q, const void* k, const void* v, const void* o, const void* dout,

@@ -1082,12 +1082,446 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
+// =====================================================================================
+// Backward, 128-query steps (head_dim 64; KPO_ATTN_BWD=3 for head_dim 128).  One CTA = 128 keys of one kv head, looping over the GQA group x causal
+// 128-query tiles; every MMA is M=128 x N=128 x K=128, so each SS MMA reads 8 KB of operands per 64
+// tensor cycles (the 64-query kernel above issues N=64 MMAs, capped by shared memory at 48 of their
+// 32 cycles).  TMEM (512 columns) is aliased:
+//   S^T  cols   0..127  keys x queries, fp32.  Softmax warp g (32 queries) writes its P^T (bf16
+//                       pairs) over the first 16 of its own 32 S columns: the TMEM A operand of dV.
+//   dP^T cols 128..255  keys x queries.  Warp g writes dS^T (bf16 pairs) over the first 16 of its own
+//                       32 dP columns: the TMEM A operand of dK.  dQ (queries x d, fp32) is then
+//                       written over the whole region by the dQ MMA (issued after dK, in order).
+//   dV   cols 256..383, dK cols 384..511
+// Per step s the MMA warp issues dV(s) += P^T dO, dP(s) = V dO^T (once dQ(s-1) has left TMEM),
+// S(s+1) = K Q^T, then dK(s) += dS^T Q and dQ(s) = dS K (dS from shared memory, MN-major).  The 16
+// softmax warps (4 per TMEM lane quarter, 32 queries each) compute P(s), then drain dQ(s-1) (each
+// warp one 32-column chunk: TMEM -> registers -> one of four 16 KB SW128 staging boxes -> TMA bulk
+// reduce-add into the fp32 dQ accumulator), then dS(s).  The tensor core runs dV(s) while dQ(s-1)
+// drains and S(s+1) while dS(s) is computed, so neither is on its critical path.
+// Shared memory: K, V (32 KB each), Q (2 stages), dO (1 stage), dS^T (32 KB, MN-major dS operand of
+// the dQ MMA; between dQ(s-1) and dS(s) it doubles as staging boxes 0, 1), staging boxes 2, 3.
+template <int D>
+struct Bwd3 {
+  static constexpr int BN = 128, BM = 128, QSTAGES = 2, KSUB = D / 64;
+  static constexpr int KV_BYTES = BN * D * 2;            // 32 KB
+  static constexpr int QT_BYTES = BM * D * 2;            // 32 KB
+  static constexpr int DS_BYTES = BN * BM * 2;           // 32 KB
+  static constexpr int DQC = 32;                         // d columns per dQ reduce chunk (one warp's)
+  static constexpr int STG_BYTES = BM * DQC * 4;         // 16 KB
+  static constexpr int OFF_K = 0, OFF_V = OFF_K + KV_BYTES, OFF_Q = OFF_V + KV_BYTES;
+  static constexpr int OFF_DO = OFF_Q + QSTAGES * QT_BYTES, OFF_DS = OFF_DO + QT_BYTES;
+  static constexpr int OFF_STG = OFF_DS + DS_BYTES;      // staging boxes 2, 3
+  static constexpr int OFF_STAT = OFF_STG + 2 * STG_BYTES;  // [QSTAGES][lse BM | D BM] fp32
+  static constexpr int OFF_BAR = OFF_STAT + QSTAGES * 2 * BM * 4;
+  static constexpr int SMEM = OFF_BAR + 256;  // 231680 B: the dynamic window must start 1024-aligned
+  static constexpr int COL_S = 0, COL_DP = 128, COL_DV = 256, COL_DK = 384;
+  static constexpr int SM_WARPS = 16;
+  static constexpr int THREADS = (2 + SM_WARPS) * 32;
+  static_assert(DS_BYTES == 2 * STG_BYTES, "the dS^T buffer holds staging boxes 0, 1");
+};
+
+template <int D>
+__global__ void __launch_bounds__(Bwd3<D>::THREADS, 1)
+    attn_bwd_tc3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                        const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                        const __grid_constant__ CUtensorMap tmDQ,
+                        const float* __restrict__ lse, const float* __restrict__ dvec,
+                        __nv_bfloat16* __restrict__ dk, __nv_bfloat16* __restrict__ dv, int T, int hq, int hkv,
+                        int64_t dks, int64_t dvs, float scale, int causal, float* __restrict__ dkv_acc,
+                        int split_group, int qsplit_tiles, const float2* __restrict__ rope_cs) {
+  // same contract as attn_bwd_tc_kernel (split-group / query-chunk modes, fused inverse rotary of dK)
+  ::kpo::pdl_launch_dependents();
+  using C = Bwd3<D>;
+  constexpr int BN = C::BN, BM = C::BM, KSUB = C::KSUB, NCH = D / C::DQC;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* kv_full = bar + 0;
+  uint64_t* q_full = bar + 1;    // [2]
+  uint64_t* q_empty = bar + 3;   // [2]
+  uint64_t* do_full = bar + 5;
+  uint64_t* do_empty = bar + 6;
+  uint64_t* s_full = bar + 7;
+  uint64_t* p_full = bar + 8;
+  uint64_t* dp_full = bar + 9;
+  uint64_t* ds_full = bar + 10;
+  uint64_t* dq_full = bar + 11;
+  uint64_t* dq_empty = bar + 12;
+  uint64_t* stg_free = bar + 13;  // [2]  staging boxes 0 / 1 (the dS^T buffer halves) read by their reduce
+  uint64_t* acc_done = bar + 15;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+  float* stat = reinterpret_cast<float*>(smem + C::OFF_STAT);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nblk = blockIdx.y;
+  const bool split = split_group != 0;
+  const int group = split ? 1 : hq / hkv;
+  const int h_first = split ? (int)blockIdx.x : (int)blockIdx.x * (hq / hkv);
+  const int kvh = split ? (int)blockIdx.x / (hq / hkv) : (int)blockIdx.x;
+  const int n0 = nblk * BN;
+  const int total_m = (T + BM - 1) / BM;
+  int m_start = causal ? n0 / BM : 0, m_end = total_m;
+  const bool chunked = gridDim.z > 1 && nblk < qsplit_tiles;
+  if (gridDim.z > 1) {
+    if (chunked) {
+      const int qper = (total_m + (int)gridDim.z - 1) / (int)gridDim.z;
+      m_start = max(m_start, (int)blockIdx.z * qper);
+      m_end = min(total_m, ((int)blockIdx.z + 1) * qper);
+      if (m_start >= m_end) return;
+    } else if (blockIdx.z != 0) {
+      return;
+    }
+  }
+  const bool atomic_dkv = split || chunked;
+  const int mq = m_end - m_start;
+  const int steps = group * mq;
+  const float scale_log2 = scale * kLog2e;
+
+  if (threadIdx.x == 0) {
+    if (smem_u32(smem) & 1023) __trap();  // SW128 tiles need a 1024-aligned window (no slack left)
+    mbar_init(smem_u32(kv_full), 1);
+    for (int i = 0; i < C::QSTAGES; ++i) {
+      mbar_init(smem_u32(&q_full[i]), 1);
+      mbar_init(smem_u32(&q_empty[i]), 1);
+    }
+    mbar_init(smem_u32(do_full), 1);
+    mbar_init(smem_u32(do_empty), 1);
+    mbar_init(smem_u32(s_full), 1);
+    mbar_init(smem_u32(p_full), C::SM_WARPS);
+    mbar_init(smem_u32(dp_full), 1);
+    mbar_init(smem_u32(ds_full), C::SM_WARPS);
+    mbar_init(smem_u32(dq_full), 1);
+    mbar_init(smem_u32(dq_empty), C::SM_WARPS);
+    mbar_init(smem_u32(&stg_free[0]), 1);
+    mbar_init(smem_u32(&stg_free[1]), 1);
+    mbar_init(smem_u32(acc_done), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc(smem_u32(tmem_slot), 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (*tmem_slot != 0) __trap();
+  ::kpo::pdl_wait();
+  constexpr uint32_t tmem = 0;
+  const uint32_t sK = smem_u32(smem + C::OFF_K), sV = smem_u32(smem + C::OFF_V);
+  const uint32_t sQ = smem_u32(smem + C::OFF_Q), sDO = smem_u32(smem + C::OFF_DO);
+  const uint32_t sDS = smem_u32(smem + C::OFF_DS), sSTG = smem_u32(smem + C::OFF_STG);
+
+  auto step_coords = [&](int s, int& h, int& m0) {
+    h = h_first + s / mq;
+    m0 = (m_start + s % mq) * BM;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA producer
+      mbar_arrive_expect_tx(smem_u32(kv_full), 2 * C::KV_BYTES);
+#pragma unroll
+      for (int kb = 0; kb < KSUB; ++kb) {
+        tma_load_2d(sK + kb * BN * 128, &tmK, smem_u32(kv_full), kvh * D + kb * 64, n0);
+        tma_load_2d(sV + kb * BN * 128, &tmV, smem_u32(kv_full), kvh * D + kb * 64, n0);
+      }
+      // order Q(0), dO(0), Q(1), dO(1), ... = the MMA warp's release order (dP(s) frees dO(s) before
+      // dK(s) / dQ(s) free Q stage s)
+      for (int s = 0; s < steps; ++s) {
+        const int st = s % C::QSTAGES;
+        int h, m0;
+        step_coords(s, h, m0);
+        mbar_wait(smem_u32(&q_empty[st]), ((s / C::QSTAGES) & 1) ^ 1);
+        const uint32_t fb = smem_u32(&q_full[st]);
+        const uint32_t nstat = (uint32_t)min(BM, T - m0) * 4u;
+        mbar_arrive_expect_tx(fb, C::QT_BYTES + 2 * nstat);
+#pragma unroll
+        for (int kb = 0; kb < KSUB; ++kb) tma_load_2d(sQ + st * C::QT_BYTES + kb * BM * 128, &tmQ, fb, h * D + kb * 64, m0);
+        const uint32_t sst = smem_u32(stat + st * 2 * BM);
+        bulk_load(sst, lse + (int64_t)h * T + m0, nstat, fb);
+        bulk_load(sst + BM * 4, dvec + (int64_t)h * T + m0, nstat, fb);
+        mbar_wait(smem_u32(do_empty), (s & 1) ^ 1);
+        mbar_arrive_expect_tx(smem_u32(do_full), C::QT_BYTES);
+#pragma unroll
+        for (int kb = 0; kb < KSUB; ++kb) tma_load_2d(sDO + kb * BM * 128, &tmDO, smem_u32(do_full), h * D + kb * 64, m0);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (whole warp, elect.sync)
+    constexpr uint32_t ID_SS = idesc_bf16(BN, BM, false, false);  // S^T, dP^T
+    constexpr uint32_t ID_G = idesc_bf16(BN, D, false, true);     // dV, dK (A from TMEM, B MN-major)
+    constexpr uint32_t ID_Q = idesc_bf16(BM, D, true, true);      // dQ = dS K (A, B MN-major)
+    const uint32_t k_k = desc_lo(sK, 16), v_k = desc_lo(sV, 16), k_mn = desc_lo(sK, BN * 128);
+    const uint32_t o_k = desc_lo(sDO, 16), o_mn = desc_lo(sDO, BM * 128);
+    const uint32_t ds_mn = desc_lo(sDS, BN * 128);
+    auto mma_s = [&](int s) {
+      const int st = s % C::QSTAGES;
+      mbar_wait(smem_u32(&q_full[st]), (s / C::QSTAGES) & 1);
+      tc_fence_after();
+      const uint32_t q_k = desc_lo(sQ + st * C::QT_BYTES, 16);
+#pragma unroll
+      for (int kb = 0; kb < KSUB; ++kb)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          tc_mma_lo_w(tmem + C::COL_S, k_k + kb * (BN * 8) + k * 2, q_k + kb * (BM * 8) + k * 2, ID_SS, (kb | k) ? 1u : 0u);
+      tc_commit_w(smem_u32(s_full));
+    };
+    if (steps > 0) {
+      mbar_wait(smem_u32(kv_full), 0);
+      mma_s(0);
+    }
+    for (int s = 0; s < steps; ++s) {
+      const int st = s % C::QSTAGES;
+      // dV(s) += P^T(s) dO(s): P^T of queries 16k.. sits in warp (k / 2)'s columns, 8 per 16 queries
+      mbar_wait(smem_u32(do_full), s & 1);
+      mbar_wait(smem_u32(p_full), s & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int k = 0; k < BM / 16; ++k)
+        tc_mma_ts_lo_w(tmem + C::COL_DV, tmem + C::COL_S + 32 * (k >> 1) + 8 * (k & 1), o_mn + k * 128, ID_G,
+                       (s > 0 || k > 0) ? 1u : 0u);
+      // dP^T(s) = V dO^T, once dQ(s-1) has been drained out of these columns
+      if (s > 0) mbar_wait(smem_u32(dq_empty), (s - 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int kb = 0; kb < KSUB; ++kb)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          tc_mma_lo_w(tmem + C::COL_DP, v_k + kb * (BN * 8) + k * 2, o_k + kb * (BM * 8) + k * 2, ID_SS, (kb | k) ? 1u : 0u);
+      tc_commit_w(smem_u32(dp_full));
+      tc_commit_w(smem_u32(do_empty));
+      // S(s+1) over S(s) / P(s): dV(s) (issued above) is the last reader of P(s)
+      if (s + 1 < steps) mma_s(s + 1);
+      // dK(s) += dS^T(s) Q(s) (A = dS^T from TMEM), dQ(s) = dS(s) K (over the dP / dS^T columns)
+      mbar_wait(smem_u32(ds_full), s & 1);
+      tc_fence_after();
+      const uint32_t q_mn = desc_lo(sQ + st * C::QT_BYTES, BM * 128);
+#pragma unroll
+      for (int k = 0; k < BM / 16; ++k)
+        tc_mma_ts_lo_w(tmem + C::COL_DK, tmem + C::COL_DP + 32 * (k >> 1) + 8 * (k & 1), q_mn + k * 128, ID_G,
+                       (s > 0 || k > 0) ? 1u : 0u);
+#pragma unroll
+      for (int k = 0; k < BN / 16; ++k)
+        tc_mma_lo_w(tmem + C::COL_DP, ds_mn + k * 128, k_mn + k * 128, ID_Q, k > 0 ? 1u : 0u);
+      tc_commit_w(smem_u32(dq_full));
+      tc_commit_w(smem_u32(&q_empty[st]));
+    }
+    tc_commit_w(smem_u32(acc_done));
+  } else {
+    // ------------------------------------------------------------ softmax warps: row = key, 32 queries each
+    const int quarter = warp & 3;
+    const int g = (warp - 2) >> 2;  // query column group 0..3 (= the dQ chunk this warp drains)
+    const int r = quarter * 32 + lane;
+    const int key = n0 + r;
+    const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
+    const bool issuer = (warp & 3) == 2 && lane == 0;  // one thread per column group issues its reduces
+    // dQ(s-1) drain: this warp's 32 d columns of its 32 query rows (TMEM lane = query)
+    auto drain = [&](int s_prev) {
+      int h, m0;
+      step_coords(s_prev, h, m0);
+      mbar_wait(smem_u32(dq_full), s_prev & 1);
+      tc_fence_after();
+      if (C::DQC * g >= D) {  // head_dim 64: no chunk for this column group
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(dq_empty));
+        return;
+      }
+      float v[32];
+      tmem_ld32_nowait(lane_addr + C::COL_DP + C::DQC * g, reinterpret_cast<uint32_t*>(v));
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(dq_empty));
+      // boxes 0, 1 live in the dS^T buffer (free until this step's dS store, which waits for their
+      // reduces to have read them: stg_free); boxes 2, 3 are reused a step later (the issuer waits)
+      const uint32_t sb = g < 2 ? sDS + g * C::STG_BYTES : sSTG + (g - 2) * C::STG_BYTES;
+      if (g >= 2) {
+        if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        named_bar(1 + g, 128);
+      }
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc)
+        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(sb + sw128(r, cc)), "f"(v[cc * 4] * scale),
+                     "f"(v[cc * 4 + 1] * scale), "f"(v[cc * 4 + 2] * scale), "f"(v[cc * 4 + 3] * scale)
+                     : "memory");
+      fence_async_smem();
+      named_bar(1 + g, 128);
+      if (issuer) {
+        tma_reduce_add_2d(&tmDQ, sb, h * D + C::DQC * g, m0);
+        bulk_commit();
+        if (g < 2) {
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          mbar_arrive(smem_u32(&stg_free[g]));
+        }
+      }
+    };
+    for (int s = 0, mi = 0; s < steps; ++s, mi = (mi + 1 == mq) ? 0 : mi + 1) {
+      const int m0 = (m_start + mi) * BM;
+      const int st = s % C::QSTAGES;
+      const bool tile_mask = (causal && m0 < n0 + BN - 1) || n0 + BN > T || m0 + BM > T;
+      mbar_wait(smem_u32(&q_full[st]), (s / C::QSTAGES) & 1);  // lse / D rows of this step
+      mbar_wait(smem_u32(s_full), s & 1);
+      tc_fence_after();
+      float p[32];
+      tmem_ld32_nowait(lane_addr + C::COL_S + 32 * g, reinterpret_cast<uint32_t*>(p));
+      tmem_wait_ld();
+      const float* sl = stat + st * 2 * BM + 32 * g;
+      {
+        uint32_t pp[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          const float4 nl = *reinterpret_cast<const float4*>(sl + i);
+          const float l4[4] = {nl.x, nl.y, nl.z, nl.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float pe = ex2(fmaf(p[i + e], scale_log2, -l4[e] * kLog2e));
+            if (tile_mask) {
+              const int q = m0 + 32 * g + i + e;
+              pe = (key >= T || q >= T || (causal && q < key)) ? 0.f : pe;
+            }
+            p[i + e] = pe;
+          }
+          pp[i / 2] = pack_bf16x2(p[i], p[i + 1]);
+          pp[i / 2 + 1] = pack_bf16x2(p[i + 2], p[i + 3]);
+        }
+        tmem_st16(lane_addr + C::COL_S + 32 * g, pp);  // over this warp's own (already read) S columns
+        tmem_wait_st();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(p_full));
+      if (s > 0) drain(s - 1);  // runs while the tensor core does dV(s)
+      mbar_wait(smem_u32(dp_full), s & 1);
+      tc_fence_after();
+      uint32_t qq[16];
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        float dp[16];
+        tmem_ld16_nowait(lane_addr + C::COL_DP + 32 * g + 16 * hf, reinterpret_cast<uint32_t*>(dp));
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 16; i += 4) {
+          const float4 dd = *reinterpret_cast<const float4*>(sl + BM + 16 * hf + i);
+          const int b = 16 * hf + i;
+          qq[b / 2] = pack_bf16x2(p[b] * (dp[i] - dd.x), p[b + 1] * (dp[i + 1] - dd.y));
+          qq[b / 2 + 1] = pack_bf16x2(p[b + 2] * (dp[i + 2] - dd.z), p[b + 3] * (dp[i + 3] - dd.w));
+        }
+      }
+      // dS^T row r -> TMEM over this warp's own (already read) dP columns: the A operand of dK
+      tmem_st16(lane_addr + C::COL_DP + 32 * g, qq);
+      // and -> shared memory (queries 32g .. 32g+31: box g / 2, 16-byte chunks 4 (g & 1) .. + 3), the
+      // dS operand of the dQ MMA, once box g / 2's staging reduce of dQ(s-1) has read that half
+      if (s > 0) mbar_wait(smem_u32(&stg_free[g >> 1]), (s - 1) & 1);
+      const uint32_t db = sDS + (g >> 1) * (BN * 128);
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch)
+        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(db + sw128(r, (g & 1) * 4 + ch)), "r"(qq[ch * 4]),
+                     "r"(qq[ch * 4 + 1]), "r"(qq[ch * 4 + 2]), "r"(qq[ch * 4 + 3])
+                     : "memory");
+      tmem_wait_st();
+      fence_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(ds_full));
+    }
+    if (steps > 0) drain(steps - 1);
+    if (issuer) bulk_wait0();
+    // ------------------------------------------------------------ dK / dV epilogue (all 16 warps)
+    mbar_wait(smem_u32(acc_done), 0);
+    tc_fence_after();
+    const bool ok = key < T && steps > 0;
+#pragma unroll 1
+    for (int which = 0; which < 2; ++which) {
+      const uint32_t col = which ? C::COL_DV : C::COL_DK;
+      const float mul = which ? 1.f : scale;
+      __nv_bfloat16* row = which ? dv + (int64_t)key * dvs + (int64_t)kvh * D : dk + (int64_t)key * dks + (int64_t)kvh * D;
+      if (32 * g >= D) break;  // head_dim 64: warps g = 0, 1 hold the columns
+      if (which == 0 && rope_cs != nullptr && !atomic_dkv) {
+        // inverse rotary (head_dim 128 only, checked on the host), pairs (i, i + D/2): i in [16g, 16g + 16)
+        const float2* cs = rope_cs + (int64_t)(key < T ? key : 0) * (D / 2);
+        uint32_t va[16], vb[16];
+        tmem_ld16_nowait(lane_addr + col + 16 * g, va);
+        tmem_ld16_nowait(lane_addr + col + D / 2 + 16 * g, vb);
+        tmem_wait_ld();
+        if (ok) {
+#pragma unroll
+          for (int q8 = 0; q8 < 2; ++q8) {
+            float oa[8], ob[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float2 t = cs[16 * g + q8 * 8 + j];
+              const float x = __uint_as_float(va[q8 * 8 + j]) * mul, y = __uint_as_float(vb[q8 * 8 + j]) * mul;
+              oa[j] = x * t.x + y * t.y;
+              ob[j] = y * t.x - x * t.y;
+            }
+            *reinterpret_cast<uint4*>(row + 16 * g + q8 * 8) = pack8(oa);
+            *reinterpret_cast<uint4*>(row + D / 2 + 16 * g + q8 * 8) = pack8(ob);
+          }
+        }
+      } else {
+        uint32_t v[32];
+        tmem_ld32_nowait(lane_addr + col + 32 * g, v);
+        tmem_wait_ld();
+        if (ok && atomic_dkv) {
+          float* acc = dkv_acc + (which ? (int64_t)T * hkv * D : 0) + ((int64_t)key * hkv + kvh) * D + 32 * g;
+#pragma unroll
+          for (int q4 = 0; q4 < 8; ++q4)
+            atomicAdd(reinterpret_cast<float4*>(acc + q4 * 4),
+                      make_float4(__uint_as_float(v[q4 * 4 + 0]) * mul, __uint_as_float(v[q4 * 4 + 1]) * mul,
+                                  __uint_as_float(v[q4 * 4 + 2]) * mul, __uint_as_float(v[q4 * 4 + 3]) * mul));
+        } else if (ok) {
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            float f[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) f[j] = __uint_as_float(v[q4 * 8 + j]) * mul;
+            *reinterpret_cast<uint4*>(row + 32 * g + q4 * 8) = pack8(f);
+          }
+        }
+      }
+      if (!atomic_dkv && steps == 0 && key < T) {  // no causal work: gradients are zero
+        for (int c = 32 * g; c < 32 * g + 32; c += 8) *reinterpret_cast<uint4*>(row + c) = make_uint4(0, 0, 0, 0);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
 template <int D>
 int bwd_launch(const void* q, const void* k, const void* v, const void* dout, const float* lse, const float* dvec,
                float* dq_acc, void* dk, void* dv, int64_t T, int hq, int hkv, int64_t qs, int64_t ks, int64_t vs,
                int64_t os, int64_t dks, int64_t dvs, float scale, int causal, float* dkv_acc, int split_group,
                int qsplit_tiles, int qchunks, cudaStream_t st,
                const float* rope_table) {
+  // head_dim 128: the 64-query kernel (measured faster: its dQ^T has TMEM of its own, so the drain
+  // and the dQ reduce-adds stay off the critical path; the 128-query kernel must alias dQ with dP^T
+  // and stage through the dS^T buffer).  head_dim 64: the 128-query kernel (3.4x the mma.sync one).
+  static const int variant = getenv("KPO_ATTN_BWD") ? atoi(getenv("KPO_ATTN_BWD")) : (D == 64 ? 3 : 2);
+  if (variant == 3 || D == 64) {  // 128-query steps
+    using C3 = Bwd3<D>;
+    CUtensorMap mq, mk, mv, mo, mdq;
+    int e;
+    if ((e = make_map_2d_f32(&mdq, dq_acc, (uint64_t)hq * D, T, (uint64_t)hq * D, C3::DQC, C3::BM, true))) return e;
+    if ((e = make_map_2d(&mq, q, (uint64_t)hq * D, T, qs, 64, C3::BM))) return e;
+    if ((e = make_map_2d(&mk, k, (uint64_t)hkv * D, T, ks, 64, C3::BN))) return e;
+    if ((e = make_map_2d(&mv, v, (uint64_t)hkv * D, T, vs, 64, C3::BN))) return e;
+    if ((e = make_map_2d(&mo, dout, (uint64_t)hq * D, T, os, 64, C3::BM))) return e;
+    static bool set3 = false;
+    if (!set3) {
+      KPO_CUDA(cudaFuncSetAttribute(attn_bwd_tc3_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C3::SMEM));
+      set3 = true;
+    }
+    const int ntiles = (int)((T + C3::BN - 1) / C3::BN);
+    dim3 grid((unsigned)(split_group ? hq : hkv), (unsigned)ntiles, (unsigned)(qchunks > 1 ? qchunks : 1));
+    KPO_CUDA(::kpo::pdl_launch(attn_bwd_tc3_kernel<D>, grid, C3::THREADS, C3::SMEM, st, mq, mk, mv, mo, mdq, lse, dvec,
+                               (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, (int)T, hq, hkv, dks, dvs, scale, causal,
+                               dkv_acc, split_group, qsplit_tiles, reinterpret_cast<const float2*>(rope_table)));
+    KPO_LAUNCH_CHECK();
+    return KPO_OK;
+  }
+  if constexpr (D == 64) {
+    return KPO_ERR_UNSUPPORTED;  // unreachable: head_dim 64 always takes the 128-query kernel
+  } else {
   using C = Bwd<D>;
   CUtensorMap mq, mk, mv, mo, mdq;
   int e;
@@ -1111,6 +1545,7 @@ int bwd_launch(const void* q, const void* k, const void* v, const void* dout, co
                                                           reinterpret_cast<const float2*>(rope_table)));
   KPO_LAUNCH_CHECK();
   return KPO_OK;
+  }
 }
 }  // namespace attn_tc
 
@@ -1126,8 +1561,16 @@ int attn_bwd_tcgen05_main(const void* q, const void* k, const void* v, const voi
                           int64_t qs, int64_t ks, int64_t vs, int64_t os, int64_t dks, int64_t dvs, float scale,
                           int causal, float* dkv_acc, int split_group, int qsplit_tiles, int qchunks,
                           cudaStream_t st, const float* rope_table) {
+  if (d == 64) {
+    if (rope_table != nullptr) {
+      set_error("attn_bwd tcgen05 path: the fused inverse rotary needs head_dim 128");
+      return KPO_ERR_UNSUPPORTED;
+    }
+    return attn_tc::bwd_launch<64>(q, k, v, dout, lse, dvec, dq_acc, dk, dv, T, hq, hkv, qs, ks, vs, os, dks, dvs,
+                                   scale, causal, dkv_acc, split_group, qsplit_tiles, qchunks, st, rope_table);
+  }
   if (d != 128) {
-    set_error("attn_bwd tcgen05 path needs head_dim 128");
+    set_error("attn_bwd tcgen05 path needs head_dim 64 or 128");
     return KPO_ERR_UNSUPPORTED;
   }
   return attn_tc::bwd_launch<128>(q, k, v, dout, lse, dvec, dq_acc, dk, dv, T, hq, hkv, qs, ks, vs, os, dks, dvs,

@@ -354,9 +354,9 @@ __device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t cols)
 PFN_cuTensorMapEncodeTiled_v12000 get_encode();
 int make_map_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t stride_elems,
                 uint32_t box_inner, uint32_t box_outer);
-// fp32, no swizzle (TMA reduce targets)
+// fp32 (TMA reduce targets); swizzle128: the smem box is SWIZZLE_128B (box_inner * 4 == 128)
 int make_map_2d_f32(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t stride_elems,
-                    uint32_t box_inner, uint32_t box_outer);
+                    uint32_t box_inner, uint32_t box_outer, bool swizzle128 = false);
 
 }  // namespace sm100
 }  // namespace kpo

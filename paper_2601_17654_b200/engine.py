@@ -81,6 +81,7 @@ class Observation:
     clock_control: str = ""
     graph: bool = False
     retried: int = 0
+    energy_trials_j: tuple = ()
 
     def as_dict(self) -> dict:
         return {k: (list(v) if isinstance(v, tuple) else v) for k, v in self.__dict__.items()}
@@ -90,6 +91,7 @@ class Engine:
     def __init__(self, programs, gpu: GpuModel, device=None, comm=None, clock_control: bool = True,
                  use_graphs: bool = True, launch_gate: bool = True, measurement_cls=Measurement,
                  cooldown_target_c: float | None = None, cooldown_max_s: float = 30.0,
+                 energy_outlier_frac: float | None = 0.10,
                  reject_throttled: bool = True, clock_tolerance_mhz: float = 30.0):
         self.gpu = gpu
         self.device = torch.device(device or "cuda")
@@ -114,6 +116,11 @@ class Engine:
         self._exec_ms: dict[tuple, float] = {}
         # multi-rank: maps this rank's execution-time estimate to the value every rank uses
         self.agree_ms = None
+        # energy-outlier re-measurement: a window whose average power departs from this program's
+        # running median by more than energy_outlier_frac (after 5 windows) is measured twice more and
+        # the median-energy window of the three is kept (NVML counter outliers)
+        self.energy_outlier_frac = energy_outlier_frac
+        self._power_hist: dict[str, list[float]] = {}
 
     @classmethod
     def for_layer(cls, layer, gpu: GpuModel, **kw) -> "Engine":
@@ -263,11 +270,40 @@ class Engine:
             if not (self.reject_throttled and bad and retried == 0):
                 break
             retried += 1
+        t_ms, e_j, obs = self._energy_outlier_check(name, prog, config, ncta, warmup_s, window_s, cooldown_s,
+                                                    t_ms, e_j, obs)
         temp = self.nvml.temperature_c()
         obs.temperature_c = temp
         obs.retried = retried
         self.history.append(obs)
         return t_ms, e_j, temp
+
+    def _energy_outlier_check(self, name, prog, config, ncta, warmup_s, window_s, cooldown_s, t_ms, e_j, obs):
+        """Re-measure a window whose average power is an outlier for this program (see __init__);
+        returns the (time, energy, observation) of the median-energy window of the three."""
+        hist = self._power_hist.setdefault(name, [])
+        power = e_j / max(t_ms / 1e3, 1e-12)
+        frac = self.energy_outlier_frac
+        suspect = False
+        if frac is not None and len(hist) >= 5:
+            med = sorted(hist)[len(hist) // 2]
+            suspect = abs(power - med) > frac * med
+        if self.agree_ms is not None and frac is not None and len(hist) >= 5:
+            suspect = bool(self.agree_ms(1.0 if suspect else 0.0) > 0.5)  # same branch on every rank
+        if suspect:
+            trials = [(e_j, t_ms, obs)]
+            for _ in range(2):
+                t2, e2, _ = self._window(prog, config, ncta, warmup_s, window_s)
+                o2 = self.last
+                o2.cooldown_s = self._cooldown(cooldown_s)
+                trials.append((e2, t2, o2))
+            energies = tuple(round(x[0], 6) for x in trials)  # in measurement order
+            e_j, t_ms, obs = sorted(trials, key=lambda x: x[0])[1]
+            obs.flags = tuple(obs.flags) + ("energy_outlier_remeasured",)
+            obs.energy_trials_j = energies
+            power = e_j / max(t_ms / 1e3, 1e-12)
+        hist.append(power)
+        return t_ms, e_j, obs
 
     def measure(self, partition, config, gpu: GpuModel | None = None, thermal=None, protocol=None, state=None):
         """Thermally-stable profiling pass (reference measure, simgpu.py:321-364)."""

@@ -128,3 +128,30 @@ def test_bench_reference_cpu_path_reports_per_candidate_costs():
         pytest.skip("reference package not installed (baseline/_ref)")
     assert r["partitions"] == 8 and r["candidates"] > 1000
     assert r["simulate_schedule_us"] > 0 and r["measure_us"] > 0 and r["cores"] == 1
+
+
+def test_energy_outlier_remeasured_median_of_three():
+    """Engine._energy_outlier_check (no GPU): after 5 windows of a program, a window whose average power
+    departs from the running median by more than energy_outlier_frac is measured twice more and the
+    median-energy window is kept; a consistent window is kept as is."""
+    from paper_2601_17654_b200.engine import Engine, Observation
+
+    eng = object.__new__(Engine)
+    eng.energy_outlier_frac = 0.10
+    eng._power_hist = {"p": [1000.0] * 5}
+    eng.agree_ms = None
+    queue = [(1.0, 0.99e-3 * 1000), (1.0, 1.01e-3 * 1000)]  # two re-measurements near 1 kW
+
+    def window(prog, config, ncta, warmup_s, window_s):
+        t, e = queue.pop(0)
+        eng.last = Observation(window_s=1.0)
+        return t, e, 1
+
+    eng._window = window
+    eng._cooldown = lambda s: 0.0
+    # a 560 W outlier (1 ms per execution, 0.56 J) -> re-measured, the median (0.99 J) is kept
+    t, e, obs = eng._energy_outlier_check("p", None, None, 8, 0.1, 1.0, 0.0, 1.0, 0.56, Observation())
+    assert e == 0.99 and "energy_outlier_remeasured" in obs.flags and obs.energy_trials_j == (0.56, 0.99, 1.01)
+    # a consistent window: no re-measurement
+    t, e, obs = eng._energy_outlier_check("p", None, None, 8, 0.1, 1.0, 0.0, 1.0, 1.02, Observation())
+    assert e == 1.02 and "energy_outlier_remeasured" not in obs.flags and not queue

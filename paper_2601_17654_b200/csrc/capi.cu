@@ -33,15 +33,20 @@ __global__ void kpo_probe_kernel() {}
 extern "C" int kpo_probe_launch_completion(void* event, void* stream) {
   KPO_CHECK_ARG(event, "probe_launch_completion: null event");
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(1);
+  // the same attribute set as the collectives' launches (comm.cu): 2-CTA clusters + the completion event
+  cfg.gridDim = dim3(2);
   cfg.blockDim = dim3(32);
   cfg.stream = (cudaStream_t)stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeLaunchCompletionEvent;
-  attr[0].val.launchCompletionEvent.event = (cudaEvent_t)event;
-  attr[0].val.launchCompletionEvent.flags = 0;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeLaunchCompletionEvent;
+  attr[1].val.launchCompletionEvent.event = (cudaEvent_t)event;
+  attr[1].val.launchCompletionEvent.flags = 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   KPO_CUDA(cudaLaunchKernelEx(&cfg, kpo_probe_kernel));
   KPO_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
   KPO_CUDA(cudaEventQuery((cudaEvent_t)event));

@@ -11,7 +11,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 
 from paper_2601_17654_b200.comm import Communicator
-from paper_2601_17654_b200.device import b200_model
+from paper_2601_17654_b200.device import b200_model_measured as b200_model
 from paper_2601_17654_b200.engine import Engine
 from paper_2601_17654_b200.layer import PartitionedLayer
 from paper_2601_17654_b200.model import baseline_workload

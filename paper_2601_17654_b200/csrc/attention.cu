@@ -17,6 +17,11 @@ int attn_bwd_tcgen05_main(const void* q, const void* k, const void* v, const voi
                           int64_t qs, int64_t ks, int64_t vs, int64_t os, int64_t dks, int64_t dvs, float scale,
                           int causal, float* dkv_acc, int split_group, int qsplit_tiles, int qchunks,
                           cudaStream_t st, const float* rope_table);
+int attn_bwd_tcgen05_split(const void* q, const void* k, const void* v, const void* o, const void* dout,
+                           const float* lse, float* dvec, void* dq, void* dk, void* dv, int64_t T, int hq, int hkv,
+                           int d, int64_t qs, int64_t ks, int64_t vs, int64_t os, int64_t dqs, int64_t dks,
+                           int64_t dvs, float scale, int causal, float* dkv_acc, int split_group, int qsplit_tiles,
+                           int qchunks, cudaStream_t st, const float* rope_table);
 }
 
 namespace kpo {
@@ -565,7 +570,11 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* o
   using CF = BwdCfg<D>;
   float* dq_acc = (float*)ws;
   float* dvec = dq_acc + T * hq * D;
-  {
+  // KPO_ATTN_BWD: 4 (default) = two kernels (dQ, then dK / dV; no dQ reduction, no pre / post kernels),
+  // 2 / 3 = the single-kernel 64- / 128-query tcgen05 backward, 1 = mma.sync (A/B baselines)
+  static const int variant = getenv("KPO_ATTN_BWD") ? atoi(getenv("KPO_ATTN_BWD")) : 4;
+  const bool two_kernels = use_tc && T % 8 == 0 && variant == 4;
+  if (!two_kernels) {
     const int64_t threads = T * hq * (D / 8);
     KPO_CUDA(::kpo::pdl_launch(attn_bwd_pre_kernel<D>, (unsigned)((threads + 255) / 256), 256, 0, s, 
         (const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, dvec, dq_acc, (int)T, hq, os));
@@ -602,8 +611,13 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* o
       KPO_CUDA(cudaMemsetAsync(dkv_acc, 0, sizeof(float) * acc_rows * hkv * D, s));
       KPO_CUDA(cudaMemsetAsync(dkv_acc + T * hkv * D, 0, sizeof(float) * acc_rows * hkv * D, s));
     }
-    int st = attn_bwd_tcgen05_main(q, k, v, dout, lse, dvec, dq_acc, dk, dv, T, hq, hkv, D, qs, ks, vs, os, dks, dvs,
-                                   scale, causal, dkv_acc, split ? 1 : 0, qsplit_tiles, qchunks, s, rope_table);
+    int st = two_kernels
+                 ? attn_bwd_tcgen05_split(q, k, v, o, dout, lse, dvec, dq, dk, dv, T, hq, hkv, D, qs, ks, vs, os, dqs,
+                                          dks, dvs, scale, causal, dkv_acc, split ? 1 : 0, qsplit_tiles, qchunks, s,
+                                          rope_table)
+                 : attn_bwd_tcgen05_main(q, k, v, dout, lse, dvec, dq_acc, dk, dv, T, hq, hkv, D, qs, ks, vs, os,
+                                         dks, dvs, scale, causal, dkv_acc, split ? 1 : 0, qsplit_tiles, qchunks, s,
+                                         rope_table);
     if (st) return st;
     if (dkv_acc) {
       // convert the accumulated rows; the accumulator layout [T][hkv][D] makes them a prefix, so the
@@ -632,7 +646,7 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* o
       dq_acc, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, (int)T, hq, hkv, qs, ks, vs, os, dks, dvs, scale, causal));
   KPO_LAUNCH_CHECK();
   }
-  {
+  if (!two_kernels) {  // dQ accumulator -> bf16 (the two-kernel path writes dQ directly)
     const int64_t n = T * hq * D / 8;
     if (rope_cs)
       KPO_CUDA(::kpo::pdl_launch(attn_bwd_post_rope_kernel<D>, (unsigned)((n / 2 + 255) / 256), 256, 0, s, dq_acc,

@@ -1487,6 +1487,623 @@ __global__ void __launch_bounds__(Bwd3<D>::THREADS, 1)
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
+// =====================================================================================
+// Backward as two kernels (default for head_dim 128; KPO_ATTN_BWD=4):
+//   attn_bwd_dq_kernel    one CTA per (q head, 128 queries), loops over the causal key tiles:
+//                           S = Q K^T, dP = dO V^T, dS = P (dP - D), dQ += dS K
+//                         Q and dO stay in TMEM (the A operands of S and dP), dS is written over dP
+//                         (the TMEM A operand of the dQ MMA), dQ accumulates in TMEM and leaves once,
+//                         in bf16 (inverse-rotated for the fused RoPE path).  It also computes
+//                         D = rowsum(dO * O) for its rows and writes it for the second kernel.
+//   attn_bwd_dkdv_kernel  one CTA per (kv head, 128 keys), loops over the GQA group x causal query
+//                         tiles: S^T = K Q^T, dP^T = V dO^T, dV += P^T dO, dK += dS^T Q, with P^T / dS^T
+//                         written over S^T / dP^T (the TMEM A operands of dV / dK).
+// The single-kernel backward reduces dQ across key tiles through fp32 atomics in L2 and stages it
+// through shared memory; here every MMA is M=128 x N=128 x K=128, the K / V (dQ kernel) and Q / dO
+// (dK/dV kernel) A operands come from TMEM or are read once per 128x128 block, nothing is reduced
+// across CTAs (deterministic), and the pre / post kernels (D vector, dQ accumulator zeroing and
+// conversion) disappear, at the price of recomputing S and dP (7 GEMMs per block instead of 5).
+template <int D>
+struct BwdDq {
+  static constexpr int BM = 128, BN = 128, STAGES = 2, KSUB = D / 64;
+  static constexpr int KV_BYTES = BN * D * 2;
+  static constexpr int OFF_K = 0, OFF_V = STAGES * KV_BYTES, OFF_RED = 2 * STAGES * KV_BYTES;
+  static constexpr int OFF_BAR = OFF_RED + 4 * BM * 4;
+  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+  static constexpr int COL_S = 0, COL_DP = 128, COL_DQ = 256, COL_Q = 384, COL_DO = 384 + D / 2;
+  static constexpr int SM_WARPS = 16;
+  static constexpr int THREADS = (2 + SM_WARPS) * 32;
+};
+
+template <int D>
+__global__ void __launch_bounds__(BwdDq<D>::THREADS, 1)
+    attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                       const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ dout,
+                       const __nv_bfloat16* __restrict__ o, const float* __restrict__ lse,
+                       float* __restrict__ dvec, __nv_bfloat16* __restrict__ dq, int T, int hq, int hkv,
+                       int64_t qs, int64_t os, int64_t dqs, float scale, int causal,
+                       const float2* __restrict__ rope_cs) {
+  ::kpo::pdl_launch_dependents();
+  using C = BwdDq<D>;
+  constexpr int BM = C::BM, BN = C::BN, KSUB = C::KSUB;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* kv_full = bar + 0;   // [2]
+  uint64_t* kv_empty = bar + 2;  // [2]
+  uint64_t* s_full = bar + 4;
+  uint64_t* s_empty = bar + 5;
+  uint64_t* dp_full = bar + 6;
+  uint64_t* ds_full = bar + 7;
+  uint64_t* qo_ready = bar + 8;
+  uint64_t* acc_done = bar + 9;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10);
+  float* red = reinterpret_cast<float*>(smem + C::OFF_RED);  // [4 column groups][BM] partial D
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int h = blockIdx.x;
+  const int ntiles = (T + BM - 1) / BM;
+  const int mt = ntiles - 1 - (int)blockIdx.y;  // the longest causal rows first
+  const int m0 = mt * BM;
+  const int kvh = h / (hq / hkv);
+  const int steps = causal ? min(mt + 1, (T + BN - 1) / BN) : (T + BN - 1) / BN;
+  const float scale_log2 = scale * kLog2e;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::STAGES; ++i) {
+      mbar_init(smem_u32(&kv_full[i]), 1);
+      mbar_init(smem_u32(&kv_empty[i]), 1);
+    }
+    mbar_init(smem_u32(s_full), 1);
+    mbar_init(smem_u32(s_empty), C::SM_WARPS);
+    mbar_init(smem_u32(dp_full), 1);
+    mbar_init(smem_u32(ds_full), C::SM_WARPS);
+    mbar_init(smem_u32(qo_ready), C::SM_WARPS);
+    mbar_init(smem_u32(acc_done), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc(smem_u32(tmem_slot), 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (*tmem_slot != 0) __trap();
+  ::kpo::pdl_wait();
+  constexpr uint32_t tmem = 0;
+  const uint32_t sK = smem_u32(smem + C::OFF_K), sV = smem_u32(smem + C::OFF_V);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA producer: K_n, V_n ring
+      for (int n = 0; n < steps; ++n) {
+        const int st = n % C::STAGES;
+        mbar_wait(smem_u32(&kv_empty[st]), ((n / C::STAGES) & 1) ^ 1);
+        const uint32_t fb = smem_u32(&kv_full[st]);
+        mbar_arrive_expect_tx(fb, 2 * C::KV_BYTES);
+#pragma unroll
+        for (int kb = 0; kb < KSUB; ++kb) {
+          tma_load_2d(sK + st * C::KV_BYTES + kb * BN * 128, &tmK, fb, kvh * D + kb * 64, n * BN);
+          tma_load_2d(sV + st * C::KV_BYTES + kb * BN * 128, &tmV, fb, kvh * D + kb * 64, n * BN);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (whole warp, elect.sync)
+    constexpr uint32_t ID_S = idesc_bf16(BM, BN, false, false);   // S, dP: A (Q / dO) from TMEM
+    constexpr uint32_t ID_Q = idesc_bf16(BM, D, false, true);     // dQ += dS K: A = dS from TMEM, B MN-major
+    mbar_wait(smem_u32(qo_ready), 0);
+    tc_fence_after();
+    auto mma_qk = [&](int n, uint32_t col_a, uint32_t b_base, uint32_t col_d, uint64_t* done) {
+      // col_d = A (from TMEM, D / 2 packed columns) x B^T (tile [BN keys][D], K-major)
+      const uint32_t b_k = desc_lo(b_base, 16);
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk)
+        tc_mma_ts_lo_w(tmem + col_d, tmem + col_a + 8 * kk, b_k + (kk >> 2) * (BN * 8) + (kk & 3) * 2, ID_S,
+                       kk > 0 ? 1u : 0u);
+      tc_commit_w(smem_u32(done));
+    };
+    auto mma_s = [&](int n) {
+      const int st = n % C::STAGES;
+      mbar_wait(smem_u32(&kv_full[st]), (n / C::STAGES) & 1);
+      tc_fence_after();
+      mma_qk(n, C::COL_Q, sK + st * C::KV_BYTES, C::COL_S, s_full);
+    };
+    auto mma_dp = [&](int n) {
+      const int st = n % C::STAGES;  // kv_full[st] was waited for by mma_s(n)
+      mma_qk(n, C::COL_DO, sV + st * C::KV_BYTES, C::COL_DP, dp_full);
+    };
+    if (steps > 0) {
+      mma_s(0);
+      mma_dp(0);
+    }
+    for (int n = 0; n < steps; ++n) {
+      const int st = n % C::STAGES;
+      if (n + 1 < steps) {
+        mbar_wait(smem_u32(s_empty), n & 1);  // the softmax has read S(n)
+        mma_s(n + 1);
+      }
+      // dQ += dS(n) K_n: dS of keys 16k.. sits in softmax warp (k / 2)'s dP columns, 8 per 16 keys
+      mbar_wait(smem_u32(ds_full), n & 1);
+      tc_fence_after();
+      const uint32_t k_mn = desc_lo(sK + st * C::KV_BYTES, BN * 128);
+#pragma unroll
+      for (int k = 0; k < BN / 16; ++k)
+        tc_mma_ts_lo_w(tmem + C::COL_DQ, tmem + C::COL_DP + 32 * (k >> 1) + 8 * (k & 1), k_mn + k * 128, ID_Q,
+                       (n > 0 || k > 0) ? 1u : 0u);
+      tc_commit_w(smem_u32(&kv_empty[st]));
+      if (n + 1 < steps) mma_dp(n + 1);  // over dS(n): the dQ MMA above is its last reader
+    }
+    tc_commit_w(smem_u32(acc_done));
+  } else {
+    // ------------------------------------------------------------ softmax warps: row = query, 32 keys each
+    const int quarter = warp & 3;
+    const int g = (warp - 2) >> 2;
+    const int qr = quarter * 32 + lane;
+    const int t = m0 + qr;
+    const bool row_ok = t < T;
+    const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
+    // Q / dO rows -> TMEM (this warp's 32 head-dim columns = 16 packed TMEM columns); D partials
+    float dpart = 0.f;
+    if (32 * g < D) {
+      uint32_t qa[16], da[16];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint4 uq = make_uint4(0, 0, 0, 0), ud = uq, uo = uq;
+        if (row_ok) {
+          uq = *reinterpret_cast<const uint4*>(q + (int64_t)t * qs + (int64_t)h * D + 32 * g + 8 * c);
+          ud = *reinterpret_cast<const uint4*>(dout + (int64_t)t * os + (int64_t)h * D + 32 * g + 8 * c);
+          uo = *reinterpret_cast<const uint4*>(o + (int64_t)t * os + (int64_t)h * D + 32 * g + 8 * c);
+        }
+        qa[4 * c] = uq.x, qa[4 * c + 1] = uq.y, qa[4 * c + 2] = uq.z, qa[4 * c + 3] = uq.w;
+        da[4 * c] = ud.x, da[4 * c + 1] = ud.y, da[4 * c + 2] = ud.z, da[4 * c + 3] = ud.w;
+        float fd[8], fo[8];
+        unpack8(ud, fd);
+        unpack8(uo, fo);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) dpart = fmaf(fd[j], fo[j], dpart);
+      }
+      tmem_st16(lane_addr + C::COL_Q + 16 * g, qa);
+      tmem_st16(lane_addr + C::COL_DO + 16 * g, da);
+      tmem_wait_st();
+    }
+    red[g * BM + qr] = dpart;
+    tc_fence_before();
+    named_bar(1, C::SM_WARPS * 32);
+    const float dsum = red[qr] + red[BM + qr] + red[2 * BM + qr] + red[3 * BM + qr];
+    if (g == 0 && row_ok) dvec[(int64_t)h * T + t] = dsum;
+    const float nl = row_ok ? lse[(int64_t)h * T + t] * kLog2e : 0.f;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_u32(qo_ready));
+    for (int n = 0; n < steps; ++n) {
+      const int k0 = n * BN + 32 * g;
+      const bool tile_mask = (causal && n * BN + BN - 1 > m0) || n * BN + BN > T || m0 + BM > T;
+      mbar_wait(smem_u32(s_full), n & 1);
+      tc_fence_after();
+      float p[32];
+      tmem_ld32_nowait(lane_addr + C::COL_S + 32 * g, reinterpret_cast<uint32_t*>(p));
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(s_empty));
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        float pe = ex2(fmaf(p[i], scale_log2, -nl));
+        if (tile_mask) {
+          const int key = k0 + i;
+          pe = (!row_ok || key >= T || (causal && key > t)) ? 0.f : pe;
+        }
+        p[i] = pe;
+      }
+      mbar_wait(smem_u32(dp_full), n & 1);
+      tc_fence_after();
+      uint32_t qq[16];
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        float dp[16];
+        tmem_ld16_nowait(lane_addr + C::COL_DP + 32 * g + 16 * hf, reinterpret_cast<uint32_t*>(dp));
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 16; i += 2)
+          qq[(16 * hf + i) / 2] = pack_bf16x2(p[16 * hf + i] * (dp[i] - dsum), p[16 * hf + i + 1] * (dp[i + 1] - dsum));
+      }
+      tmem_st16(lane_addr + C::COL_DP + 32 * g, qq);  // over this warp's own (already read) dP columns
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(ds_full));
+    }
+    // ------------------------------------------------------------ dQ epilogue: row t, bf16 (+ inverse rotary)
+    mbar_wait(smem_u32(acc_done), 0);
+    tc_fence_after();
+    if (32 * g < D) {
+      __nv_bfloat16* row = dq + (int64_t)t * dqs + (int64_t)h * D;
+      if (rope_cs != nullptr) {  // head_dim 128 (host-checked): pairs (i, i + 64), i in [16g, 16g + 16)
+        uint32_t va[16], vb[16];
+        tmem_ld16_nowait(lane_addr + C::COL_DQ + 16 * g, va);
+        tmem_ld16_nowait(lane_addr + C::COL_DQ + D / 2 + 16 * g, vb);
+        tmem_wait_ld();
+        if (row_ok) {
+          const float2* cs = rope_cs + (int64_t)t * (D / 2);
+#pragma unroll
+          for (int q8 = 0; q8 < 2; ++q8) {
+            float oa[8], ob[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float2 r = cs[16 * g + q8 * 8 + j];
+              const float x = __uint_as_float(va[q8 * 8 + j]) * scale, y = __uint_as_float(vb[q8 * 8 + j]) * scale;
+              oa[j] = x * r.x + y * r.y;
+              ob[j] = y * r.x - x * r.y;
+            }
+            *reinterpret_cast<uint4*>(row + 16 * g + q8 * 8) = pack8(oa);
+            *reinterpret_cast<uint4*>(row + D / 2 + 16 * g + q8 * 8) = pack8(ob);
+          }
+        }
+      } else {
+        uint32_t v[32];
+        tmem_ld32_nowait(lane_addr + C::COL_DQ + 32 * g, v);
+        tmem_wait_ld();
+        if (row_ok) {
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            float f[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) f[j] = __uint_as_float(v[q4 * 8 + j]) * scale;
+            *reinterpret_cast<uint4*>(row + 32 * g + q4 * 8) = pack8(f);
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+template <int D>
+struct BwdKV {
+  static constexpr int BN = 128, BM = 128, STAGES = 2, KSUB = D / 64;
+  static constexpr int KV_BYTES = BN * D * 2, QT_BYTES = BM * D * 2;
+  static constexpr int OFF_K = 0, OFF_V = KV_BYTES, OFF_Q = 2 * KV_BYTES;
+  static constexpr int OFF_DO = OFF_Q + STAGES * QT_BYTES;
+  static constexpr int OFF_STAT = OFF_DO + STAGES * QT_BYTES;  // [STAGES][lse BM | D BM]
+  static constexpr int OFF_BAR = OFF_STAT + STAGES * 2 * BM * 4;
+  static constexpr int SMEM = OFF_BAR + 256 + 1024;
+  static constexpr int COL_S = 0, COL_DP = 128, COL_DV = 256, COL_DK = 384;
+  static constexpr int SM_WARPS = 16;
+  static constexpr int THREADS = (2 + SM_WARPS) * 32;
+};
+
+template <int D>
+__global__ void __launch_bounds__(BwdKV<D>::THREADS, 1)
+    attn_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                         const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+                         const float* __restrict__ lse, const float* __restrict__ dvec,
+                         __nv_bfloat16* __restrict__ dk, __nv_bfloat16* __restrict__ dv, int T, int hq, int hkv,
+                         int64_t dks, int64_t dvs, float scale, int causal, float* __restrict__ dkv_acc,
+                         int split_group, int qsplit_tiles, const float2* __restrict__ rope_cs) {
+  // grid / modes as attn_bwd_tc_kernel (split-group, query chunks, fused inverse rotary of dK)
+  ::kpo::pdl_launch_dependents();
+  using C = BwdKV<D>;
+  constexpr int BN = C::BN, BM = C::BM, KSUB = C::KSUB;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* kv_full = bar + 0;
+  uint64_t* q_full = bar + 1;    // [2]
+  uint64_t* q_empty = bar + 3;   // [2]
+  uint64_t* do_full = bar + 5;   // [2]
+  uint64_t* do_empty = bar + 7;  // [2]
+  uint64_t* s_full = bar + 9;
+  uint64_t* p_full = bar + 10;
+  uint64_t* dp_full = bar + 11;
+  uint64_t* ds_full = bar + 12;
+  uint64_t* acc_done = bar + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+  float* stat = reinterpret_cast<float*>(smem + C::OFF_STAT);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nblk = blockIdx.y;
+  const bool split = split_group != 0;
+  const int group = split ? 1 : hq / hkv;
+  const int h_first = split ? (int)blockIdx.x : (int)blockIdx.x * (hq / hkv);
+  const int kvh = split ? (int)blockIdx.x / (hq / hkv) : (int)blockIdx.x;
+  const int n0 = nblk * BN;
+  const int total_m = (T + BM - 1) / BM;
+  int m_start = causal ? n0 / BM : 0, m_end = total_m;
+  const bool chunked = gridDim.z > 1 && nblk < qsplit_tiles;
+  if (gridDim.z > 1) {
+    if (chunked) {
+      const int qper = (total_m + (int)gridDim.z - 1) / (int)gridDim.z;
+      m_start = max(m_start, (int)blockIdx.z * qper);
+      m_end = min(total_m, ((int)blockIdx.z + 1) * qper);
+      if (m_start >= m_end) return;
+    } else if (blockIdx.z != 0) {
+      return;
+    }
+  }
+  const bool atomic_dkv = split || chunked;
+  const int mq = m_end - m_start;
+  const int steps = group * mq;
+  const float scale_log2 = scale * kLog2e;
+
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(kv_full), 1);
+    for (int i = 0; i < C::STAGES; ++i) {
+      mbar_init(smem_u32(&q_full[i]), 1);
+      mbar_init(smem_u32(&q_empty[i]), 1);
+      mbar_init(smem_u32(&do_full[i]), 1);
+      mbar_init(smem_u32(&do_empty[i]), 1);
+    }
+    mbar_init(smem_u32(s_full), 1);
+    mbar_init(smem_u32(p_full), C::SM_WARPS);
+    mbar_init(smem_u32(dp_full), 1);
+    mbar_init(smem_u32(ds_full), C::SM_WARPS);
+    mbar_init(smem_u32(acc_done), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc(smem_u32(tmem_slot), 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (*tmem_slot != 0) __trap();
+  ::kpo::pdl_wait();  // the dQ kernel before us wrote the D vector
+  constexpr uint32_t tmem = 0;
+  const uint32_t sK = smem_u32(smem + C::OFF_K), sV = smem_u32(smem + C::OFF_V);
+  const uint32_t sQ = smem_u32(smem + C::OFF_Q), sDO = smem_u32(smem + C::OFF_DO);
+
+  auto step_coords = [&](int s, int& h, int& m0) {
+    h = h_first + s / mq;
+    m0 = (m_start + s % mq) * BM;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA producer
+      mbar_arrive_expect_tx(smem_u32(kv_full), 2 * C::KV_BYTES);
+#pragma unroll
+      for (int kb = 0; kb < KSUB; ++kb) {
+        tma_load_2d(sK + kb * BN * 128, &tmK, smem_u32(kv_full), kvh * D + kb * 64, n0);
+        tma_load_2d(sV + kb * BN * 128, &tmV, smem_u32(kv_full), kvh * D + kb * 64, n0);
+      }
+      for (int s = 0; s < steps; ++s) {
+        const int st = s % C::STAGES;
+        const uint32_t ph = ((s / C::STAGES) & 1) ^ 1;
+        int h, m0;
+        step_coords(s, h, m0);
+        const uint32_t nstat = (uint32_t)min(BM, T - m0) * 4u;
+        mbar_wait(smem_u32(&q_empty[st]), ph);
+        const uint32_t fb = smem_u32(&q_full[st]);
+        mbar_arrive_expect_tx(fb, C::QT_BYTES + 2 * nstat);
+#pragma unroll
+        for (int kb = 0; kb < KSUB; ++kb) tma_load_2d(sQ + st * C::QT_BYTES + kb * BM * 128, &tmQ, fb, h * D + kb * 64, m0);
+        const uint32_t sst = smem_u32(stat + st * 2 * BM);
+        bulk_load(sst, lse + (int64_t)h * T + m0, nstat, fb);
+        bulk_load(sst + BM * 4, dvec + (int64_t)h * T + m0, nstat, fb);
+        mbar_wait(smem_u32(&do_empty[st]), ph);
+        const uint32_t ob = smem_u32(&do_full[st]);
+        mbar_arrive_expect_tx(ob, C::QT_BYTES);
+#pragma unroll
+        for (int kb = 0; kb < KSUB; ++kb) tma_load_2d(sDO + st * C::QT_BYTES + kb * BM * 128, &tmDO, ob, h * D + kb * 64, m0);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (whole warp, elect.sync)
+    constexpr uint32_t ID_SS = idesc_bf16(BN, BM, false, false);  // S^T, dP^T
+    constexpr uint32_t ID_G = idesc_bf16(BN, D, false, true);     // dV, dK: A from TMEM, B MN-major
+    const uint32_t k_k = desc_lo(sK, 16), v_k = desc_lo(sV, 16);
+    auto mma_ss = [&](uint32_t a_k, uint32_t b_base, uint32_t col_d, uint64_t* done) {
+      const uint32_t b_k = desc_lo(b_base, 16);
+#pragma unroll
+      for (int kb = 0; kb < KSUB; ++kb)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          tc_mma_lo_w(tmem + col_d, a_k + kb * (BN * 8) + k * 2, b_k + kb * (BM * 8) + k * 2, ID_SS, (kb | k) ? 1u : 0u);
+      tc_commit_w(smem_u32(done));
+    };
+    auto mma_s = [&](int s) {
+      const int st = s % C::STAGES;
+      mbar_wait(smem_u32(&q_full[st]), (s / C::STAGES) & 1);
+      tc_fence_after();
+      mma_ss(k_k, sQ + st * C::QT_BYTES, C::COL_S, s_full);
+    };
+    auto mma_dp = [&](int s) {
+      const int st = s % C::STAGES;
+      mbar_wait(smem_u32(&do_full[st]), (s / C::STAGES) & 1);
+      tc_fence_after();
+      mma_ss(v_k, sDO + st * C::QT_BYTES, C::COL_DP, dp_full);
+    };
+    if (steps > 0) {
+      mbar_wait(smem_u32(kv_full), 0);
+      mma_s(0);
+      mma_dp(0);
+    }
+    for (int s = 0; s < steps; ++s) {
+      const int st = s % C::STAGES;
+      // dV += P^T(s) dO(s): P^T of queries 16k.. sits in softmax warp (k / 2)'s S columns
+      mbar_wait(smem_u32(p_full), s & 1);
+      tc_fence_after();
+      const uint32_t o_mn = desc_lo(sDO + st * C::QT_BYTES, BM * 128);
+#pragma unroll
+      for (int k = 0; k < BM / 16; ++k)
+        tc_mma_ts_lo_w(tmem + C::COL_DV, tmem + C::COL_S + 32 * (k >> 1) + 8 * (k & 1), o_mn + k * 128, ID_G,
+                       (s > 0 || k > 0) ? 1u : 0u);
+      tc_commit_w(smem_u32(&do_empty[st]));
+      if (s + 1 < steps) mma_s(s + 1);  // over S / P(s): the dV MMA above is its last reader
+      // dK += dS^T(s) Q(s): dS^T over the dP^T columns, same per-warp layout
+      mbar_wait(smem_u32(ds_full), s & 1);
+      tc_fence_after();
+      const uint32_t q_mn = desc_lo(sQ + st * C::QT_BYTES, BM * 128);
+#pragma unroll
+      for (int k = 0; k < BM / 16; ++k)
+        tc_mma_ts_lo_w(tmem + C::COL_DK, tmem + C::COL_DP + 32 * (k >> 1) + 8 * (k & 1), q_mn + k * 128, ID_G,
+                       (s > 0 || k > 0) ? 1u : 0u);
+      tc_commit_w(smem_u32(&q_empty[st]));
+      if (s + 1 < steps) mma_dp(s + 1);  // over dP^T / dS^T(s): the dK MMA above is its last reader
+    }
+    tc_commit_w(smem_u32(acc_done));
+  } else {
+    // ------------------------------------------------------------ softmax warps: row = key, 32 queries each
+    const int quarter = warp & 3;
+    const int g = (warp - 2) >> 2;
+    const int r = quarter * 32 + lane;
+    const int key = n0 + r;
+    const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
+    for (int s = 0, mi = 0; s < steps; ++s, mi = (mi + 1 == mq) ? 0 : mi + 1) {
+      const int m0 = (m_start + mi) * BM;
+      const int st = s % C::STAGES;
+      const bool tile_mask = (causal && m0 < n0 + BN - 1) || n0 + BN > T || m0 + BM > T;
+      mbar_wait(smem_u32(&q_full[st]), (s / C::STAGES) & 1);  // lse / D rows of this step
+      mbar_wait(smem_u32(s_full), s & 1);
+      tc_fence_after();
+      float p[32];
+      tmem_ld32_nowait(lane_addr + C::COL_S + 32 * g, reinterpret_cast<uint32_t*>(p));
+      tmem_wait_ld();
+      const float* sl = stat + st * 2 * BM + 32 * g;
+      {
+        uint32_t pp[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          const float4 nl = *reinterpret_cast<const float4*>(sl + i);
+          const float l4[4] = {nl.x, nl.y, nl.z, nl.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float pe = ex2(fmaf(p[i + e], scale_log2, -l4[e] * kLog2e));
+            if (tile_mask) {
+              const int qi = m0 + 32 * g + i + e;
+              pe = (key >= T || qi >= T || (causal && qi < key)) ? 0.f : pe;
+            }
+            p[i + e] = pe;
+          }
+          pp[i / 2] = pack_bf16x2(p[i], p[i + 1]);
+          pp[i / 2 + 1] = pack_bf16x2(p[i + 2], p[i + 3]);
+        }
+        tmem_st16(lane_addr + C::COL_S + 32 * g, pp);  // over this warp's own (already read) S columns
+        tmem_wait_st();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(p_full));
+      mbar_wait(smem_u32(dp_full), s & 1);
+      tc_fence_after();
+      uint32_t qq[16];
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        float dp[16];
+        tmem_ld16_nowait(lane_addr + C::COL_DP + 32 * g + 16 * hf, reinterpret_cast<uint32_t*>(dp));
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 16; i += 4) {
+          const float4 dd = *reinterpret_cast<const float4*>(sl + BM + 16 * hf + i);
+          const int b = 16 * hf + i;
+          qq[b / 2] = pack_bf16x2(p[b] * (dp[i] - dd.x), p[b + 1] * (dp[i + 1] - dd.y));
+          qq[b / 2 + 1] = pack_bf16x2(p[b + 2] * (dp[i + 2] - dd.z), p[b + 3] * (dp[i + 3] - dd.w));
+        }
+      }
+      tmem_st16(lane_addr + C::COL_DP + 32 * g, qq);  // over this warp's own (already read) dP^T columns
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(ds_full));
+    }
+    // ------------------------------------------------------------ dK / dV epilogue (all 16 warps)
+    mbar_wait(smem_u32(acc_done), 0);
+    tc_fence_after();
+    const bool ok = key < T && steps > 0;
+#pragma unroll 1
+    for (int which = 0; which < 2; ++which) {
+      const uint32_t col = which ? C::COL_DV : C::COL_DK;
+      const float mul = which ? 1.f : scale;
+      __nv_bfloat16* row = which ? dv + (int64_t)key * dvs + (int64_t)kvh * D : dk + (int64_t)key * dks + (int64_t)kvh * D;
+      if (32 * g >= D) break;  // head_dim 64: warps g = 0, 1 hold the columns
+      if (which == 0 && rope_cs != nullptr && !atomic_dkv) {
+        // inverse rotary (head_dim 128, host-checked), pairs (i, i + D/2): i in [16g, 16g + 16)
+        const float2* cs = rope_cs + (int64_t)(key < T ? key : 0) * (D / 2);
+        uint32_t va[16], vb[16];
+        tmem_ld16_nowait(lane_addr + col + 16 * g, va);
+        tmem_ld16_nowait(lane_addr + col + D / 2 + 16 * g, vb);
+        tmem_wait_ld();
+        if (ok) {
+#pragma unroll
+          for (int q8 = 0; q8 < 2; ++q8) {
+            float oa[8], ob[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float2 tc = cs[16 * g + q8 * 8 + j];
+              const float x = __uint_as_float(va[q8 * 8 + j]) * mul, y = __uint_as_float(vb[q8 * 8 + j]) * mul;
+              oa[j] = x * tc.x + y * tc.y;
+              ob[j] = y * tc.x - x * tc.y;
+            }
+            *reinterpret_cast<uint4*>(row + 16 * g + q8 * 8) = pack8(oa);
+            *reinterpret_cast<uint4*>(row + D / 2 + 16 * g + q8 * 8) = pack8(ob);
+          }
+        }
+      } else {
+        uint32_t v[32];
+        tmem_ld32_nowait(lane_addr + col + 32 * g, v);
+        tmem_wait_ld();
+        if (ok && atomic_dkv) {
+          float* acc = dkv_acc + (which ? (int64_t)T * hkv * D : 0) + ((int64_t)key * hkv + kvh) * D + 32 * g;
+#pragma unroll
+          for (int q4 = 0; q4 < 8; ++q4)
+            atomicAdd(reinterpret_cast<float4*>(acc + q4 * 4),
+                      make_float4(__uint_as_float(v[q4 * 4 + 0]) * mul, __uint_as_float(v[q4 * 4 + 1]) * mul,
+                                  __uint_as_float(v[q4 * 4 + 2]) * mul, __uint_as_float(v[q4 * 4 + 3]) * mul));
+        } else if (ok) {
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            float f[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) f[j] = __uint_as_float(v[q4 * 8 + j]) * mul;
+            *reinterpret_cast<uint4*>(row + 32 * g + q4 * 8) = pack8(f);
+          }
+        }
+      }
+      if (!atomic_dkv && steps == 0 && key < T) {
+        for (int c = 32 * g; c < 32 * g + 32; c += 8) *reinterpret_cast<uint4*>(row + c) = make_uint4(0, 0, 0, 0);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+// dQ kernel, then the dK / dV kernel (same stream; PDL lets the second one's prologue overlap).
+template <int D>
+int bwd_split_launch(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse,
+                     float* dvec, void* dq, void* dk, void* dv, int64_t T, int hq, int hkv, int64_t qs, int64_t ks,
+                     int64_t vs, int64_t os, int64_t dqs, int64_t dks, int64_t dvs, float scale, int causal,
+                     float* dkv_acc, int split_group, int qsplit_tiles, int qchunks, cudaStream_t st,
+                     const float* rope_table) {
+  using A = BwdDq<D>;
+  using B = BwdKV<D>;
+  CUtensorMap mq, mk, mv, mo;
+  int e;
+  if ((e = make_map_2d(&mq, q, (uint64_t)hq * D, T, qs, 64, B::BM))) return e;
+  if ((e = make_map_2d(&mk, k, (uint64_t)hkv * D, T, ks, 64, B::BN))) return e;
+  if ((e = make_map_2d(&mv, v, (uint64_t)hkv * D, T, vs, 64, B::BN))) return e;
+  if ((e = make_map_2d(&mo, dout, (uint64_t)hq * D, T, os, 64, B::BM))) return e;
+  static bool set = false;
+  if (!set) {
+    KPO_CUDA(cudaFuncSetAttribute(attn_bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, A::SMEM));
+    KPO_CUDA(cudaFuncSetAttribute(attn_bwd_dkdv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, B::SMEM));
+    set = true;
+  }
+  const float2* cs = reinterpret_cast<const float2*>(rope_table);
+  const unsigned ntiles = (unsigned)((T + A::BM - 1) / A::BM);
+  KPO_CUDA(::kpo::pdl_launch(attn_bwd_dq_kernel<D>, dim3((unsigned)hq, ntiles), A::THREADS, A::SMEM, st, mk, mv,
+                             (const __nv_bfloat16*)q, (const __nv_bfloat16*)dout, (const __nv_bfloat16*)o, lse, dvec,
+                             (__nv_bfloat16*)dq, (int)T, hq, hkv, qs, os, dqs, scale, causal, cs));
+  KPO_LAUNCH_CHECK();
+  dim3 grid((unsigned)(split_group ? hq : hkv), (unsigned)((T + B::BN - 1) / B::BN), (unsigned)(qchunks > 1 ? qchunks : 1));
+  KPO_CUDA(::kpo::pdl_launch(attn_bwd_dkdv_kernel<D>, grid, B::THREADS, B::SMEM, st, mq, mk, mv, mo, lse,
+                             (const float*)dvec, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, (int)T, hq, hkv, dks, dvs,
+                             scale, causal, dkv_acc, split_group, qsplit_tiles, cs));
+  KPO_LAUNCH_CHECK();
+  return KPO_OK;
+}
+
 template <int D>
 int bwd_launch(const void* q, const void* k, const void* v, const void* dout, const float* lse, const float* dvec,
                float* dq_acc, void* dk, void* dv, int64_t T, int hq, int hkv, int64_t qs, int64_t ks, int64_t vs,
@@ -1548,6 +2165,23 @@ int bwd_launch(const void* q, const void* k, const void* v, const void* dout, co
   }
 }
 }  // namespace attn_tc
+
+int attn_bwd_tcgen05_split(const void* q, const void* k, const void* v, const void* o, const void* dout,
+                           const float* lse, float* dvec, void* dq, void* dk, void* dv, int64_t T, int hq, int hkv,
+                           int d, int64_t qs, int64_t ks, int64_t vs, int64_t os, int64_t dqs, int64_t dks,
+                           int64_t dvs, float scale, int causal, float* dkv_acc, int split_group, int qsplit_tiles,
+                           int qchunks, cudaStream_t st, const float* rope_table) {
+  if (d == 128)
+    return attn_tc::bwd_split_launch<128>(q, k, v, o, dout, lse, dvec, dq, dk, dv, T, hq, hkv, qs, ks, vs, os, dqs,
+                                          dks, dvs, scale, causal, dkv_acc, split_group, qsplit_tiles, qchunks, st,
+                                          rope_table);
+  if (d == 64 && rope_table == nullptr)
+    return attn_tc::bwd_split_launch<64>(q, k, v, o, dout, lse, dvec, dq, dk, dv, T, hq, hkv, qs, ks, vs, os, dqs,
+                                         dks, dvs, scale, causal, dkv_acc, split_group, qsplit_tiles, qchunks, st,
+                                         rope_table);
+  set_error("attn_bwd two-kernel path: head_dim 64 or 128 (fused rotary: 128)");
+  return KPO_ERR_UNSUPPORTED;
+}
 
 // entry used by attention.cu's kpo_attn_fwd
 int attn_fwd_tcgen05(const void* q, const void* k, const void* v, void* o, float* lse, int64_t T, int hq, int hkv,

@@ -1,5 +1,6 @@
 """Numerics of the hand-written sm_100a kernels against plain PyTorch fp32 references."""
 import math
+import os
 
 import pytest
 import torch
@@ -313,3 +314,22 @@ def test_attention_bwd_rope_fused(cuda, T, hq, hkv):
     torch.cuda.synchronize()
     assert rel_err(d1[:, :qd], ref[:, :qd]) < 1e-2
     assert rel_err(d1[:, qd:], ref[:, qd:]) < 1e-2
+
+
+@pytest.mark.parametrize("shape", ["1024:6:2", "2048:4:1", "512:8:8:64"])
+def test_attention_bwd_variants_match_reference(cuda, shape):
+    """Every attention-backward implementation (selected per process by KPO_ATTN_BWD: 2 = the 64-query
+    single kernel, 3 = the 128-query single kernel, 4 = the dQ + dK/dV two-kernel default) against the
+    same torch fp32 reference (tools/attn_bwd_ab.py runs each in its own process)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    variants = "3,4" if shape.endswith(":64") else "2,3,4"
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "attn_bwd_ab.py"), "--variants", variants,
+                        "--shapes", shape, "--reps", "2"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    for key, v in res.items():
+        assert "rel" in v, (key, v)
+        assert all(e < 2e-2 for e in v["rel"].values()), (key, v)

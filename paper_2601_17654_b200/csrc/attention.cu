@@ -570,9 +570,11 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* o
   using CF = BwdCfg<D>;
   float* dq_acc = (float*)ws;
   float* dvec = dq_acc + T * hq * D;
-  // KPO_ATTN_BWD: 4 (default) = two kernels (dQ, then dK / dV; no dQ reduction, no pre / post kernels),
-  // 2 / 3 = the single-kernel 64- / 128-query tcgen05 backward, 1 = mma.sync (A/B baselines)
-  static const int variant = getenv("KPO_ATTN_BWD") ? atoi(getenv("KPO_ATTN_BWD")) : 4;
+  // KPO_ATTN_BWD: unset = the single-kernel tcgen05 backward (64-query steps for head_dim 128, 128-query
+  // steps for 64); 2 / 3 force one of them; 4 = two kernels (dQ, then dK / dV: no cross-CTA dQ
+  // reduction, so dQ is bitwise deterministic, and no pre / post kernels; measured 1.33x slower at
+  // config 1); 1 = mma.sync (A/B baseline)
+  static const int variant = getenv("KPO_ATTN_BWD") ? atoi(getenv("KPO_ATTN_BWD")) : 0;
   const bool two_kernels = use_tc && T % 8 == 0 && variant == 4;
   if (!two_kernels) {
     const int64_t threads = T * hq * (D / 8);

@@ -1488,7 +1488,9 @@ __global__ void __launch_bounds__(Bwd3<D>::THREADS, 1)
 }
 
 // =====================================================================================
-// Backward as two kernels (default for head_dim 128; KPO_ATTN_BWD=4):
+// Backward as two kernels (KPO_ATTN_BWD=4; deterministic dQ, measured slower than the 64-query kernel:
+// with P / dS aliased over S / dP in TMEM, each step's softmax sits between the dV and S MMAs, and
+// the dQ kernel's short CTAs pay their prologue / epilogue serially):
 //   attn_bwd_dq_kernel    one CTA per (q head, 128 queries), loops over the causal key tiles:
 //                           S = Q K^T, dP = dO V^T, dS = P (dP - D), dQ += dS K
 //                         Q and dO stay in TMEM (the A operands of S and dP), dS is written over dP

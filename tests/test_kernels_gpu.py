@@ -333,3 +333,22 @@ def test_attention_bwd_variants_match_reference(cuda, shape):
     for key, v in res.items():
         assert "rel" in v, (key, v)
         assert all(e < 2e-2 for e in v["rel"].values()), (key, v)
+
+
+def test_attention_bwd_two_kernel_path_is_deterministic(cuda):
+    """KPO_ATTN_BWD=4 (dQ kernel + dK/dV kernel) reduces nothing across CTAs in grouped mode, so two
+    processes on the same seeded inputs produce bit-identical dq / dk / dv."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, KPO_ATTN_BWD="4")
+    shas = []
+    for _ in range(2):
+        r = subprocess.run([sys.executable, os.path.join(root, "tools", "attn_bwd_ab.py"), "--child", "2048:8:2",
+                            "--reps", "2"], capture_output=True, text=True, timeout=600, env=env)
+        assert r.returncode == 0, r.stderr[-2000:]
+        line = json.loads(r.stdout.strip().splitlines()[-1])
+        assert all(e < 2e-2 for e in line["rel"].values()), line
+        shas.append(line["sha"])
+    assert shas[0] == shas[1], shas

@@ -54,7 +54,11 @@ def child(T, hq, hkv, reps, d=128):
     errs = {"dq": rel(dqkv[:, :hq * d], qh.grad.transpose(0, 1).reshape(T, -1)),
             "dk": rel(dqkv[:, hq * d:(hq + hkv) * d], kh.grad.transpose(0, 1).reshape(T, -1)),
             "dv": rel(dqkv[:, (hq + hkv) * d:], vh.grad.transpose(0, 1).reshape(T, -1))}
-    print(json.dumps({"ms": round(ms, 4), "tflops": round(fl / ms / 1e9, 1), "rel": {k: round(x, 5) for k, x in errs.items()}}))
+    import hashlib
+    run()  # one more call on the same inputs: a deterministic backward reproduces its bits
+    digest = hashlib.sha256(dqkv.contiguous().view(torch.int16).cpu().numpy().tobytes()).hexdigest()[:16]
+    print(json.dumps({"ms": round(ms, 4), "tflops": round(fl / ms / 1e9, 1),
+                      "rel": {k: round(x, 5) for k, x in errs.items()}, "sha": digest}))
 
 
 def main():

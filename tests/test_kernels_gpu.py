@@ -342,7 +342,7 @@ def test_attention_bwd_two_kernel_path_is_deterministic(cuda):
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, KPO_ATTN_BWD="4")
+    env = dict(os.environ, KPO_ATTN_BWD="4", KPO_ATTN_BWD_SPLIT="0")  # grouped mode: no dK / dV atomics
     shas = []
     for _ in range(2):
         r = subprocess.run([sys.executable, os.path.join(root, "tools", "attn_bwd_ab.py"), "--child", "2048:8:2",

@@ -209,6 +209,12 @@ int kpo_set_launch_completion_event(kpo_comm* c, void* launched_event);
  * overlap starts instantly, simgpu.py:217-221). */
 int kpo_probe_launch_completion(void* launched_event, void* stream);
 
+/* SM blocker for solo-kernel timing at a reduced SM count (reference kernel_duration(k, f, sms),
+ * simgpu.py:144-168, whose `sms` argument the executor realises as "the SMs the collective leaves"):
+ * `ncta` CTAs that each hold a whole SM (full opt-in shared memory) spin for `spin_ns` on `stream`;
+ * `launched_event` (cudaEvent_t, may be null) completes once all of them are resident. */
+int kpo_sm_blocker(int ncta, int64_t spin_ns, void* launched_event, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

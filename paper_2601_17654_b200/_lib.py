@@ -81,6 +81,7 @@ SIGNATURES = {
     "kpo_comm_trace": (_i32, [_c_void_p, _c_void_p, _i32]),
     "kpo_set_launch_completion_event": (_i32, [_c_void_p, _c_void_p]),
     "kpo_probe_launch_completion": (_i32, [_c_void_p, _c_void_p]),
+    "kpo_sm_blocker": (_i32, [_i32, _i64, _c_void_p, _c_void_p]),
 }
 
 
@@ -108,6 +109,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
             raise KpoUnavailable(f"{path} not built; run __graft_entry__.build() (make -C csrc)")
         lib = ctypes.CDLL(path)
         for name, (res, args) in SIGNATURES.items():
+            if path != os.path.join(_HERE, "libkpo.so") and not hasattr(lib, name):
+                continue  # an older build loaded through KPO_LIB_PATH for a same-box A/B
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

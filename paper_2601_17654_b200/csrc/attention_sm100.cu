@@ -509,13 +509,13 @@ __global__ void __launch_bounds__(384, 1)
           sv[i] = (key >= T || (causal && key > q)) ? -INFINITY : sv[i];
         }
       }
+      // row max: 8 independent FMNMX3 chains (two elements per instruction)
       float pm[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) pm[e] = sv[e];
 #pragma unroll
-      for (int i = 8; i < BN; ++i) pm[i & 7] = fmaxf(pm[i & 7], sv[i]);
-      const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
-                             fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7]))) * scale_log2;
+      for (int i = 8; i < BN; i += 2) pm[(i >> 1) & 7] = fmax3(pm[(i >> 1) & 7], sv[i], sv[i + 1]);
+      const float mx = fmaxf(fmax3(fmax3(pm[0], pm[1], pm[2]), fmax3(pm[3], pm[4], pm[5]), pm[6]), pm[7]) * scale_log2;
       float corr = 1.f;
       bool rescale = false;
       if (mx > m_run + 8.f) {
@@ -542,21 +542,21 @@ __global__ void __launch_bounds__(384, 1)
         if (g == 0 && j > 0) named_bar(1, 256);
         if (g == 1 && j < n_g[0]) named_bar(2, 256);
       }
-      float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      // exponent arguments with FFMA2 and row sums with FADD2, two keys per instruction
+      uint64_t ps2[4] = {0, 0, 0, 0};
+      const uint64_t sc2 = f2_pack(scale_log2, scale_log2), nm2 = f2_pack(neg_m, neg_m);
       constexpr int PC = BN / 2 / NP;  // packed bf16-pair columns per P part
 #pragma unroll
       for (int pp = 0; pp < NP; ++pp) {  // BN / NP keys -> PC columns of bf16 pairs over S_g
         uint32_t pk[PC];
 #pragma unroll
         for (int c = 0; c < PC; ++c) {
-          float p[2];
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int i = pp * 2 * PC + c * 2 + e;
-            p[e] = ex2(fmaf(sv[i], scale_log2, neg_m));
-            ps[i & 7] += p[e];
-          }
-          pk[c] = pack_bf16x2(p[0], p[1]);
+          const int i = pp * 2 * PC + c * 2;
+          float x0, x1;
+          f2_unpack(f2_fma(f2_pack(sv[i], sv[i + 1]), sc2, nm2), x0, x1);
+          const float p0 = ex2(x0), p1 = ex2(x1);
+          ps2[c & 3] = f2_add(ps2[c & 3], f2_pack(p0, p1));
+          pk[c] = pack_bf16x2(p0, p1);
         }
         if constexpr (PC == 32) tmem_st32(s_addr + pp * PC, pk);
         else tmem_st16(s_addr + pp * PC, pk);
@@ -570,6 +570,9 @@ __global__ void __launch_bounds__(384, 1)
         if (g == 0) asm volatile("bar.arrive 2, 256;" ::: "memory");
         if (g == 1 && j + 1 < n_g[0]) asm volatile("bar.arrive 1, 256;" ::: "memory");
       }
+      float ps[8];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) f2_unpack(ps2[c], ps[2 * c], ps[2 * c + 1]);
       const float lsum = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
       l_run = l_run * corr + lsum;
     }
@@ -921,25 +924,28 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
       // CTA-uniform: does this tile need the causal / tail mask at all?
       const bool tile_mask = (causal && m0 < n0 + BN - 1) || n0 + BN > T || m0 + BM > T;
       uint32_t pp[HC / 2], qq[HC / 2];
+      // two query columns per FFMA2 / FMUL2 / FADD2: x = S scale - lse log2e, P = 2^x, dS = P (dP - D)
+      const uint64_t sc2 = f2_pack(scale_log2, scale_log2), nlg2 = f2_pack(-kLog2e, -kLog2e);
 #pragma unroll
       for (int i = 0; i < HC; i += 2) {
+        uint64_t nl2, dd2;
+        asm volatile("ld.shared.b64 %0, [%1];" : "=l"(nl2) : "r"(sst + i * 4));
+        asm volatile("ld.shared.b64 %0, [%1];" : "=l"(dd2) : "r"(sst + BM * 4 + i * 4));
         float p2[2], d2[2];
-        float nl[2], dd[2];
-        asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(nl[0]), "=f"(nl[1]) : "r"(sst + i * 4));
-        asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(dd[0]), "=f"(dd[1]) : "r"(sst + BM * 4 + i * 4));
+        f2_unpack(f2_fma(f2_pack(sv[i], sv[i + 1]), sc2, f2_mul(nl2, nlg2)), p2[0], p2[1]);
+        if (!(ablate & 4)) {
+          p2[0] = ex2(p2[0]);
+          p2[1] = ex2(p2[1]);
+        }
+        f2_unpack(f2_mul(f2_pack(p2[0], p2[1]), f2_sub(f2_pack(dp[i], dp[i + 1]), dd2)), d2[0], d2[1]);
+        if (tile_mask) {
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const float xe = fmaf(sv[i + e], scale_log2, -nl[e] * kLog2e);
-          float pe = (ablate & 4) ? xe : ex2(xe);
-          float de = pe * (dp[i + e] - dd[e]);
-          if (tile_mask) {
+          for (int e = 0; e < 2; ++e) {
             const int q = m0 + half * HC + i + e;
             const bool z = key >= T || q >= T || (causal && q < key);
-            pe = z ? 0.f : pe;
-            de = z ? 0.f : de;
+            p2[e] = z ? 0.f : p2[e];
+            d2[e] = z ? 0.f : d2[e];
           }
-          p2[e] = pe;
-          d2[e] = de;
         }
         pp[i / 2] = pack_bf16x2(p2[0], p2[1]);
         qq[i / 2] = pack_bf16x2(d2[0], d2[1]);

@@ -52,3 +52,55 @@ extern "C" int kpo_probe_launch_completion(void* event, void* stream) {
   KPO_CUDA(cudaEventQuery((cudaEvent_t)event));
   return KPO_OK;
 }
+
+// SM blocker: `ncta` CTAs, each holding the whole opt-in shared memory (so exactly one per SM and no
+// other CTA can share its SM), spinning on the global timer for `spin_ns`.  Measures a kernel's time
+// on (num_sms - ncta) SMs without touching the kernel (reference kernel_duration(k, f, sms),
+// simgpu.py:144-168, tools/unit_sm_sweep.py).  `launched_event` (cudaEvent_t, may be null) is
+// recorded with cudaLaunchAttributeLaunchCompletionEvent: once it completes, every blocker CTA is
+// resident.
+__global__ void kpo_sm_blocker_kernel(unsigned long long spin_ns) {
+  extern __shared__ uint8_t kpo_blocker_smem[];
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  if (threadIdx.x == 0) kpo_blocker_smem[0] = 0;
+  do {
+    __nanosleep(500);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < spin_ns);
+}
+
+extern "C" int kpo_sm_blocker(int ncta, int64_t spin_ns, void* launched_event, void* stream) {
+  KPO_CHECK_ARG(ncta >= 0 && spin_ns >= 0, "sm_blocker: ncta and spin_ns must be >= 0");
+  if (ncta == 0) return KPO_OK;
+  int dev = 0, smem = 0;
+  KPO_CUDA(cudaGetDevice(&dev));
+  KPO_CUDA(cudaDeviceGetAttribute(&smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  KPO_CUDA(cudaFuncSetAttribute(kpo_sm_blocker_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)ncta);
+  cfg.blockDim = dim3(32);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = (cudaStream_t)stream;
+  // like the collectives (comm.cu): an even count is launched as 2-CTA clusters, so it takes whole
+  // TPCs and leaves whole TPCs to the CTA-pair GEMMs
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (ncta % 2 == 0) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (launched_event) {
+    attr[na].id = cudaLaunchAttributeLaunchCompletionEvent;
+    attr[na].val.launchCompletionEvent.event = (cudaEvent_t)launched_event;
+    attr[na].val.launchCompletionEvent.flags = 0;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  KPO_CUDA(cudaLaunchKernelEx(&cfg, kpo_sm_blocker_kernel, (unsigned long long)spin_ns));
+  return KPO_OK;
+}

@@ -26,6 +26,15 @@ def child(T, hq, hkv, reps, d=128):
     lse = torch.empty(hq, T, device=dev)
     scale = 1 / math.sqrt(d)
     ops.attn_fwd(q, k, v, o, lse, T, hq, hkv, d, scale)
+    for _ in range(3):
+        ops.attn_fwd(q, k, v, o, lse, T, hq, hkv, d, scale)
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record()
+    for _ in range(reps):
+        ops.attn_fwd(q, k, v, o, lse, T, hq, hkv, d, scale)
+    f1.record()
+    torch.cuda.synchronize()
+    fwd_ms = f0.elapsed_time(f1) / reps
     dout = torch.randn(T, hq * d, device=dev, generator=g).bfloat16()
     dqkv = torch.empty_like(qkv)
     ws = ops.attn_bwd_workspace(T, hq, hkv, d, dev)
@@ -57,7 +66,8 @@ def child(T, hq, hkv, reps, d=128):
     import hashlib
     run()  # one more call on the same inputs: a deterministic backward reproduces its bits
     digest = hashlib.sha256(dqkv.contiguous().view(torch.int16).cpu().numpy().tobytes()).hexdigest()[:16]
-    print(json.dumps({"ms": round(ms, 4), "tflops": round(fl / ms / 1e9, 1),
+    print(json.dumps({"ms": round(ms, 4), "tflops": round(fl / ms / 1e9, 1), "fwd_ms": round(fwd_ms, 4),
+                      "fwd_tflops": round(fl / 2.5 / fwd_ms / 1e9, 1),
                       "rel": {k: round(x, 5) for k, x in errs.items()}, "sha": digest}))
 
 
@@ -75,7 +85,11 @@ def main():
     for shape in a.shapes.split(","):
         for var in a.variants.split(","):
             # "3+dv": variant 3 with the dV-before-dP MMA order (KPO_ATTN_BWD3_DVFIRST=1)
-            env = dict(os.environ, KPO_ATTN_BWD=var.split("+")[0], KPO_ATTN_BWD3_DVFIRST="1" if "+dv" in var else "0")
+            # "2@base": variant 2 of the library at tools/ab/libkpo_base.so (an older build, same-box A/B)
+            v, _, lib = var.partition("@")
+            env = dict(os.environ, KPO_ATTN_BWD=v)
+            if lib:
+                env["KPO_LIB_PATH"] = os.path.join(ROOT, "tools", "ab", f"libkpo_{lib}.so")
             r = subprocess.run([sys.executable, __file__, "--child", shape, "--reps", str(a.reps)], env=env,
                                capture_output=True, text=True, timeout=600)
             try:

@@ -15,8 +15,10 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
 }
+// Watchdog: a wait that has not completed after 2^26 try_wait rounds (seconds; every legitimate wait
+// here is well under a millisecond) traps, so a pipeline bug fails the launch instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  uint32_t done = 0;
+  uint32_t done = 0, spins = 0;
   while (!done) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -25,6 +27,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "=r"(done)
         : "r"(bar), "r"(parity)
         : "memory");
+    if (!done && ++spins == (1u << 26)) __trap();
   }
 }
 // non-blocking probe of an mbarrier phase

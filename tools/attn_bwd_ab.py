@@ -86,8 +86,12 @@ def main():
         for var in a.variants.split(","):
             # "3+dv": variant 3 with the dV-before-dP MMA order (KPO_ATTN_BWD3_DVFIRST=1)
             # "2@base": variant 2 of the library at tools/ab/libkpo_base.so (an older build, same-box A/B)
-            v, _, lib = var.partition("@")
+            # "2+f2": also KPO_ATTN_FWD=2 (the forward variant the child times)
+            var_b, _, fwd = var.partition("+f")
+            v, _, lib = var_b.partition("@")
             env = dict(os.environ, KPO_ATTN_BWD=v)
+            if fwd:
+                env["KPO_ATTN_FWD"] = fwd
             if lib:
                 env["KPO_LIB_PATH"] = os.path.join(ROOT, "tools", "ab", f"libkpo_{lib}.so")
             r = subprocess.run([sys.executable, __file__, "--child", shape, "--reps", str(a.reps)], env=env,

@@ -95,7 +95,7 @@ def main():
             if lib:
                 env["KPO_LIB_PATH"] = os.path.join(ROOT, "tools", "ab", f"libkpo_{lib}.so")
             r = subprocess.run([sys.executable, __file__, "--child", shape, "--reps", str(a.reps)], env=env,
-                               capture_output=True, text=True, timeout=600)
+                               capture_output=True, text=True, timeout=240)
             try:
                 res[f"{shape}/v{var}"] = json.loads(r.stdout.strip().splitlines()[-1])
             except Exception:

@@ -607,306 +607,6 @@ __global__ void __launch_bounds__(384, 1)
   if (warp == 9) tmem_dealloc(tmem, 512);
 }
 
-// -------------------------------------------------------------------------------------------------
-// Forward, two Q tiles per CTA and two softmax warps per TMEM lane quarter and Q tile (16 softmax
-// warps, each thread half of a row: 64 keys).  Per KV tile the two groups together exponentiate
-// 2 x 128 x 128 scores, as much MUFU work as the tile's four MMAs take on the tensor core; with one
-// warp per quarter and group (the kernel above) each warp's exp phase (128 keys per thread) sits
-// between its S and P.V MMAs.  Halving it per warp shortens each group's S -> softmax -> P -> P.V
-// turn-around; the row max is exchanged between the two halves through shared memory.
-//   warps 0-15 softmax: group g = warp / 8 (Q tile), half h = (warp / 4) % 2 (keys 64h .. 64h+63),
-//              lane quarter = warp % 4                                           (setmaxnreg 104)
-//   warp 16    TMA producer; warp 17 TMEM allocator + MMA issuer; 18-19 idle   (setmaxnreg 40)
-//   TMEM / MMA order as above: S0 0..127, S1 128..255 (P_g over the first 64 columns: half h writes
-//   the 32 packed columns of its keys after both halves have read S), O0 256..383, O1 384..511.
-template <int D>
-struct Fwd3 {
-  static constexpr int BM = 128, BN = 128;
-  static constexpr int Q_BYTES = BM * D * 2;
-  static constexpr int KV_BYTES = BN * D * 2;
-  static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
-  static constexpr int OFF_V = OFF_K + 2 * KV_BYTES;
-  static constexpr int OFF_BAR = OFF_V + 2 * KV_BYTES;
-  static constexpr int OFF_XCH = OFF_BAR + 256;  // [2 parities][2 groups][2 halves][BM] partial row max
-  static constexpr int OFF_LX = OFF_XCH + 2 * 2 * 2 * BM * 4;  // [2 groups][2 halves][BM] partial row sum
-  static constexpr int SMEM = OFF_LX + 2 * 2 * BM * 4 + 1024;
-  static constexpr int COL_S0 = 0, COL_S1 = 128, COL_O0 = 256, COL_O1 = 384;
-  static constexpr int THREADS = 640;
-};
-
-template <int D>
-__global__ void __launch_bounds__(640, 1)
-    attn_fwd_tc3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                        const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ o,
-                        float* __restrict__ lse, int T, int hq, int hkv, int64_t os, float scale_log2, int causal) {
-  ::kpo::pdl_launch_dependents();
-  using C = Fwd3<D>;
-  constexpr int BM = C::BM, BN = C::BN, KSUB = D / 64;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-  uint64_t* q_full = bar + 0;
-  uint64_t* k_full = bar + 1;    // [2]
-  uint64_t* k_empty = bar + 3;   // [2]
-  uint64_t* v_full = bar + 5;    // [2]
-  uint64_t* v_empty = bar + 7;   // [2]
-  uint64_t* s_full = bar + 9;    // [2] per Q tile
-  uint64_t* pv_done = bar + 13;  // [2] per Q tile
-  uint64_t* p_full = bar + 15;   // [2 halves][2 Q tiles] (4 warps each): P of keys 64h .. 64h+63 in TMEM
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 19);
-  float* xch = reinterpret_cast<float*>(smem + C::OFF_XCH);
-  float* lx = reinterpret_cast<float*>(smem + C::OFF_LX);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int mblk = gridDim.y - 1 - blockIdx.y;  // heavy (late) causal rows first
-  const int h = blockIdx.x;
-  const int kvh = h / (hq / hkv);
-  const int m0 = mblk * 2 * BM;
-  const int tiles_all = (T + BN - 1) / BN;
-  int n_g[2];
-#pragma unroll
-  for (int g = 0; g < 2; ++g) {
-    n_g[g] = tiles_all;
-    if (causal) n_g[g] = min(tiles_all, (m0 + g * BM + BM + BN - 1) / BN);
-    if (m0 + g * BM >= T) n_g[g] = 0;
-  }
-  const int n_all = max(n_g[0], n_g[1]);
-
-  if (threadIdx.x == 0) {
-    mbar_init(smem_u32(q_full), 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(smem_u32(&k_full[i]), 1);
-      mbar_init(smem_u32(&k_empty[i]), 1);
-      mbar_init(smem_u32(&v_full[i]), 1);
-      mbar_init(smem_u32(&v_empty[i]), 1);
-      mbar_init(smem_u32(&s_full[i]), 1);
-      mbar_init(smem_u32(&pv_done[i]), 1);
-      mbar_init(smem_u32(&p_full[i]), 4);
-      mbar_init(smem_u32(&p_full[2 + i]), 4);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 17) tmem_alloc(smem_u32(tmem_slot), 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (*tmem_slot != 0) __trap();
-  ::kpo::pdl_wait();
-  constexpr uint32_t tmem = 0;
-  const uint32_t sQ = smem_u32(smem + C::OFF_Q), sK = smem_u32(smem + C::OFF_K), sV = smem_u32(smem + C::OFF_V);
-
-  if (warp >= 16) {
-    // 640 threads launch at 96 registers and setmaxnreg only moves registers inside the CTA's own
-    // allocation: this warpgroup frees 128 x 56, the four softmax warpgroups take 512 x 8 of them
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
-    if (warp == 16 && lane == 0) {
-      // ------------------------------------------------------------ TMA producer
-      mbar_arrive_expect_tx(smem_u32(q_full), 2 * C::Q_BYTES);
-#pragma unroll
-      for (int g = 0; g < 2; ++g)
-#pragma unroll
-        for (int kb = 0; kb < KSUB; ++kb)
-          tma_load_2d(sQ + g * C::Q_BYTES + kb * BM * 128, &tmQ, smem_u32(q_full), h * D + kb * 64, m0 + g * BM);
-      for (int j = 0; j < n_all; ++j) {
-        const int s = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
-        mbar_wait(smem_u32(&k_empty[s]), ph ^ 1);
-        uint32_t fb = smem_u32(&k_full[s]);
-        mbar_arrive_expect_tx(fb, C::KV_BYTES);
-#pragma unroll
-        for (int kb = 0; kb < KSUB; ++kb)
-          tma_load_2d(sK + s * C::KV_BYTES + kb * BN * 128, &tmK, fb, kvh * D + kb * 64, j * BN);
-        mbar_wait(smem_u32(&v_empty[s]), ph ^ 1);
-        fb = smem_u32(&v_full[s]);
-        mbar_arrive_expect_tx(fb, C::KV_BYTES);
-#pragma unroll
-        for (int kb = 0; kb < KSUB; ++kb)
-          tma_load_2d(sV + s * C::KV_BYTES + kb * BN * 128, &tmV, fb, kvh * D + kb * 64, j * BN);
-      }
-    } else if (warp == 17) {
-      // ------------------------------------------------------------ MMA issuer (as attn_fwd_tc2_kernel)
-      constexpr uint32_t ID_S = idesc_bf16(BM, BN, false, false);
-      constexpr uint32_t ID_O = idesc_bf16(BM, D, false, true);
-      mbar_wait(smem_u32(q_full), 0);
-      auto issue_s = [&](int g, int j) {
-        const int s = j & 1;
-        const uint32_t q_k = desc_lo(sQ + g * C::Q_BYTES, 16), k_k = desc_lo(sK + s * C::KV_BYTES, 16);
-        const uint32_t d_s = tmem + (g ? C::COL_S1 : C::COL_S0);
-#pragma unroll
-        for (int kb = 0; kb < KSUB; ++kb)
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            tc_mma_lo_w(d_s, q_k + kb * (BM * 8) + k * 2, k_k + kb * (BN * 8) + k * 2, ID_S, (kb | k) ? 1u : 0u);
-        tc_commit_w(smem_u32(&s_full[g]));
-      };
-      auto issue_pv = [&](int g, int j) {
-        const int s = j & 1;
-        const uint32_t v_mn = desc_lo(sV + s * C::KV_BYTES, BN * 128);
-        const uint32_t p_t = tmem + (g ? C::COL_S1 : C::COL_S0);
-        const uint32_t o_t = tmem + (g ? C::COL_O1 : C::COL_O0);
-#pragma unroll
-        for (int pp = 0; pp < 2; ++pp) {
-          mbar_wait(smem_u32(&p_full[pp * 2 + g]), j & 1);
-          tc_fence_after();
-#pragma unroll
-          for (int kk = pp * BN / 32; kk < (pp + 1) * BN / 32; ++kk)
-            tc_mma_ts_lo_w(o_t, p_t + kk * 8, v_mn + kk * 128, ID_O, (j > 0 || kk > 0) ? 1u : 0u);
-        }
-        tc_commit_w(smem_u32(&pv_done[g]));
-      };
-      mbar_wait(smem_u32(&k_full[0]), 0);
-      tc_fence_after();
-      if (n_g[0] > 0) issue_s(0, 0);
-      if (n_g[1] > 0) issue_s(1, 0);
-      tc_commit_w(smem_u32(&k_empty[0]));
-      for (int j = 0; j < n_all; ++j) {
-        const int s = j & 1;
-        const bool more = j + 1 < n_all;
-        mbar_wait(smem_u32(&v_full[s]), (j >> 1) & 1);
-        if (more) mbar_wait(smem_u32(&k_full[s ^ 1]), ((j + 1) >> 1) & 1);
-        tc_fence_after();
-        bool need0 = j < n_g[0], need1 = j < n_g[1];
-        while (need0 || need1) {
-          int g = need0 ? 0 : 1;
-          if (need0 && need1) {
-            while (true) {
-              if (mbar_test(smem_u32(&p_full[0]), j & 1)) { g = 0; break; }
-              if (mbar_test(smem_u32(&p_full[1]), j & 1)) { g = 1; break; }
-            }
-          }
-          issue_pv(g, j);
-          if (j + 1 < (g ? n_g[1] : n_g[0])) issue_s(g, j + 1);
-          if (g == 0) need0 = false;
-          else need1 = false;
-        }
-        tc_commit_w(smem_u32(&v_empty[s]));
-        if (more) tc_commit_w(smem_u32(&k_empty[s ^ 1]));
-      }
-    }
-  } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 104;");
-    // ------------------------------------------------------------ softmax: group g, half hf, one half-row per thread
-    const int g = warp >> 3;
-    const int hf = (warp >> 2) & 1;
-    const int quarter = warp & 3;
-    const int r = quarter * 32 + lane;
-    const int q = m0 + g * BM + r;
-    const uint32_t lane_addr = tmem + ((uint32_t)(quarter * 32) << 16);
-    const uint32_t s_addr = lane_addr + (g ? C::COL_S1 : C::COL_S0);
-    const uint32_t o_addr = lane_addr + (g ? C::COL_O1 : C::COL_O0);
-    const int bar_id = 1 + g * 4 + quarter;  // the two halves of these 32 rows (64 threads)
-    const int ng = g ? n_g[1] : n_g[0];  // (a select: a runtime-indexed array would live in local memory)
-    float m_run = -INFINITY, l_run = 0.f;
-    for (int j = 0; j < ng; ++j) {
-      mbar_wait(smem_u32(&s_full[g]), j & 1);
-      tc_fence_after();
-      float sv[BN / 2];
-      tmem_ld32_nowait(s_addr + 64 * hf, reinterpret_cast<uint32_t*>(sv));
-      tmem_ld32_nowait(s_addr + 64 * hf + 32, reinterpret_cast<uint32_t*>(sv + 32));
-      tmem_wait_ld();
-      const int k0 = j * BN + 64 * hf;
-      const bool mask = (causal && j * BN + BN - 1 > m0 + g * BM) || (j * BN + BN > T);  // group-uniform
-      if (mask) {
-#pragma unroll
-        for (int i = 0; i < BN / 2; ++i) {
-          const int key = k0 + i;
-          sv[i] = (key >= T || (causal && key > q)) ? -INFINITY : sv[i];
-        }
-      }
-      float pm[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) pm[e] = sv[e];
-#pragma unroll
-      for (int i = 8; i < BN / 2; i += 2) pm[(i >> 1) & 7] = fmax3(pm[(i >> 1) & 7], sv[i], sv[i + 1]);
-      const float mh = fmaxf(fmax3(fmax3(pm[0], pm[1], pm[2]), fmax3(pm[3], pm[4], pm[5]), pm[6]), pm[7]);
-      // exchange the half-row maxima (both halves have read their S columns after this barrier, so
-      // either may then overwrite the first 64 columns with P)
-      float* xp = xch + ((j & 1) * 4 + g * 2) * BM;
-      xp[hf * BM + r] = mh;
-      tc_fence_before();
-      named_bar(bar_id, 64);
-      tc_fence_after();
-      const float mx = fmaxf(mh, xp[(hf ^ 1) * BM + r]) * scale_log2;
-      float corr = 1.f;
-      bool rescale = false;
-      if (mx > m_run + 8.f) {
-        corr = (m_run == -INFINITY) ? 0.f : ex2(m_run - mx);
-        rescale = (j > 0);
-        m_run = mx;
-      }
-      // O_g is stable here (S_g(j) complete implies PV_g(j-1) complete); each half rescales its 64
-      // head-dim columns, and both finish before either releases P (the P.V MMAs write all of O)
-      if (__any_sync(0xffffffffu, rescale)) {
-#pragma unroll 1
-        for (int c = 0; c < D / 64; ++c) {
-          uint32_t ov[32];
-          tmem_ld32_nowait(o_addr + (D / 2) * hf + c * 32, ov);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * corr);
-          tmem_st32(o_addr + (D / 2) * hf + c * 32, ov);
-        }
-        tmem_wait_st();
-        tc_fence_before();
-        named_bar(bar_id, 64);
-      }
-      const float neg_m = -m_run;
-      uint64_t ps2[4] = {0, 0, 0, 0};
-      const uint64_t sc2 = f2_pack(scale_log2, scale_log2), nm2 = f2_pack(neg_m, neg_m);
-      uint32_t pk[32];
-#pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        float x0, x1;
-        f2_unpack(f2_fma(f2_pack(sv[2 * c], sv[2 * c + 1]), sc2, nm2), x0, x1);
-        const float p0 = ex2(x0), p1 = ex2(x1);
-        ps2[c & 3] = f2_add(ps2[c & 3], f2_pack(p0, p1));
-        pk[c] = pack_bf16x2(p0, p1);
-      }
-      tmem_st32(s_addr + 32 * hf, pk);  // P of keys 64hf .. 64hf+63 -> packed columns 32hf .. 32hf+31
-      tmem_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&p_full[hf * 2 + g]));
-      float ps[8];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) f2_unpack(ps2[c], ps[2 * c], ps[2 * c + 1]);
-      l_run = l_run * corr + (((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7])));
-    }
-    if (ng > 0) {
-      // ------------------------------------------------------------ epilogue: half hf writes O columns
-      lx[(g * 2 + hf) * BM + r] = l_run;
-      named_bar(bar_id, 64);
-      const float l_all = l_run + lx[(g * 2 + (hf ^ 1)) * BM + r];
-      mbar_wait(smem_u32(&pv_done[g]), (ng - 1) & 1);
-      tc_fence_after();
-      const float inv = 1.f / l_all;
-      const bool row_ok = q < T;
-      __nv_bfloat16* orow = o + (int64_t)q * os + (int64_t)h * D + (D / 2) * hf;
-#pragma unroll 1
-      for (int c = 0; c < D / 64; ++c) {
-        uint32_t ov[32];
-        tmem_ld32_nowait(o_addr + (D / 2) * hf + c * 32, ov);
-        tmem_wait_ld();
-        if (row_ok) {
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            float f[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(ov[v * 8 + e]) * inv;
-            *reinterpret_cast<uint4*>(orow + c * 32 + v * 8) = pack8(f);
-          }
-        }
-      }
-      if (row_ok && hf == 0) lse[(int64_t)h * T + q] = (m_run + __log2f(l_all)) / kLog2e;
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (warp == 17) tmem_dealloc(tmem, 512);
-}
-
 template <int D>
 int fwd_launch(const void* q, const void* k, const void* v, void* o, float* lse, int64_t T, int hq, int hkv,
                int64_t qs, int64_t ks, int64_t vs, int64_t os, float scale, int causal, cudaStream_t st) {
@@ -926,16 +626,6 @@ int fwd_launch(const void* q, const void* k, const void* v, void* o, float* lse,
     return KPO_OK;
   };
   static const int variant = getenv("KPO_ATTN_FWD") ? atoi(getenv("KPO_ATTN_FWD")) : 2;
-  if (variant == 3) {  // two Q tiles, two softmax warps per lane quarter and tile
-    using C3 = Fwd3<D>;
-    dim3 grid3((unsigned)hq, (unsigned)((T + 2 * C3::BM - 1) / (2 * C3::BM)));
-    auto kern3 = attn_fwd_tc3_kernel<D>;
-    KPO_CUDA(cudaFuncSetAttribute(kern3, cudaFuncAttributeMaxDynamicSharedMemorySize, C3::SMEM));
-    KPO_CUDA(::kpo::pdl_launch(kern3, grid3, C3::THREADS, C3::SMEM, st, mq, mk, mv, (__nv_bfloat16*)o, lse, (int)T,
-                               hq, hkv, os, scale * kLog2e, causal));
-    KPO_LAUNCH_CHECK();
-    return KPO_OK;
-  }
   if (variant == 2 && D == 128) {
     using C2 = Fwd2<D>;
     dim3 grid2((unsigned)hq, (unsigned)((T + 2 * C2::BM - 1) / (2 * C2::BM)));

@@ -29,7 +29,10 @@ dys = [pin(x["dy"]).copy_(x["dy"].cpu()) for x in layer.nb]
 dxs = [pin(x["dx"]) for x in layer.nb]
 
 
-def wall(fn):
+clk = {}
+
+
+def wall(fn, key=None):
     for _ in range(3):
         fn()
     run.drain()
@@ -39,7 +42,11 @@ def wall(fn):
         fn()
     run.drain()
     torch.cuda.synchronize()
-    return (time.perf_counter() - t0) / a.n * 1e3
+    t1 = time.perf_counter()
+    if key:  # median SM clock and power over the window (NVML, engine sampler)
+        c = eng.sampler.clocks_summary(t0, t1)
+        clk.setdefault(key, []).append((c.get("sm_mhz"), c.get("power_w_max")))
+    return (t1 - t0) / a.n * 1e3
 
 
 comp = eng.exec.compute
@@ -67,8 +74,8 @@ variants = {"step_only_ms": run.step, "pipelined_e2e_ms": lambda: run.step_host_
 res = {k: [] for k in variants}
 for _ in range(3):  # interleaved rounds: the box's power / thermal drift hits every variant alike
     for k, fn in variants.items():
-        res[k].append(wall(fn))
+        res[k].append(wall(fn, k))
         if k != "pipelined_e2e_ms":
             h2d.synchronize()
             d2h.synchronize()
-print(json.dumps({k: [round(x, 4) for x in v] for k, v in res.items()}))
+print(json.dumps({"ms": {k: [round(x, 4) for x in v] for k, v in res.items()}, "sm_mhz_power_w": clk}))

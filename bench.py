@@ -514,9 +514,28 @@ def run_kpo(args):
             for k, v in ex_rows.items():
                 v["time_vs_default"] = round(v["s_per_iter"] / d0["s_per_iter"] - 1, 5)
                 v["energy_vs_default"] = round(v["j_per_iter"] / d0["j_per_iter"] - 1, 5)
+            # the same per-unit in-step timing as `kernels`, under the MBO min-time schedule set (its
+            # collectives launch later and on fewer SMs, so fewer units share their SMs with one)
+            kernels_mbo = None
+            if "mbo_min_time" in runners:
+                try:
+                    ut2 = runners["mbo_min_time"].unit_times_graph(iters=3)
+                    kernels_mbo = {}
+                    for k2, v2 in ut2.items():
+                        u2 = next(u for nm in layer.order for u in layer.programs[nm].units if u.name == k2)
+                        avg2 = statistics.mean(v2)
+                        if u2.kind in ("gemm", "attention"):
+                            kernels_mbo[k2] = {"avg_launch_ms": round(avg2, 4),
+                                               "frac": round(u2.spec.flops / (avg2 / 1e3) / 1e12 / tf_sust, 4)}
+                        else:
+                            kernels_mbo[k2] = {"avg_launch_ms": round(avg2, 4),
+                                               "frac": round(u2.spec.bytes / (avg2 / 1e3) / 1e9 / hbm, 4)}
+                except Exception as ex:  # reported, never fatal
+                    kernels_mbo = f"failed: {type(ex).__name__}: {ex}"
             frontier = {"source": os.path.relpath(mbo_path, ROOT), "optimizer": mb.get("optimizer"),
                         "protocol": mb.get("protocol"), "sets": mb.get("sets"), "executed": ex_rows,
                         "trials": args.sweep_trials, "iterations_per_trial": n_it,
+                        "kernels_mbo_min_time": kernels_mbo,
                         "note": "frequency axis fixed at f_max: every NVML clock knob is refused on this pool "
                                 "(profiles/r2_clock_probe.json)"}
             # the measured profile tables feed the reference's microbatch composition below

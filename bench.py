@@ -464,7 +464,10 @@ def run_kpo(args):
     # interleaved trials of >= --sweep-window s each (device time max over ranks, NVML energy summed).
     frontier = None
     per_part = None
-    mbo_path = os.path.join(ROOT, "profiles", f"r2_mbo_config{args.config}.json")
+    # the 2 s-window run (frontier rows within 0.9% median of their re-measurement), else the first run
+    mbo_path = os.path.join(ROOT, "profiles", f"r2w2_mbo_config{args.config}.json")
+    if not os.path.exists(mbo_path):
+        mbo_path = os.path.join(ROOT, "profiles", f"r2_mbo_config{args.config}.json")
     if args.no_sweep:
         pass
     elif not os.path.exists(mbo_path):

@@ -625,8 +625,13 @@ int fwd_launch(const void* q, const void* k, const void* v, void* o, float* lse,
                                          causal));
     return KPO_OK;
   };
-  static const int variant = getenv("KPO_ATTN_FWD") ? atoi(getenv("KPO_ATTN_FWD")) : 2;
-  if (variant == 2 && D == 128) {
+  // KPO_ATTN_FWD: 2 = the two-Q-tile kernel, 1 = the one-tile kernel, unset = the two-tile kernel
+  // when its grid (q heads x 256-row tiles) fills the GPU, else the one-tile kernel (twice the CTAs:
+  // TP8's 4 heads per rank give 64 two-tile CTAs for 148 SMs)
+  static const int variant = getenv("KPO_ATTN_FWD") ? atoi(getenv("KPO_ATTN_FWD")) : 0;
+  const int sms = num_sms() > 0 ? num_sms() : 148;
+  const bool two_tile = D == 128 && (variant == 2 || (variant == 0 && (int64_t)hq * ((T + 255) / 256) >= sms));
+  if (two_tile) {
     using C2 = Fwd2<D>;
     dim3 grid2((unsigned)hq, (unsigned)((T + 2 * C2::BM - 1) / (2 * C2::BM)));
     auto kern2 = attn_fwd_tc2_kernel<D>;

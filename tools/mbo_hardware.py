@@ -52,6 +52,7 @@ def main():
     ap.add_argument("--table-dir", default="profiles/tables")
     ap.add_argument("--tag", default="r2")
     ap.add_argument("--out", default="gpurun_out/mbo_hardware.json")
+    ap.add_argument("--resume", action="store_true", help="reuse rows of existing tables in --table-dir")
     a = ap.parse_args()
 
     import torch
@@ -97,8 +98,19 @@ def main():
                                     "sm_grid": list(sgrid.values), "protocol": out["protocol"], "seed": a.seed,
                                     "hyper": {"n_init": hyper.n_init, "b_max": hyper.b_max, "batch_k": hyper.batch_k}})
         orig = eng.measure
+        path = os.path.join(a.table_dir, f"{a.tag}_{wl.tag}_{name}.jsonl")
+        prior = None
+        if a.resume and os.path.exists(path):
+            # a table from an interrupted run: its rows answer the optimizer's requests (the replay is
+            # bit-exact, so the run continues exactly where the measurements left off); only
+            # configurations missing from it are measured
+            prior = ProfileTable.read(path)
+            prior_eval = prior.evaluator(Meas)
 
-        def recording(partition, config, gpu_, thermal_, protocol_, state_, table=table):
+        def recording(partition, config, gpu_, thermal_, protocol_, state_, table=table, prior=prior):
+            if prior is not None and config in prior:
+                table.add(config, prior_eval(partition, config), prior.lookup(config).obs)
+                return prior_eval(partition, config)
             m = orig(partition, config, gpu_, thermal_, protocol_, state_)
             table.add(config, m, observation_dict(eng.last))
             return m
@@ -110,7 +122,6 @@ def main():
         wall = time.perf_counter() - t0
         mbo.measure = orig
         space = mbo.enumerate_space(part, gpu, fgrid, sgrid)
-        path = os.path.join(a.table_dir, f"{a.tag}_{wl.tag}_{name}.jsonl")
         table.write(path)
         # replay: the table alone reproduces the optimizer's records bit-exactly
         ev = ProfileTable.read(path).evaluator(Meas)

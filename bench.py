@@ -272,6 +272,44 @@ def run_microbatch(args, wl, eng, gpu, layer, per_part, hbm, tf_sust, torch):
 
 
 # ---------------------------------------------------------------------------- GPU arm
+def dominant_solo(unit, ncta: int, dev, torch, peak: float, bound: str, reps: int = 10, trials: int = 3) -> dict:
+    """The dominant launch unit timed alone: on all SMs, and with `ncta` whole SMs held by
+    `kpo_sm_blocker` (2-CTA clusters, like the collectives) for the whole timed region. Median of
+    `trials` windows of `reps` back-to-back launches, CUDA events on the launching stream."""
+    from paper_2601_17654_b200 import _lib
+
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    compute = torch.cuda.Stream(dev)
+    side = torch.cuda.Stream(dev, priority=-1)
+    launched = torch.cuda.Event()
+    launched.record(side)
+
+    def window(c: int, est_ms: float) -> float:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        if c:
+            spin_ns = int((est_ms * reps * 3 * sms / max(1, sms - c) + 0.5) * 1e6)
+            _lib.call("kpo_sm_blocker", c, spin_ns, launched.cuda_event, side.cuda_stream)
+            compute.wait_event(launched)
+        e0.record(compute)
+        for _ in range(reps):
+            unit.fn(compute)
+        e1.record(compute)
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1) / reps
+
+    window(0, 1.0)
+    est = window(0, 1.0)
+    work = unit.spec.flops / 1e12 if bound == "tensor" else unit.spec.bytes / 1e9
+    out = {"method": "unit alone, median of %d windows x %d launches; 'blocked' holds the default collective's "
+                     "%d whole SMs with kpo_sm_blocker" % (trials, reps, ncta)}
+    for key, c in (("all_sms", 0), ("blocked", ncta)):
+        t = statistics.median(window(c, est) for _ in range(trials))
+        out[key] = {"sms": sms - c, "avg_launch_ms": round(t, 4), "achieved": round(work / (t / 1e3), 1),
+                    "frac": round(work / (t / 1e3) / peak, 4)}
+    return out
+
+
 def run_kpo(args):
     import torch
     import torch.distributed as dist
@@ -316,6 +354,7 @@ def run_kpo(args):
     layer = PartitionedLayer(wl, comm)
     # the bench runs at the unlocked default clock (f_max); the frequency axis is the profiler's
     eng = Engine.for_layer(layer, gpu, clock_control=False)
+    eng.sampler.aux_period_s = 0.01  # clock / power / throttle samples every 10 ms (a K-step region is ~0.1 s)
     run = LayerRunner(layer, eng)
     run.warm()
 
@@ -427,15 +466,32 @@ def run_kpo(args):
         except Exception:
             traffic = None
 
+    # ------------------------------------------------ the dominant unit alone (explains the in-step frac)
+    # timed alone on an idle GPU, and alone with the default collective's CTA count of whole SMs held by
+    # kpo_sm_blocker (the SM budget an overlapped collective takes from it inside the step;
+    # tools/unit_sm_sweep.py does this for every unit and SM count)
+    solo = None
+    try:
+        solo = dominant_solo(dom_unit, eng.default_ncta(), dev, torch,
+                             tf_sust if dom_row["bound"] == "tensor" else hbm, dom_row["bound"])
+    except Exception as ex:  # reported, never fatal
+        solo = f"failed: {type(ex).__name__}: {ex}"
+
     # ------------------------------------------------ energy over a >= 2 s window of back-to-back steps
     n_energy = max(args.steps, int(math.ceil(2.0 / max(ms / 1e3, 1e-4))))
     barrier()
     torch.cuda.synchronize(dev)
     w0 = time.perf_counter()
+    ew0, ew1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ew0.record(st)
     for _ in range(n_energy):
         run.step()
+    ew1.record(st)
     torch.cuda.synchronize(dev)
     w1 = time.perf_counter()
+    # the same steps over the >= 2 s window: the clock the power controller settles at under sw_power_cap
+    # (the K-step timed region may end before the controller has pulled the SM clock down)
+    ms_sustained = max_over_ranks(ew0.elapsed_time(ew1) / n_energy)
     energy_iter = sum_over_ranks(eng.sampler.window_j(w0, w1) / n_energy)
     eclocks = eng.sampler.clocks_summary(w0, w1)
 
@@ -604,6 +660,11 @@ def run_kpo(args):
             "graphs": {"captured": len(eng.exec.graphs), "failures": len(eng.exec.graph_failures),
                        "launch_gate": eng.exec.gate_status},
             "energy_j_per_iter": energy_iter, "energy_window_steps": n_energy,
+            "sustained": {"ms_per_step": round(ms_sustained, 4), "steps": n_energy,
+                          "sm_mhz": eclocks.get("sm_mhz"), "clock_samples": eclocks.get("samples"),
+                          "reasons": eclocks.get("reasons"),
+                          "note": "the same step back to back over the >= 2 s energy window (CUDA events, max "
+                                  "over ranks); value / ms_per_step are the K-step timed region"},
             "avg_power_w": energy_iter / (ms / 1e3) if ms > 0 else None,
             "tflops_per_gpu": iteration_flops(wl) / (ms / 1e3) / 1e12,
             "roofline": {"bound": dom_row["bound"], "kernel": dom, "achieved": dom_row["achieved"],
@@ -613,7 +674,8 @@ def run_kpo(args):
                                        if dom_row["bound"] == "tensor" else f"{peak_src} HBM copy"),
                          "share_of_step": dom_row["share"],
                          "algorithmic_per_launch": dom_unit.spec.flops if dom_row["bound"] == "tensor"
-                         else dom_unit.spec.bytes, "avg_launch_ms": dom_row["avg_launch_ms"]},
+                         else dom_unit.spec.bytes, "avg_launch_ms": dom_row["avg_launch_ms"],
+                         "solo": solo},
             "kernels": kernels,
             "kernels_timing": "CUDA events around each launch unit on the compute stream, " + ut_mode + ", 3 iterations",
             "iteration_roofline": iter_roofline,
@@ -627,6 +689,7 @@ def run_kpo(args):
                     "unpipelined_value": e2e_sync_s},
             "gpu_launches": launches,
             "clocks": {"sm_mhz": clocks.get("sm_mhz") or eclocks.get("sm_mhz"), "sm_max_mhz": eng.nvml.max_sm_clock_mhz(),
+                       "samples": clocks.get("samples", 0), "energy_window_sm_mhz": eclocks.get("sm_mhz"),
                        "reasons": sorted(set(clocks.get("reasons", [])) | set(eclocks.get("reasons", []))),
                        "power_w_max": eclocks.get("power_w_max")},
         }

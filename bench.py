@@ -272,10 +272,13 @@ def run_microbatch(args, wl, eng, gpu, layer, per_part, hbm, tf_sust, torch):
 
 
 # ---------------------------------------------------------------------------- GPU arm
-def dominant_solo(unit, ncta: int, dev, torch, peak: float, bound: str, reps: int = 10, trials: int = 3) -> dict:
+def dominant_solo(unit, ncta: int, dev, torch, peak: float, bound: str, sampler=None, trials: int = 3,
+                  window_ms: float = 50.0, idle_s: float = 1.0) -> dict:
     """The dominant launch unit timed alone: on all SMs, and with `ncta` whole SMs held by
     `kpo_sm_blocker` (2-CTA clusters, like the collectives) for the whole timed region. Median of
-    `trials` windows of `reps` back-to-back launches, CUDA events on the launching stream."""
+    `trials` windows of back-to-back launches (>= `window_ms` each), CUDA events on the launching stream,
+    after `idle_s` of idle GPU so the power-capped clock of the preceding steps has recovered; the SM
+    clock the sampler saw over the windows is reported next to the times."""
     from paper_2601_17654_b200 import _lib
 
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
@@ -298,15 +301,20 @@ def dominant_solo(unit, ncta: int, dev, torch, peak: float, bound: str, reps: in
         torch.cuda.synchronize(dev)
         return e0.elapsed_time(e1) / reps
 
+    reps = 2
     window(0, 1.0)
     est = window(0, 1.0)
+    reps = max(10, int(math.ceil(window_ms / max(est, 1e-3))))
+    time.sleep(idle_s)
     work = unit.spec.flops / 1e12 if bound == "tensor" else unit.spec.bytes / 1e9
-    out = {"method": "unit alone, median of %d windows x %d launches; 'blocked' holds the default collective's "
-                     "%d whole SMs with kpo_sm_blocker" % (trials, reps, ncta)}
+    out = {"method": "unit alone after %.1f s idle, median of %d windows x %d launches; 'blocked' holds the default "
+                     "collective's %d whole SMs with kpo_sm_blocker" % (idle_s, trials, reps, ncta)}
     for key, c in (("all_sms", 0), ("blocked", ncta)):
+        t0 = time.perf_counter()
         t = statistics.median(window(c, est) for _ in range(trials))
+        clk = sampler.clocks_summary(t0, time.perf_counter()) if sampler is not None else {}
         out[key] = {"sms": sms - c, "avg_launch_ms": round(t, 4), "achieved": round(work / (t / 1e3), 1),
-                    "frac": round(work / (t / 1e3) / peak, 4)}
+                    "frac": round(work / (t / 1e3) / peak, 4), "sm_mhz": clk.get("sm_mhz")}
     return out
 
 
@@ -400,12 +408,14 @@ def run_kpo(args):
 
     # ------------------------------------------------ dominant kernel: per-unit times inside the step
     # (right after the timed steps, in the same thermal / power state as the headline number)
+    ut_t0 = time.perf_counter()
     try:
         ut = run.unit_times_graph(iters=3)
         ut_mode = "graph replay"
     except Exception as ex:  # capture unsupported: eager issue with the same events
         ut = run.unit_times(iters=3)
         ut_mode = "eager (" + type(ex).__name__ + ")"
+    ut_clock = eng.sampler.clocks_summary(ut_t0, time.perf_counter())
     # ------------------------------------------------ end to end through the host-buffer entry point
     pin = lambda t: torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
     xs = [pin(a["x"]).copy_(a["x"].cpu()) for a in layer.nb]
@@ -473,7 +483,7 @@ def run_kpo(args):
     solo = None
     try:
         solo = dominant_solo(dom_unit, eng.default_ncta(), dev, torch,
-                             tf_sust if dom_row["bound"] == "tensor" else hbm, dom_row["bound"])
+                             tf_sust if dom_row["bound"] == "tensor" else hbm, dom_row["bound"], eng.sampler)
     except Exception as ex:  # reported, never fatal
         solo = f"failed: {type(ex).__name__}: {ex}"
 
@@ -678,6 +688,7 @@ def run_kpo(args):
                          "solo": solo},
             "kernels": kernels,
             "kernels_timing": "CUDA events around each launch unit on the compute stream, " + ut_mode + ", 3 iterations",
+            "kernels_sm_mhz": ut_clock.get("sm_mhz"),
             "iteration_roofline": iter_roofline,
             "comm": {"mode": "loopback (HBM)" if world == 1 else "cuda-ipc p2p (NVLink)", "units": comm_rows},
             "frontier": frontier,

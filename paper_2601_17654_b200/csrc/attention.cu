@@ -16,7 +16,7 @@ int attn_bwd_tcgen05_main(const void* q, const void* k, const void* v, const voi
                           const float* dvec, float* dq_acc, void* dk, void* dv, int64_t T, int hq, int hkv, int d,
                           int64_t qs, int64_t ks, int64_t vs, int64_t os, int64_t dks, int64_t dvs, float scale,
                           int causal, float* dkv_acc, int split_group, int qsplit_tiles, int qchunks,
-                          cudaStream_t st, const float* rope_table);
+                          int hybrid_tiles, cudaStream_t st, const float* rope_table);
 int attn_bwd_tcgen05_split(const void* q, const void* k, const void* v, const void* o, const void* dout,
                            const float* lse, float* dvec, void* dq, void* dk, void* dv, int64_t T, int hq, int hkv,
                            int d, int64_t qs, int64_t ks, int64_t vs, int64_t os, int64_t dqs, int64_t dks,
@@ -606,8 +606,29 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* o
         if (qsplit_tiles > 0) qchunks = 2;
       }
     }
+    // hybrid grid (grouped mode, 64-query kernel): the first `hybrid` key tiles run one CTA per q head so
+    // that no CTA carries more causal work than the per-SM average (LPT bound); `hybrid` = the first key
+    // tile whose grouped CTA fits under that average.  KPO_ATTN_BWD_HYBRID=n forces n (0 = off).
+    int hybrid = 0;
+    static const int env_h = getenv("KPO_ATTN_BWD_HYBRID") ? atoi(getenv("KPO_ATTN_BWD_HYBRID")) : -1;
+    if (D == 128 && !two_kernels && (variant == 0 || variant == 2) && causal && !split && qchunks == 1 &&
+        hq > hkv) {
+      const int64_t M = (T + 63) / 64, g = hq / hkv;
+      if (env_h >= 0) {
+        hybrid = env_h;
+      } else {
+        int64_t total = 0;
+        for (int64_t j = 0; j < ntiles; ++j) total += g * hkv * std::max<int64_t>(M - 2 * j, 0);
+        const int sms = num_sms() > 0 ? num_sms() : 148;
+        const int64_t avg = (total + sms - 1) / sms;
+        while (hybrid < ntiles && g * (M - 2 * hybrid) > avg) ++hybrid;
+      }
+      if (hybrid >= ntiles) hybrid = 0;
+    }
     // key rows whose dK / dV are reduced through the fp32 accumulators (a prefix of the T rows)
-    const int64_t acc_rows = split ? T : (qchunks > 1 ? std::min<int64_t>(T, (int64_t)qsplit_tiles * 128) : 0);
+    const int64_t acc_rows = split ? T
+                                   : (qchunks > 1 ? std::min<int64_t>(T, (int64_t)qsplit_tiles * 128)
+                                                  : std::min<int64_t>(T, (int64_t)hybrid * 128));
     float* dkv_acc = acc_rows > 0 ? dvec + (int64_t)hq * T : nullptr;
     if (dkv_acc) {
       KPO_CUDA(cudaMemsetAsync(dkv_acc, 0, sizeof(float) * acc_rows * hkv * D, s));
@@ -618,8 +639,8 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* o
                                           dks, dvs, scale, causal, dkv_acc, split ? 1 : 0, qsplit_tiles, qchunks, s,
                                           rope_table)
                  : attn_bwd_tcgen05_main(q, k, v, dout, lse, dvec, dq_acc, dk, dv, T, hq, hkv, D, qs, ks, vs, os,
-                                         dks, dvs, scale, causal, dkv_acc, split ? 1 : 0, qsplit_tiles, qchunks, s,
-                                         rope_table);
+                                         dks, dvs, scale, causal, dkv_acc, split ? 1 : 0, qsplit_tiles, qchunks,
+                                         hybrid, s, rope_table);
     if (st) return st;
     if (dkv_acc) {
       // convert the accumulated rows; the accumulator layout [T][hkv][D] makes them a prefix, so the

@@ -606,25 +606,17 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* o
         if (qsplit_tiles > 0) qchunks = 2;
       }
     }
-    // hybrid grid (grouped mode, 64-query kernel): the first `hybrid` key tiles run one CTA per q head so
-    // that no CTA carries more causal work than the per-SM average (LPT bound); `hybrid` = the first key
-    // tile whose grouped CTA fits under that average.  KPO_ATTN_BWD_HYBRID=n forces n (0 = off).
+    // hybrid grid (grouped mode, 64-query kernel; KPO_ATTN_BWD_HYBRID=n, A/B only): the first n key tiles
+    // run one CTA per q head in a work-ordered 1-D grid, so that no CTA carries more causal work than the
+    // per-SM average (config 1: a grouped tile-0 CTA has 192 of the 171 steps per SM).  Measured slower
+    // at every n on the config-1 and 70B shapes (0.316 -> 0.328 / 0.341 / 0.339 ms for n = 2 / 4 / 6;
+    // 70B 0.854 -> 0.850 / 0.875 / 0.907): the split tiles' extra K / V loads, fp32 dK / dV atomics and
+    // the accumulator memset / conversion launches cost more than the tail they remove.  Off by default.
     int hybrid = 0;
-    static const int env_h = getenv("KPO_ATTN_BWD_HYBRID") ? atoi(getenv("KPO_ATTN_BWD_HYBRID")) : -1;
-    if (D == 128 && !two_kernels && (variant == 0 || variant == 2) && causal && !split && qchunks == 1 &&
-        hq > hkv) {
-      const int64_t M = (T + 63) / 64, g = hq / hkv;
-      if (env_h >= 0) {
-        hybrid = env_h;
-      } else {
-        int64_t total = 0;
-        for (int64_t j = 0; j < ntiles; ++j) total += g * hkv * std::max<int64_t>(M - 2 * j, 0);
-        const int sms = num_sms() > 0 ? num_sms() : 148;
-        const int64_t avg = (total + sms - 1) / sms;
-        while (hybrid < ntiles && g * (M - 2 * hybrid) > avg) ++hybrid;
-      }
-      if (hybrid >= ntiles) hybrid = 0;
-    }
+    static const int env_h = getenv("KPO_ATTN_BWD_HYBRID") ? atoi(getenv("KPO_ATTN_BWD_HYBRID")) : 0;
+    if (env_h > 0 && D == 128 && !two_kernels && (variant == 0 || variant == 2) && causal && !split &&
+        qchunks == 1 && hq > hkv && env_h < ntiles)
+      hybrid = env_h;
     // key rows whose dK / dV are reduced through the fp32 accumulators (a prefix of the T rows)
     const int64_t acc_rows = split ? T
                                    : (qchunks > 1 ? std::min<int64_t>(T, (int64_t)qsplit_tiles * 128)

@@ -29,6 +29,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+UT_ITERS = 10  # iterations of per-unit in-step timing (graph replay with events around every unit)
 METRIC = "iteration time (s) & energy (J/iter) Pareto frontier, 1-8 B200; comm bus GB/s"
 
 
@@ -410,10 +411,10 @@ def run_kpo(args):
     # (right after the timed steps, in the same thermal / power state as the headline number)
     ut_t0 = time.perf_counter()
     try:
-        ut = run.unit_times_graph(iters=3)
+        ut = run.unit_times_graph(iters=UT_ITERS)
         ut_mode = "graph replay"
     except Exception as ex:  # capture unsupported: eager issue with the same events
-        ut = run.unit_times(iters=3)
+        ut = run.unit_times(iters=UT_ITERS)
         ut_mode = "eager (" + type(ex).__name__ + ")"
     ut_clock = eng.sampler.clocks_summary(ut_t0, time.perf_counter())
     # ------------------------------------------------ end to end through the host-buffer entry point
@@ -449,7 +450,7 @@ def run_kpo(args):
     for name in layer.order:
         for u in layer.programs[name].units:
             per_unit.setdefault(u.name, (u, []))
-    totals = {k: sum(v) / 3.0 for k, v in ut.items()}
+    totals = {k: sum(v) / UT_ITERS for k, v in ut.items()}
     step_ms_instr = sum(totals.values())
     dom = max(totals, key=lambda k: totals[k])  # dominant launch unit by share of the step
     kernels = []
@@ -588,7 +589,7 @@ def run_kpo(args):
             kernels_mbo = None
             if "mbo_min_time" in runners:
                 try:
-                    ut2 = runners["mbo_min_time"].unit_times_graph(iters=3)
+                    ut2 = runners["mbo_min_time"].unit_times_graph(iters=UT_ITERS)
                     kernels_mbo = {}
                     for k2, v2 in ut2.items():
                         u2 = next(u for nm in layer.order for u in layer.programs[nm].units if u.name == k2)
@@ -687,7 +688,7 @@ def run_kpo(args):
                          else dom_unit.spec.bytes, "avg_launch_ms": dom_row["avg_launch_ms"],
                          "solo": solo},
             "kernels": kernels,
-            "kernels_timing": "CUDA events around each launch unit on the compute stream, " + ut_mode + ", 3 iterations",
+            "kernels_timing": "CUDA events around each launch unit on the compute stream, " + ut_mode + f", {UT_ITERS} iterations",
             "kernels_sm_mhz": ut_clock.get("sm_mhz"),
             "iteration_roofline": iter_roofline,
             "comm": {"mode": "loopback (HBM)" if world == 1 else "cuda-ipc p2p (NVLink)", "units": comm_rows},

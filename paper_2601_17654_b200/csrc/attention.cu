@@ -16,7 +16,7 @@ int attn_bwd_tcgen05_main(const void* q, const void* k, const void* v, const voi
                           const float* dvec, float* dq_acc, void* dk, void* dv, int64_t T, int hq, int hkv, int d,
                           int64_t qs, int64_t ks, int64_t vs, int64_t os, int64_t dks, int64_t dvs, float scale,
                           int causal, float* dkv_acc, int split_group, int qsplit_tiles, int qchunks,
-                          int hybrid_tiles, cudaStream_t st, const float* rope_table);
+                          cudaStream_t st, const float* rope_table);
 int attn_bwd_tcgen05_split(const void* q, const void* k, const void* v, const void* o, const void* dout,
                            const float* lse, float* dvec, void* dq, void* dk, void* dv, int64_t T, int hq, int hkv,
                            int d, int64_t qs, int64_t ks, int64_t vs, int64_t os, int64_t dqs, int64_t dks,
@@ -606,21 +606,8 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* o
         if (qsplit_tiles > 0) qchunks = 2;
       }
     }
-    // hybrid grid (grouped mode, 64-query kernel; KPO_ATTN_BWD_HYBRID=n, A/B only): the first n key tiles
-    // run one CTA per q head in a work-ordered 1-D grid, so that no CTA carries more causal work than the
-    // per-SM average (config 1: a grouped tile-0 CTA has 192 of the 171 steps per SM).  Measured slower
-    // at every n on the config-1 and 70B shapes (0.316 -> 0.328 / 0.341 / 0.339 ms for n = 2 / 4 / 6;
-    // 70B 0.854 -> 0.850 / 0.875 / 0.907): the split tiles' extra K / V loads, fp32 dK / dV atomics and
-    // the accumulator memset / conversion launches cost more than the tail they remove.  Off by default.
-    int hybrid = 0;
-    static const int env_h = getenv("KPO_ATTN_BWD_HYBRID") ? atoi(getenv("KPO_ATTN_BWD_HYBRID")) : 0;
-    if (env_h > 0 && D == 128 && !two_kernels && (variant == 0 || variant == 2) && causal && !split &&
-        qchunks == 1 && hq > hkv && env_h < ntiles)
-      hybrid = env_h;
     // key rows whose dK / dV are reduced through the fp32 accumulators (a prefix of the T rows)
-    const int64_t acc_rows = split ? T
-                                   : (qchunks > 1 ? std::min<int64_t>(T, (int64_t)qsplit_tiles * 128)
-                                                  : std::min<int64_t>(T, (int64_t)hybrid * 128));
+    const int64_t acc_rows = split ? T : (qchunks > 1 ? std::min<int64_t>(T, (int64_t)qsplit_tiles * 128) : 0);
     float* dkv_acc = acc_rows > 0 ? dvec + (int64_t)hq * T : nullptr;
     if (dkv_acc) {
       KPO_CUDA(cudaMemsetAsync(dkv_acc, 0, sizeof(float) * acc_rows * hkv * D, s));
@@ -631,8 +618,8 @@ static int bwd_launch(const void* q, const void* k, const void* v, const void* o
                                           dks, dvs, scale, causal, dkv_acc, split ? 1 : 0, qsplit_tiles, qchunks, s,
                                           rope_table)
                  : attn_bwd_tcgen05_main(q, k, v, dout, lse, dvec, dq_acc, dk, dv, T, hq, hkv, D, qs, ks, vs, os,
-                                         dks, dvs, scale, causal, dkv_acc, split ? 1 : 0, qsplit_tiles, qchunks,
-                                         hybrid, s, rope_table);
+                                         dks, dvs, scale, causal, dkv_acc, split ? 1 : 0, qsplit_tiles, qchunks, s,
+                                         rope_table);
     if (st) return st;
     if (dkv_acc) {
       // convert the accumulated rows; the accumulator layout [T][hkv][D] makes them a prefix, so the

@@ -703,7 +703,7 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
                        const float* __restrict__ lse, const float* __restrict__ dvec, float* __restrict__ dq_acc,
                        __nv_bfloat16* __restrict__ dk, __nv_bfloat16* __restrict__ dv, int T, int hq, int hkv,
                        int64_t dks, int64_t dvs, float scale, int causal, float* __restrict__ dkv_acc,
-                       int split_group, int qsplit_tiles, int hybrid_tiles,
+                       int split_group, int qsplit_tiles,
                        int ablate, const float2* __restrict__ rope_cs) {
   // rope_cs != nullptr: dK leaves inverse-rotated (the gradient w.r.t. the un-rotated k), the fused
   // backward of the QKV GEMM's rotary epilogue; dQ is rotated by the dq conversion kernel
@@ -732,37 +732,13 @@ __global__ void __launch_bounds__(Bwd<D>::THREADS, 1)
   float* stat = reinterpret_cast<float*>(smem + C::OFF_STAT);  // [2][lse2 64 | dvec 64]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int total_m = (T + BM - 1) / BM;
-  // CTA -> (key tile, head): the 2-D grid is (heads, key tiles), early key tiles (the most causal work)
-  // dispatched first.  hybrid_tiles > 0 (grouped mode, causal): a 1-D grid in which the first
-  // hybrid_tiles key tiles run one CTA per q head (their dK / dV meet in the fp32 accumulators) and the
-  // others one CTA per kv head, ordered by causal work, heaviest first, so the in-order block dispatch
-  // is a longest-first schedule whose largest item no longer exceeds the per-SM average (config 1: a
-  // grouped tile-0 CTA carries 192 of the 171 steps per SM)
-  int nblk = blockIdx.y, head = blockIdx.x;
-  bool split = split_group != 0;
-  if (hybrid_tiles > 0) {
-    const int g = hq / hkv, ntiles = (T + BN - 1) / BN, id = blockIdx.x;
-    int jg = hybrid_tiles, js = 0, base = 0;
-    for (;;) {
-      const int wg = jg < ntiles ? g * (total_m - 2 * jg) : -1;  // causal steps of the next grouped tile
-      const int ws = js < hybrid_tiles ? total_m - 2 * js : -1;  // ... of the next per-q-head tile
-      if (wg < 0 && ws < 0) return;  // past the last item (before any barrier / TMEM use)
-      if (wg >= ws) {
-        if (id < base + hkv) { nblk = jg; head = id - base; split = false; break; }
-        base += hkv;
-        ++jg;
-      } else {
-        if (id < base + hq) { nblk = js; head = id - base; split = true; break; }
-        base += hq;
-        ++js;
-      }
-    }
-  }
+  const int nblk = blockIdx.y;  // early key tiles carry the most causal work: dispatched first
+  const bool split = split_group != 0;
   const int group = split ? 1 : hq / hkv;
-  const int h_first = split ? head : head * (hq / hkv);
-  const int kvh = split ? head / (hq / hkv) : head;
+  const int h_first = split ? (int)blockIdx.x : (int)blockIdx.x * (hq / hkv);
+  const int kvh = split ? (int)blockIdx.x / (hq / hkv) : (int)blockIdx.x;
   const int n0 = nblk * BN;
+  const int total_m = (T + BM - 1) / BM;
   int m_start = causal ? n0 / BM : 0, m_end = total_m;
   // query chunks (blockIdx.z) for the first qsplit_tiles key tiles (all of them in split-group mode):
   // this CTA takes the query tiles of chunk z, so the long causal key tiles are spread over several
@@ -2145,17 +2121,13 @@ template <int D>
 int bwd_launch(const void* q, const void* k, const void* v, const void* dout, const float* lse, const float* dvec,
                float* dq_acc, void* dk, void* dv, int64_t T, int hq, int hkv, int64_t qs, int64_t ks, int64_t vs,
                int64_t os, int64_t dks, int64_t dvs, float scale, int causal, float* dkv_acc, int split_group,
-               int qsplit_tiles, int qchunks, int hybrid_tiles, cudaStream_t st,
+               int qsplit_tiles, int qchunks, cudaStream_t st,
                const float* rope_table) {
   // head_dim 128: the 64-query kernel (measured faster: its dQ^T has TMEM of its own, so the drain
   // and the dQ reduce-adds stay off the critical path; the 128-query kernel must alias dQ with dP^T
   // and stage through the dS^T buffer).  head_dim 64: the 128-query kernel (3.4x the mma.sync one).
   static const int variant = getenv("KPO_ATTN_BWD") ? atoi(getenv("KPO_ATTN_BWD")) : (D == 64 ? 3 : 2);
   if (variant == 3 || D == 64) {  // 128-query steps
-    if (hybrid_tiles > 0) {
-      set_error("attn_bwd: the hybrid grid is a 64-query-kernel mode");
-      return KPO_ERR_INVALID;
-    }
     using C3 = Bwd3<D>;
     CUtensorMap mq, mk, mv, mo, mdq;
     int e;
@@ -2196,16 +2168,9 @@ int bwd_launch(const void* q, const void* k, const void* v, const void* dout, co
   }
   const int ntiles = (int)((T + C::BN - 1) / C::BN);
   dim3 grid((unsigned)(split_group ? hq : hkv), (unsigned)ntiles, (unsigned)(qchunks > 1 ? qchunks : 1));
-  if (hybrid_tiles > 0) {
-    if (split_group || qchunks > 1 || !causal || hybrid_tiles >= ntiles) {
-      set_error("attn_bwd: the hybrid grid needs grouped mode, causal, no query chunks and fewer tiles than T / 128");
-      return KPO_ERR_INVALID;
-    }
-    grid = dim3((unsigned)(hybrid_tiles * hq + (ntiles - hybrid_tiles) * hkv), 1, 1);
-  }
   KPO_CUDA(::kpo::pdl_launch(attn_bwd_tc_kernel<D>, grid, C::THREADS, C::SMEM, st, mq, mk, mv, mo, mdq, lse, dvec, dq_acc, (__nv_bfloat16*)dk,
                                                           (__nv_bfloat16*)dv, (int)T, hq, hkv, dks, dvs, scale, causal,
-                                                          dkv_acc, split_group, qsplit_tiles, hybrid_tiles,
+                                                          dkv_acc, split_group, qsplit_tiles,
                                                           getenv("KPO_ATTN_BWD_ABLATE") ? atoi(getenv("KPO_ATTN_BWD_ABLATE")) : 0,
                                                           reinterpret_cast<const float2*>(rope_table)));
   KPO_LAUNCH_CHECK();
@@ -2242,23 +2207,21 @@ int attn_bwd_tcgen05_main(const void* q, const void* k, const void* v, const voi
                           const float* dvec, float* dq_acc, void* dk, void* dv, int64_t T, int hq, int hkv, int d,
                           int64_t qs, int64_t ks, int64_t vs, int64_t os, int64_t dks, int64_t dvs, float scale,
                           int causal, float* dkv_acc, int split_group, int qsplit_tiles, int qchunks,
-                          int hybrid_tiles, cudaStream_t st, const float* rope_table) {
+                          cudaStream_t st, const float* rope_table) {
   if (d == 64) {
     if (rope_table != nullptr) {
       set_error("attn_bwd tcgen05 path: the fused inverse rotary needs head_dim 128");
       return KPO_ERR_UNSUPPORTED;
     }
     return attn_tc::bwd_launch<64>(q, k, v, dout, lse, dvec, dq_acc, dk, dv, T, hq, hkv, qs, ks, vs, os, dks, dvs,
-                                   scale, causal, dkv_acc, split_group, qsplit_tiles, qchunks, hybrid_tiles, st,
-                                   rope_table);
+                                   scale, causal, dkv_acc, split_group, qsplit_tiles, qchunks, st, rope_table);
   }
   if (d != 128) {
     set_error("attn_bwd tcgen05 path needs head_dim 64 or 128");
     return KPO_ERR_UNSUPPORTED;
   }
   return attn_tc::bwd_launch<128>(q, k, v, dout, lse, dvec, dq_acc, dk, dv, T, hq, hkv, qs, ks, vs, os, dks, dvs,
-                                  scale, causal, dkv_acc, split_group, qsplit_tiles, qchunks, hybrid_tiles, st,
-                                  rope_table);
+                                  scale, causal, dkv_acc, split_group, qsplit_tiles, qchunks, st, rope_table);
 }
 
 }  // namespace kpo

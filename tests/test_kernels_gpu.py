@@ -319,15 +319,13 @@ def test_attention_bwd_rope_fused(cuda, T, hq, hkv):
 @pytest.mark.parametrize("shape", ["1024:6:2", "2048:4:1", "512:8:8:64"])
 def test_attention_bwd_variants_match_reference(cuda, shape):
     """Every attention-backward implementation (selected per process by KPO_ATTN_BWD: 2 = the 64-query
-    single kernel, 3 = the 128-query single kernel, 4 = the dQ + dK/dV two-kernel default; 2+h3 = the
-    64-query kernel on the hybrid grid, KPO_ATTN_BWD_HYBRID=3) against the same torch fp32 reference
-    (tools/attn_bwd_ab.py runs each in its own process)."""
+    single kernel, 3 = the 128-query single kernel, 4 = the dQ + dK/dV two-kernel default) against the
+    same torch fp32 reference (tools/attn_bwd_ab.py runs each in its own process)."""
     import json
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    # "2+h3": the 64-query kernel on the hybrid grid, first 3 key tiles one CTA per q head (grouped shapes)
-    variants = "3,4" if shape.endswith(":64") else "2,3,4,2+h3"
+    variants = "3,4" if shape.endswith(":64") else "2,3,4"
     r = subprocess.run([sys.executable, os.path.join(root, "tools", "attn_bwd_ab.py"), "--variants", variants,
                         "--shapes", shape, "--reps", "2"], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
@@ -355,24 +353,3 @@ def test_attention_bwd_two_kernel_path_is_deterministic(cuda):
         shas.append(line["sha"])
     assert shas[0] == shas[1], shas
 
-
-def test_attention_bwd_hybrid_grid_config1_shape(cuda):
-    """The hybrid grid (KPO_ATTN_BWD_HYBRID, an A/B mode measured slower, off by default) at the config-1
-    shape (T 4096, 24 / 8 heads): off, 4 and 8 split key tiles all match the torch fp32 reference; dq / dk /
-    dv of the three agree closely (only the fp32 reduction order of the split tiles' dK / dV differs)."""
-    import json
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, os.path.join(root, "tools", "attn_bwd_ab.py"), "--variants", "2,2+h4,2+h8",
-                        "--shapes", "4096:24:8", "--reps", "2"], capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stderr[-2000:]
-    res = json.loads(r.stdout.strip().splitlines()[-1])
-    assert len(res) == 3
-    for key, v in res.items():
-        assert "rel" in v, (key, v)
-        assert all(e < 2e-2 for e in v["rel"].values()), (key, v)
-    base = res["4096:24:8/v2"]["rel"]
-    for key, v in res.items():
-        for g in ("dq", "dk", "dv"):
-            assert abs(v["rel"][g] - base[g]) < 1e-3, (key, g, v["rel"][g], base[g])

@@ -87,15 +87,12 @@ def main():
             # "3+dv": variant 3 with the dV-before-dP MMA order (KPO_ATTN_BWD3_DVFIRST=1)
             # "2@base": variant 2 of the library at tools/ab/libkpo_base.so (an older build, same-box A/B)
             # "2+f2": also KPO_ATTN_FWD=2 (the forward variant the child times)
-            # "2+h4": KPO_ATTN_BWD_HYBRID=4 (first 4 key tiles one CTA per q head; h0 = off)
             var_b, *opts = var.split("+")
             v, _, lib = var_b.partition("@")
             env = dict(os.environ, KPO_ATTN_BWD=v)
             for o in opts:
                 if o.startswith("f"):
                     env["KPO_ATTN_FWD"] = o[1:]
-                elif o.startswith("h"):
-                    env["KPO_ATTN_BWD_HYBRID"] = o[1:]
             if lib:
                 env["KPO_LIB_PATH"] = os.path.join(ROOT, "tools", "ab", f"libkpo_{lib}.so")
             r = subprocess.run([sys.executable, __file__, "--child", shape, "--reps", str(a.reps)], env=env,

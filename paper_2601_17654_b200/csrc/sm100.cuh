@@ -18,7 +18,10 @@ __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
 // Watchdog: a wait that has not completed after 2^26 try_wait rounds (seconds; every legitimate wait
 // here is well under a millisecond) traps, so a pipeline bug fails the launch instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  uint32_t done = 0, spins = 0;
+  uint32_t done = 0;
+#ifndef KPO_NO_MBAR_WATCHDOG
+  uint32_t spins = 0;
+#endif
   while (!done) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -27,7 +30,9 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "=r"(done)
         : "r"(bar), "r"(parity)
         : "memory");
+#ifndef KPO_NO_MBAR_WATCHDOG
     if (!done && ++spins == (1u << 26)) __trap();
+#endif
   }
 }
 // non-blocking probe of an mbarrier phase

@@ -15,11 +15,14 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
 }
-// Watchdog: a wait that has not completed after 2^26 try_wait rounds (seconds; every legitimate wait
-// here is well under a millisecond) traps, so a pipeline bug fails the launch instead of hanging the GPU.
+// Watchdog (debug builds, -DKPO_MBAR_WATCHDOG): a wait that has not completed after 2^26 try_wait rounds
+// (seconds; every legitimate wait here is well under a millisecond) traps, so a pipeline bug under
+// development fails the launch instead of hanging the GPU.  Off in the product build: its per-round
+// counter made the attention backward 9% slower (same-box A/B, profiles/r2s_watchdog_ab.log:
+// 0.317 -> 0.290 ms at config 1, 0.849 -> 0.786 ms at 70B; forward and GEMMs unchanged).
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t done = 0;
-#ifndef KPO_NO_MBAR_WATCHDOG
+#ifdef KPO_MBAR_WATCHDOG
   uint32_t spins = 0;
 #endif
   while (!done) {
@@ -30,7 +33,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "=r"(done)
         : "r"(bar), "r"(parity)
         : "memory");
-#ifndef KPO_NO_MBAR_WATCHDOG
+#ifdef KPO_MBAR_WATCHDOG
     if (!done && ++spins == (1u << 26)) __trap();
 #endif
   }

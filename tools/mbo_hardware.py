@@ -185,6 +185,13 @@ def main():
                     [min(pts, key=lambda p: p[1]["repeat_time_ms"][0])], key=lambda p: p[1]["repeat_total_j"][0])}
         for label, fn in pick.items():
             sets[label] = {n_: fn(frontiers[n_], n_)[0] for n_ in layer.order}
+        # the reference's pruning can leave the default schedule out of a partition's space (TP8 forward
+        # attention: the space is the single sequential candidate, 75% slower than the default overlap);
+        # this set adds the measured default to every partition's candidates before the iso-time pick
+        with_dflt = {n_: list(frontiers[n_]) + [(dflt[n_], {"repeat_time_ms": [dflt_meas[n_][0]],
+                                                           "repeat_total_j": [dflt_meas[n_][1]]})]
+                     for n_ in layer.order}
+        sets["mbo_iso_time_with_default"] = {n_: pick["mbo_iso_time"](with_dflt[n_], n_)[0] for n_ in layer.order}
         out["default_partition_measurements"] = {n_: {"time_ms": v[0], "total_j": v[1]} for n_, v in dflt_meas.items()}
         out["sets"] = {k: {n_: f"{c.timing.encode()}@{c.sm_alloc}@{c.frequency_mhz:g}" for n_, c in s.items()}
                        for k, s in sets.items()}

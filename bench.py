@@ -532,7 +532,11 @@ def run_kpo(args):
     frontier = None
     per_part = None
     # the 2 s-window run (frontier rows within 0.9% median of their re-measurement), else the first run
-    mbo_path = os.path.join(ROOT, "profiles", f"r2w2_mbo_config{args.config}.json")
+    # (config 1: the same tables replayed with the final kernels and the set that keeps the default among
+    # each partition's candidates, r2x)
+    mbo_path = os.path.join(ROOT, "profiles", f"r2x_mbo_config{args.config}.json")
+    if not os.path.exists(mbo_path):
+        mbo_path = os.path.join(ROOT, "profiles", f"r2w2_mbo_config{args.config}.json")
     if not os.path.exists(mbo_path):
         mbo_path = os.path.join(ROOT, "profiles", f"r2_mbo_config{args.config}.json")
     if args.no_sweep:

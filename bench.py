@@ -391,6 +391,21 @@ def run_kpo(args):
     for _ in range(max(3, args.warmup)):
         run.step()
     torch.cuda.synchronize(dev)
+    # ------------------------------------------------ dominant kernel: per-unit times inside the step
+    # (right before the timed steps, after the warm-up: the SM clock is then where the timed region
+    # starts, so the per-unit fractions and `value` share a clock state; measured after the timed region
+    # the power controller had already pulled the clock down by 200-500 MHz and the fractions moved with it)
+    ut_t0 = time.perf_counter()
+    try:
+        ut = run.unit_times_graph(iters=UT_ITERS)
+        ut_mode = "graph replay"
+    except Exception as ex:  # capture unsupported: eager issue with the same events
+        ut = run.unit_times(iters=UT_ITERS)
+        ut_mode = "eager (" + type(ex).__name__ + ")"
+    ut_clock = eng.sampler.clocks_summary(ut_t0, time.perf_counter())
+    for _ in range(2):  # back on the step's own graphs before the timed region
+        run.step()
+    torch.cuda.synchronize(dev)
     # ------------------------------------------------ timed region (device time, max over ranks)
     barrier()
     torch.cuda.synchronize(dev)
@@ -407,16 +422,6 @@ def run_kpo(args):
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     clocks = eng.sampler.clocks_summary(t0, t1)
 
-    # ------------------------------------------------ dominant kernel: per-unit times inside the step
-    # (right after the timed steps, in the same thermal / power state as the headline number)
-    ut_t0 = time.perf_counter()
-    try:
-        ut = run.unit_times_graph(iters=UT_ITERS)
-        ut_mode = "graph replay"
-    except Exception as ex:  # capture unsupported: eager issue with the same events
-        ut = run.unit_times(iters=UT_ITERS)
-        ut_mode = "eager (" + type(ex).__name__ + ")"
-    ut_clock = eng.sampler.clocks_summary(ut_t0, time.perf_counter())
     # ------------------------------------------------ end to end through the host-buffer entry point
     pin = lambda t: torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
     xs = [pin(a["x"]).copy_(a["x"].cpu()) for a in layer.nb]
